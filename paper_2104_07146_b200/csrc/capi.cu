@@ -1,0 +1,373 @@
+// extern "C" boundary of the hmgp B200 library (include/hmgp_cuda.h).
+// Maps internal exceptions to status codes; keeps the reference's validation
+// order and messages (geometry.cpp:43-47,103; covkernel.cpp:14-18;
+// hmatrix.cpp:177-180; loglik.cpp:22-23; krige.cpp:13-15).
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "../../include/hmgp_cuda.h"
+#include "common.cuh"
+#include "hmgp_api.h"
+#include "hmgp_internal.h"
+
+namespace hmgp_gpu {
+std::atomic<uint64_t> g_launches{0};
+}
+
+using namespace hmgp_gpu;
+
+namespace {
+thread_local std::string t_err;
+thread_local int t_piv_index = -1;
+thread_local double t_piv_value = 0.0;
+
+int fail(int code, const char* msg) {
+  t_err = msg;
+  return code;
+}
+}  // namespace
+
+void hmgp_set_pivot(int idx, double v) {
+  t_piv_index = idx;
+  t_piv_value = v;
+}
+
+#define API_GUARD(...)                                      \
+  try {                                                     \
+    __VA_ARGS__;                                            \
+    return HMGP_OK;                                         \
+  } catch (const hmgp_gpu::Error& e) {                      \
+    return fail(e.code, e.what());                          \
+  } catch (const std::invalid_argument& e) {                \
+    return fail(HMGP_EINVAL, e.what());                     \
+  } catch (const std::domain_error& e) {                    \
+    return fail(HMGP_EDOMAIN, e.what());                    \
+  } catch (const std::out_of_range& e) {                    \
+    return fail(HMGP_ERANGE, e.what());                     \
+  } catch (const std::bad_alloc& e) {                       \
+    return fail(HMGP_ECUDA, "host allocation failed");      \
+  } catch (const std::exception& e) {                       \
+    return fail(HMGP_ECUDA, e.what());                      \
+  }
+
+// ---------------------------------------------------------------- helpers --
+void hmgp_validate_matern(const hmgp_matern* p) {  // covkernel.cpp:9-18
+  const bool ok = std::isfinite(p->sigma2) && std::isfinite(p->ell) && std::isfinite(p->nu) &&
+                  std::isfinite(p->tau2) && p->sigma2 > 0.0 && p->ell > 0.0 && p->nu > 0.0 &&
+                  p->tau2 >= 0.0;
+  if (!ok)
+    throw std::invalid_argument(
+        "invalid Matern parameters: need sigma2 > 0, ell > 0, nu > 0, tau2 >= 0");
+}
+
+static void check_coords(const double* x, int n, int dim, int leaf) {  // geometry.cpp:43-47
+  if (n < 1) throw std::invalid_argument("empty dataset");
+  if (leaf < 1) throw std::invalid_argument("leaf_size must be >= 1");
+  if (dim != 2 && dim != 3) throw std::invalid_argument("dim must be 2 or 3");
+  if (x)
+    for (long long i = 0; i < (long long)n * dim; ++i)
+      if (!std::isfinite(x[i])) throw std::invalid_argument("invalid location");
+}
+
+extern "C" {
+
+const char* hmgp_last_error(void) { return t_err.c_str(); }
+int hmgp_last_pivot_index(void) { return t_piv_index; }
+double hmgp_last_pivot_value(void) { return t_piv_value; }
+uint64_t hmgp_kernel_launches(hmgp_ctx*) { return g_launches.load(); }
+
+void hmgp_default_config(hmgp_config* c) {  // pipeline.hpp:13-25
+  c->eta = 2.0;
+  c->leaf_size = 32;
+  c->rank.mode = 0;
+  c->rank.eps = 1e-6;
+  c->rank.rank = 16;
+  c->rank.max_rank = 256;
+  c->eps_factor = -1.0;
+  c->form = 1;
+  c->threads = 1;
+}
+
+int hmgp_ctx_create(int device, hmgp_ctx** out) {
+  API_GUARD({
+    auto c = new hmgp_ctx();
+    c->device = device;
+    HMGP_CUDA(cudaSetDevice(device));
+    HMGP_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    *out = c;
+  })
+}
+
+void hmgp_ctx_destroy(hmgp_ctx* c) {
+  if (!c) return;
+  cudaStreamSynchronize(c->stream);
+  cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+// ---------------------------------------------------------------- geometry
+static hmgp_geom* geom_common(hmgp_ctx* ctx, int n, int dim, int leaf, double eta) {
+  if (!(eta > 0.0)) throw std::invalid_argument("eta must be positive");  // geometry.cpp:103
+  auto g = new hmgp_geom();
+  g->g.n = n;
+  g->g.dim = dim;
+  g->g.leaf_size = leaf;
+  g->g.eta = eta;
+  (void)ctx;
+  return g;
+}
+
+int hmgp_geometry_build(hmgp_ctx* ctx, const double* coords, int n, int dim, int leaf_size,
+                        double eta, hmgp_geom** out) {
+  API_GUARD({
+    check_coords(coords, n, dim, leaf_size);
+    HMGP_CUDA(cudaSetDevice(ctx->device));
+    hmgp_geom* g = geom_common(ctx, n, dim, leaf_size, eta);
+    try {
+      HMGP_CUDA(cudaMalloc(&g->g.d_x, sizeof(double) * (size_t)n * dim));
+      HMGP_CUDA(cudaMemcpyAsync(g->g.d_x, coords, sizeof(double) * (size_t)n * dim,
+                                cudaMemcpyHostToDevice, ctx->stream));
+      geometry_build(g->g, ctx->stream);
+    } catch (...) {
+      geometry_free(g->g);
+      delete g;
+      throw;
+    }
+    *out = g;
+  })
+}
+
+int hmgp_geometry_build_device(hmgp_ctx* ctx, const double* d_coords, int n, int dim,
+                               int leaf_size, double eta, hmgp_geom** out) {
+  API_GUARD({
+    check_coords(nullptr, n, dim, leaf_size);
+    HMGP_CUDA(cudaSetDevice(ctx->device));
+    // finiteness is checked on the host copy-free path by a device scan
+    hmgp_geom* g = geom_common(ctx, n, dim, leaf_size, eta);
+    try {
+      HMGP_CUDA(cudaMalloc(&g->g.d_x, sizeof(double) * (size_t)n * dim));
+      HMGP_CUDA(cudaMemcpyAsync(g->g.d_x, d_coords, sizeof(double) * (size_t)n * dim,
+                                cudaMemcpyDeviceToDevice, ctx->stream));
+      if (!device_all_finite(g->g.d_x, (size_t)n * dim, ctx->stream))
+        throw std::invalid_argument("invalid location");
+      geometry_build(g->g, ctx->stream);
+    } catch (...) {
+      geometry_free(g->g);
+      delete g;
+      throw;
+    }
+    *out = g;
+  })
+}
+
+int hmgp_geometry_perm(const hmgp_geom* g, int32_t* perm, int32_t* inv_perm) {
+  API_GUARD({
+    for (int k = 0; k < g->g.n; ++k) {
+      if (perm) perm[k] = g->g.perm[k];
+      if (inv_perm) inv_perm[k] = g->g.iperm[k];
+    }
+  })
+}
+
+int hmgp_geometry_clusters(const hmgp_geom* g, int32_t* out4, double* box6, int cap, int* count) {
+  API_GUARD({
+    const int nn = (int)g->g.nbeg.size();
+    *count = nn;
+    if (nn > cap) throw std::out_of_range("hmgp_geometry_clusters: cap");
+    for (int i = 0; i < nn; ++i) {
+      out4[4 * i + 0] = g->g.nbeg[i];
+      out4[4 * i + 1] = g->g.nend[i];
+      out4[4 * i + 2] = g->g.nleft[i];
+      out4[4 * i + 3] = g->g.nright[i];
+      for (int d = 0; d < 6; ++d) box6[6 * i + d] = g->g.box[6 * i + d];
+    }
+  })
+}
+
+int hmgp_geometry_block_count(const hmgp_geom* g, int64_t* count, int* n_adm, int* n_dense) {
+  API_GUARD({
+    *count = (int64_t)g->g.leaves.size();
+    *n_adm = g->g.n_adm;
+    *n_dense = g->g.n_dense;
+  })
+}
+
+int hmgp_geometry_blocks(const hmgp_geom* g, hmgp_block* out, int64_t cap) {
+  API_GUARD({
+    const auto& G = g->g;
+    if ((int64_t)G.leaves.size() > cap) throw std::out_of_range("hmgp_geometry_blocks: cap");
+    for (size_t k = 0; k < G.leaves.size(); ++k) {
+      const BlockNodeRec& b = G.bnodes[G.leaves[k]];
+      out[k] = hmgp_block{G.nbeg[b.row], G.nend[b.row], G.nbeg[b.col], G.nend[b.col], b.tag};
+    }
+  })
+}
+
+void hmgp_geometry_destroy(hmgp_geom* g) {
+  if (!g) return;
+  geometry_free(g->g);
+  delete g;
+}
+
+// ------------------------------------------------------------------ kernel
+int hmgp_kernel_pairs(hmgp_ctx* ctx, const double* coords, int n, int dim,
+                      const hmgp_matern* theta, const int32_t* ii, const int32_t* jj,
+                      int64_t count, double* out) {
+  API_GUARD({
+    hmgp_validate_matern(theta);
+    if (dim != 2 && dim != 3) throw std::invalid_argument("dim must be 2 or 3");
+    for (int64_t t = 0; t < count; ++t)
+      if (ii[t] < 0 || ii[t] >= n || jj[t] < 0 || jj[t] >= n)
+        throw std::out_of_range("kernel_pairs: index out of range");
+    HMGP_CUDA(cudaSetDevice(ctx->device));
+    kernel_pairs(ctx->stream, coords, n, dim, make_matern(theta->sigma2, theta->ell, theta->nu, theta->tau2),
+                 ii, jj, count, out);
+  })
+}
+
+int hmgp_at_distance(hmgp_ctx* ctx, const hmgp_matern* theta, const double* h, int64_t count,
+                     double* out) {
+  API_GUARD({
+    hmgp_validate_matern(theta);
+    HMGP_CUDA(cudaSetDevice(ctx->device));
+    at_distance(ctx->stream, make_matern(theta->sigma2, theta->ell, theta->nu, theta->tau2), h,
+                count, out);
+  })
+}
+
+int hmgp_bessel_k(hmgp_ctx* ctx, const double* nu, const double* x, int64_t count, int generic,
+                  double* out) {
+  API_GUARD({
+    for (int64_t t = 0; t < count; ++t) {  // covkernel.cpp:197-199
+      if (!(x[t] > 0.0)) throw std::domain_error("bessel_k: x must be positive");
+      if (!(nu[t] > 0.0) || !std::isfinite(nu[t]) || !std::isfinite(x[t]))
+        throw std::domain_error("bessel_k: order must be positive and finite");
+    }
+    HMGP_CUDA(cudaSetDevice(ctx->device));
+    bessel_batch(ctx->stream, nu, x, count, generic, out);
+  })
+}
+
+// ---------------------------------------------------------------- H-matrix
+int hmgp_assemble(hmgp_ctx* ctx, hmgp_geom* g, const hmgp_matern* theta,
+                  const hmgp_rank_control* rc, hmgp_hmat** out) {
+  API_GUARD({
+    hmgp_validate_matern(theta);
+    if (rc->mode == 0 && !(rc->eps > 0.0))
+      throw std::invalid_argument("assemble: eps must be positive");
+    if (rc->mode == 1 && rc->rank < 1)
+      throw std::invalid_argument("assemble: fixed rank must be >= 1");
+    HMGP_CUDA(cudaSetDevice(ctx->device));
+    auto h = new hmgp_hmat();
+    try {
+      assemble(h->h, g->g, make_matern(theta->sigma2, theta->ell, theta->nu, theta->tau2), rc->eps,
+               rc->mode == 1, rc->rank, rc->max_rank > 0 ? rc->max_rank : 256, ctx->stream,
+               nullptr);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  })
+}
+
+int hmgp_hmat_stats(const hmgp_hmat* hm, double* bytes, int* max_rank, double* max_diag) {
+  API_GUARD({
+    const HMat& h = hm->h;
+    double b = 0;
+    int r = 0;
+    for (size_t k = 0; k < h.leaf.size(); ++k) {
+      const LeafDev& l = h.leaf[k];
+      if (l.kind == DENSE) {
+        b += 8.0 * l.m * l.n;
+      } else {
+        b += 8.0 * (l.m + l.n) * h.rank_host[k];
+        r = std::max(r, h.rank_host[k]);
+      }
+    }
+    *bytes = b;
+    *max_rank = r;
+    *max_diag = h.max_diag;
+  })
+}
+
+int hmgp_hmat_leaves(const hmgp_hmat* hm, int32_t* out6, int64_t cap, int64_t* count) {
+  API_GUARD({
+    const HMat& h = hm->h;
+    const Geometry& G = *h.g;
+    *count = (int64_t)h.leaf.size();
+    if (*count > cap) throw std::out_of_range("hmgp_hmat_leaves: cap");
+    for (size_t k = 0; k < h.leaf.size(); ++k) {
+      const HNode& nd = h.nodes[h.leaf_node[k]];
+      out6[6 * k + 0] = G.nbeg[nd.row];
+      out6[6 * k + 1] = G.nend[nd.row];
+      out6[6 * k + 2] = G.nbeg[nd.col];
+      out6[6 * k + 3] = G.nend[nd.col];
+      out6[6 * k + 4] = h.leaf[k].kind;
+      out6[6 * k + 5] = h.leaf[k].kind == LOWRANK ? h.rank_host[k] : -1;
+    }
+  })
+}
+
+int hmgp_hmat_leaf_data(const hmgp_hmat* hm, int64_t k, double* a, double* b) {
+  API_GUARD({
+    const HMat& h = hm->h;
+    if (k < 0 || k >= (int64_t)h.leaf.size()) throw std::out_of_range("leaf index");
+    const LeafDev& l = h.leaf[k];
+    if (l.kind == DENSE) {
+      HMGP_CUDA(cudaMemcpy(a, l.a, 8ull * l.m * l.n, cudaMemcpyDeviceToHost));
+    } else {
+      const int r = h.rank_host[k];
+      HMGP_CUDA(cudaMemcpy(a, l.a, 8ull * l.m * r, cudaMemcpyDeviceToHost));
+      HMGP_CUDA(cudaMemcpy(b, l.b, 8ull * l.n * r, cudaMemcpyDeviceToHost));
+    }
+  })
+}
+
+int hmgp_hmat_matvec(hmgp_ctx* ctx, const hmgp_hmat* hm, const double* x, double* y) {
+  API_GUARD({
+    HMGP_CUDA(cudaSetDevice(ctx->device));
+    hmat_matvec(ctx->stream, hm->h, x, y);
+  })
+}
+
+void hmgp_hmat_destroy(hmgp_hmat* h) { delete h; }
+
+// ---------------------------------------------------------- data utilities
+static double u01(std::mt19937_64& g) { return (static_cast<double>(g() >> 11) + 0.5) * 0x1.0p-53; }
+
+int hmgp_random_locations(int n, int dim, uint64_t seed, double* out) {
+  API_GUARD({
+    if (n < 1) throw std::invalid_argument("random_locations: n must be >= 1");
+    std::mt19937_64 g(seed);
+    for (long long i = 0; i < (long long)n * dim; ++i) out[i] = u01(g);
+  })
+}
+
+int hmgp_jittered_grid(int gsz, uint64_t seed, double* out) {
+  API_GUARD({
+    std::mt19937_64 r(seed);
+    for (int i = 0; i < gsz; ++i)
+      for (int j = 0; j < gsz; ++j) {
+        const double ux = u01(r), uy = u01(r);
+        const size_t k = (size_t)i * gsz + j;
+        out[2 * k] = (i + 0.5) / gsz + (2.0 * ux - 1.0) * 0.4 / gsz;
+        out[2 * k + 1] = (j + 0.5) / gsz + (2.0 * uy - 1.0) * 0.4 / gsz;
+      }
+  })
+}
+
+int hmgp_normals(int n, uint64_t seed, double* out) {
+  API_GUARD({
+    std::mt19937_64 g(seed);
+    for (int i = 0; i < n; ++i) out[i] = normal_quantile_host(u01(g));
+  })
+}
+
+}  // extern "C"
+
+int hmgp_fail(int code, const char* msg) { return fail(code, msg); }

@@ -1,0 +1,1231 @@
+// H-LDL^T / H-Cholesky on the GPU (hfactor.cpp:22-363), column-sweep H-solves,
+// log-determinant and quadratic form (hfactor.cpp:365-403).
+//
+// Design.  The reference factorization is a deep recursion over the payload tree
+// (factor_diag -> trsm_lower_t / sub_product -> product_low_rank / add_low_rank).
+// Its loops over row children (trsm_lower_t's `for i`, sub_product's `for ii, jj`)
+// touch disjoint targets, so the host walks the SAME recursion but with LISTS of
+// independent items: every elementary operation (GEMM, TRSM, scaling, append /
+// recompression, leaf factorization) becomes ONE batched kernel launch over all
+// items that the reference would have executed one after the other.  Per-target
+// operation order is unchanged, so each block sees exactly the reference's
+// sequence of updates.  Ranks never leave the device: every kernel reads its
+// low-rank widths from device ints and the watermark rules (hblock.cpp:200,
+// hfactor.cpp:170) are evaluated inside the update kernel.  Temporaries come from
+// a stream-ordered stack arena with structural capacity bounds.
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "factor.h"
+#include "hmgp_api.h"
+#include "linalg.cuh"
+
+namespace hmgp_gpu {
+
+constexpr int TCAP = 512;  // width bound of product temporaries (checked on device)
+
+// ------------------------------------------------------------ utilities ---
+struct Arena {
+  char* base = nullptr;
+  size_t cap = 0, top = 0, peak = 0;
+  void init(size_t bytes) {
+    cap = bytes;
+    HMGP_CUDA(cudaMalloc(&base, cap));
+  }
+  ~Arena() { cudaFree(base); }
+  size_t mark() const { return top; }
+  void release(size_t m) { top = m; }
+  void* raw(size_t bytes) {
+    const size_t a = (top + 255) & ~size_t(255);
+    if (a + bytes > cap) throw Error(6, "factorize: device temporary arena exhausted");
+    top = a + bytes;
+    peak = std::max(peak, top);
+    return base + a;
+  }
+  double* dbl(size_t n) { return static_cast<double*>(raw(std::max<size_t>(n, 1) * 8)); }
+  int* ints(size_t n) { return static_cast<int*>(raw(std::max<size_t>(n, 1) * 4)); }
+};
+
+// Pinned host ring -> device ring for item descriptors (stream ordered).
+struct Stager {
+  char* h = nullptr;
+  char* d = nullptr;
+  size_t cap = 0, off = 0;
+  cudaStream_t st = nullptr;
+  void init(size_t bytes, cudaStream_t s) {
+    cap = bytes;
+    st = s;
+    HMGP_CUDA(cudaMallocHost(&h, cap));
+    HMGP_CUDA(cudaMalloc(&d, cap));
+  }
+  ~Stager() {
+    cudaFreeHost(h);
+    cudaFree(d);
+  }
+  template <class T>
+  const T* put(const std::vector<T>& v) {
+    const size_t bytes = (v.size() * sizeof(T) + 255) & ~size_t(255);
+    if (bytes > cap) throw Error(6, "item batch exceeds staging ring");
+    if (off + bytes > cap) {
+      HMGP_CUDA(cudaStreamSynchronize(st));
+      off = 0;
+    }
+    std::memcpy(h + off, v.data(), v.size() * sizeof(T));
+    HMGP_CUDA(cudaMemcpyAsync(d + off, h + off, v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+    const T* r = reinterpret_cast<const T*>(d + off);
+    off += bytes;
+    return r;
+  }
+};
+
+// device matrix view: rows x cols (cols possibly on device; .cols.v = capacity)
+struct MV {
+  double* p = nullptr;
+  int ld = 0, rows = 0;
+  Dim cols{0, nullptr};
+};
+static MV rows_of(MV m, int r0, int cnt) {
+  m.p += r0;
+  m.rows = cnt;
+  return m;
+}
+static MV cols_of(MV m, int c0, int cnt) {  // structural columns only
+  m.p += (size_t)c0 * m.ld;
+  m.cols = dimv(cnt);
+  return m;
+}
+
+// ----------------------------------------------------------- the engine ---
+struct Engine {
+  Factor& F;
+  const Geometry& G;
+  cudaStream_t st;
+  Arena ar;
+  Stager sg;
+  bool ldl;
+  double eps;
+  int* d_err = nullptr;
+
+  Engine(Factor& f, cudaStream_t s, size_t arena_bytes)
+      : F(f), G(*f.g), st(s), ldl(f.ldl), eps(f.eps) {
+    ar.init(arena_bytes);
+    sg.init((size_t)64 << 20, s);
+    d_err = ar.ints(1);
+    HMGP_CUDA(cudaMemsetAsync(d_err, 0, 4, st));
+  }
+
+  // --- node helpers
+  const HNode& N(int id) const { return F.nodes[id]; }
+  int kind(int id) const { return F.nodes[id].kind; }
+  int rb(int id) const { return G.nbeg[N(id).row]; }
+  int cb(int id) const { return G.nbeg[N(id).col]; }
+  int nr(int id) const { return G.nend[N(id).row] - G.nbeg[N(id).row]; }
+  int nc(int id) const { return G.nend[N(id).col] - G.nbeg[N(id).col]; }
+  int kid(int id, int i, int j) const { return N(id).kids[i * N(id).kc + j]; }
+  const LeafDev& LF(int id) const { return F.leaf[N(id).leaf]; }
+  int* rankp(int id) const { return F.d_rank + N(id).leaf; }
+  int* compp(int id) const { return F.d_compact + N(id).leaf; }
+  MV Uv(int id) const {
+    const LeafDev& l = LF(id);
+    return MV{l.a, l.m, l.m, dimp(rankp(id), l.cap)};
+  }
+  MV Vv(int id) const {
+    const LeafDev& l = LF(id);
+    return MV{l.b, l.n, l.n, dimp(rankp(id), l.cap)};
+  }
+  MV Dv(int id) const {
+    const LeafDev& l = LF(id);
+    return MV{l.a, l.m, l.m, dimv(l.n)};
+  }
+  const double* dseg(int begin) const { return F.d_d + begin; }
+
+  MV temp(int rows, Dim cols) {
+    MV m;
+    m.rows = rows;
+    m.ld = std::max(rows, 1);
+    m.cols = cols;
+    m.p = ar.dbl((size_t)m.ld * std::max(cols.v, 1));
+    return m;
+  }
+
+  // --- batched primitive launchers
+  void gemm(std::vector<GemmItem>& v) {
+    if (v.empty()) return;
+    int tiles = 1;
+    for (auto& g : v) tiles = std::max(tiles, ((g.M.v + 63) / 64) * ((g.N.v + 63) / 64));
+    launch_gemm(sg.put(v), (int)v.size(), tiles, st);
+    v.clear();
+  }
+  void copy(std::vector<CopyScaleItem>& v) {
+    if (v.empty()) return;
+    int mx = 1;
+    for (auto& c : v) mx = std::max<long long>(mx, std::min<long long>((long long)c.rows * c.cols.v, 1 << 24));
+    launch_copy_scale(sg.put(v), (int)v.size(), mx, st);
+    v.clear();
+  }
+  void lrupd(std::vector<TruncItem>& v) {
+    if (v.empty()) return;
+    launch_truncate(sg.put(v), (int)v.size(), eps, d_err, st);
+    v.clear();
+  }
+  CopyScaleItem cpy(const double* src, int lds, MV dst, Dim cols, int trans, double alpha,
+                    const double* d, int mode) {
+    CopyScaleItem c{};
+    c.src = src;
+    c.lds = lds;
+    c.dst = dst.p;
+    c.ldd = dst.ld;
+    c.rows = dst.rows;
+    c.cols = cols;
+    c.trans = trans;
+    c.alpha = alpha;
+    c.d = d;
+    c.mode = ldl ? mode : 0;
+    c.set_cols = nullptr;
+    return c;
+  }
+  // fused LR update / recompression item for a target (U, V, rank, compact)
+  TruncItem lritem(double* U, double* V, int m, int n, int* rank, int* compact, int cond, int cap,
+                   const MV* P, const MV* Q, int pro, int qro, double alpha, int rcap) {
+    TruncItem t{};
+    t.U = U;
+    t.V = V;
+    t.m = m;
+    t.n = n;
+    t.rank = rank;
+    t.compact = compact;
+    t.cond = cond;
+    t.cap = cap;
+    if (P) {
+      t.P = P->p;
+      t.Q = Q->p;
+      t.ldp = P->ld;
+      t.ldq = Q->ld;
+      t.pr = P->rows;
+      t.qr = Q->rows;
+      t.pro = pro;
+      t.qro = qro;
+      t.addp = P->cols.p;
+      t.addv = P->cols.v;
+    }
+    t.alpha = alpha;
+    t.rcap = rcap;
+    t.ws = nullptr;
+    return t;
+  }
+  // assign workspaces (from the arena; caller releases) and launch
+  void lrupd_ws(std::vector<TruncItem>& v) {
+    for (auto& t : v) {
+      if (t.cond == 4) continue;
+      t.ws = ar.dbl(trunc_ws_doubles(t.m, t.n, t.rcap));
+    }
+    lrupd(v);
+  }
+
+  // --- compress_low_rank on a list of LR blocks (hblock.cpp:164-170)
+  void compress(const std::vector<int>& ids) {
+    if (ids.empty()) return;
+    const size_t mk = ar.mark();
+    std::vector<TruncItem> v;
+    for (int x : ids) {
+      const LeafDev& l = LF(x);
+      v.push_back(lritem(l.a, l.b, l.m, l.n, rankp(x), compp(x), 0, l.cap, nullptr, nullptr, 0, 0,
+                         1.0, l.cap));
+    }
+    lrupd_ws(v);
+    ar.release(mk);
+  }
+
+  // ------------------------------------------------------- hblk::apply ----
+  struct Ap {
+    int b;      // H-block node
+    MV x, y;    // y (+)= alpha op(B) x
+    double alpha;
+    int trans;  // 0: B, 1: B^T
+  };
+  void apply(const std::vector<Ap>& its) {
+    if (its.empty()) return;
+    std::vector<GemmItem> g;
+    std::vector<Ap> lr, br;
+    for (const Ap& a : its) {
+      const int k = kind(a.b);
+      if (k == DENSE) {
+        const LeafDev& l = LF(a.b);
+        GemmItem gi{};
+        gi.A = l.a;
+        gi.lda = l.m;
+        gi.ta = a.trans;
+        gi.B = a.x.p;
+        gi.ldb = a.x.ld;
+        gi.tb = 0;
+        gi.C = a.y.p;
+        gi.ldc = a.y.ld;
+        gi.M = dimv(a.trans ? l.n : l.m);
+        gi.N = a.x.cols;
+        gi.K = dimv(a.trans ? l.m : l.n);
+        gi.alpha = a.alpha;
+        g.push_back(gi);
+      } else if (k == LOWRANK) {
+        lr.push_back(a);
+      } else {
+        br.push_back(a);
+      }
+    }
+    gemm(g);
+    if (!lr.empty()) {
+      const size_t mk = ar.mark();
+      std::vector<MV> T;
+      std::vector<CopyScaleItem> z;
+      for (const Ap& a : lr) {
+        const LeafDev& l = LF(a.b);
+        MV t = temp(l.cap, a.x.cols);
+        z.push_back(cpy(nullptr, 0, t, a.x.cols, 0, 0.0, nullptr, 0));
+        T.push_back(t);
+      }
+      copy(z);
+      for (size_t i = 0; i < lr.size(); ++i) {  // T = (trans ? U : V)^T x   (rank x c)
+        const Ap& a = lr[i];
+        const LeafDev& l = LF(a.b);
+        GemmItem gi{};
+        gi.A = a.trans ? l.a : l.b;
+        gi.lda = a.trans ? l.m : l.n;
+        gi.ta = 1;
+        gi.B = a.x.p;
+        gi.ldb = a.x.ld;
+        gi.C = T[i].p;
+        gi.ldc = T[i].ld;
+        gi.M = dimp(rankp(a.b), l.cap);
+        gi.N = a.x.cols;
+        gi.K = dimv(a.trans ? l.m : l.n);
+        gi.alpha = 1.0;
+        g.push_back(gi);
+      }
+      gemm(g);
+      for (size_t i = 0; i < lr.size(); ++i) {  // y += alpha (trans ? V : U) T
+        const Ap& a = lr[i];
+        const LeafDev& l = LF(a.b);
+        GemmItem gi{};
+        gi.A = a.trans ? l.b : l.a;
+        gi.lda = a.trans ? l.n : l.m;
+        gi.B = T[i].p;
+        gi.ldb = T[i].ld;
+        gi.C = a.y.p;
+        gi.ldc = a.y.ld;
+        gi.M = dimv(a.trans ? l.n : l.m);
+        gi.N = a.x.cols;
+        gi.K = dimp(rankp(a.b), l.cap);
+        gi.alpha = a.alpha;
+        g.push_back(gi);
+      }
+      gemm(g);
+      ar.release(mk);
+    }
+    if (!br.empty()) {
+      // child positions in row-major order, sequential (shared y rows)
+      for (int pos = 0; pos < 4; ++pos) {
+        std::vector<Ap> sub;
+        for (const Ap& a : br) {
+          const HNode& nd = N(a.b);
+          if (pos >= nd.kr * nd.kc) continue;
+          const int c = nd.kids[pos];
+          if (c < 0) continue;
+          Ap s = a;
+          s.b = c;
+          if (!a.trans) {
+            s.x = rows_of(a.x, cb(c) - cb(a.b), nc(c));
+            s.y = rows_of(a.y, rb(c) - rb(a.b), nr(c));
+          } else {
+            s.x = rows_of(a.x, rb(c) - rb(a.b), nr(c));
+            s.y = rows_of(a.y, cb(c) - cb(a.b), nc(c));
+          }
+          sub.push_back(s);
+        }
+        apply(sub);
+      }
+    }
+  }
+
+  // multiply(B, X) into preallocated Y (zeroed here), hblock.cpp:89-92
+  void multiply_into(const std::vector<int>& bs, const std::vector<MV>& xs, const std::vector<MV>& ys) {
+    std::vector<CopyScaleItem> z;
+    std::vector<Ap> ap;
+    for (size_t i = 0; i < bs.size(); ++i) {
+      z.push_back(cpy(nullptr, 0, ys[i], xs[i].cols, 0, 0.0, nullptr, 0));
+      ap.push_back(Ap{bs[i], xs[i], ys[i], 1.0, 0});
+    }
+    copy(z);
+    apply(ap);
+  }
+
+  // -------------------------------------------------- solve_lower_multi ---
+  void solve_lower_multi(int l, const std::vector<MV>& ms) {
+    if (ms.empty()) return;
+    if (kind(l) == DENSE) {
+      const LeafDev& L = LF(l);
+      std::vector<TrsmLItem> v;
+      int mc = 1;
+      for (const MV& m : ms) {
+        v.push_back(TrsmLItem{L.a, L.m, L.m, m.p, m.ld, m.cols, 0});
+        mc = std::max(mc, m.cols.v);
+      }
+      launch_trsm_left(sg.put(v), (int)v.size(), mc, st);
+      return;
+    }
+    const int l00 = kid(l, 0, 0), l10 = kid(l, 1, 0), l11 = kid(l, 1, 1);
+    const int n1 = nr(l00);
+    std::vector<MV> top, bot;
+    for (const MV& m : ms) {
+      top.push_back(rows_of(m, 0, n1));
+      bot.push_back(rows_of(m, n1, m.rows - n1));
+    }
+    solve_lower_multi(l00, top);
+    std::vector<Ap> ap;
+    for (size_t i = 0; i < ms.size(); ++i) ap.push_back(Ap{l10, top[i], bot[i], -1.0, 0});
+    apply(ap);
+    solve_lower_multi(l11, bot);
+  }
+
+  // ----------------------------------------------------- trsm_dense_block -
+  // x <- x L^{-T} (D^{-1}), hfactor.cpp:107-123
+  void trsm_dense(const std::vector<MV>& xs, int l) {
+    if (xs.empty()) return;
+    if (kind(l) == DENSE) {
+      const LeafDev& L = LF(l);
+      std::vector<TrsmRItem> v;
+      int mr = 1;
+      for (const MV& x : xs) {
+        v.push_back(TrsmRItem{L.a, L.m, L.m, x.p, x.ld, x.rows});
+        mr = std::max(mr, x.rows);
+      }
+      launch_trsm_right(sg.put(v), (int)v.size(), mr, st);
+      if (ldl) {
+        std::vector<CopyScaleItem> c;
+        for (const MV& x : xs) c.push_back(cpy(x.p, x.ld, x, dimv(L.m), 0, 1.0, dseg(rb(l)), 4));
+        copy(c);
+      }
+      return;
+    }
+    const int l00 = kid(l, 0, 0), l10 = kid(l, 1, 0), l11 = kid(l, 1, 1);
+    const int n1 = nr(l00), t = nr(l);
+    std::vector<MV> x1, x2;
+    for (const MV& x : xs) {
+      x1.push_back(cols_of(x, 0, n1));
+      x2.push_back(cols_of(x, n1, t - n1));
+    }
+    trsm_dense(x1, l00);
+    const size_t mk = ar.mark();
+    std::vector<MV> wt, pr;
+    std::vector<CopyScaleItem> c;
+    std::vector<int> bs;
+    for (size_t i = 0; i < xs.size(); ++i) {
+      MV w = temp(n1, dimv(xs[i].rows));  // wt = x1^T, rows scaled by d
+      c.push_back(cpy(x1[i].p, x1[i].ld, w, dimv(xs[i].rows), 1, 1.0, dseg(rb(l00)), 1));
+      wt.push_back(w);
+      pr.push_back(temp(t - n1, dimv(xs[i].rows)));
+      bs.push_back(l10);
+    }
+    copy(c);
+    multiply_into(bs, wt, pr);
+    for (size_t i = 0; i < xs.size(); ++i) {  // x2 -= pr^T
+      CopyScaleItem a = cpy(pr[i].p, pr[i].ld, x2[i], dimv(t - n1), 1, -1.0, nullptr, 0);
+      a.accum = 1;
+      c.push_back(a);
+    }
+    copy(c);
+    ar.release(mk);
+    trsm_dense(x2, l11);
+  }
+
+  // -------------------------------------------------------- trsm_lower_t --
+  void trsm(const std::vector<int>& xs, int l) {
+    if (xs.empty()) return;
+    std::vector<int> lr, dn, br;
+    for (int x : xs) (kind(x) == LOWRANK ? lr : kind(x) == DENSE ? dn : br).push_back(x);
+    if (kind(l) == DENSE) {
+      const LeafDev& L = LF(l);
+      if (!lr.empty()) {
+        compress(lr);
+        std::vector<TrsmLItem> v;
+        std::vector<CopyScaleItem> c;
+        int mc = 1;
+        for (int x : lr) {
+          const MV V = Vv(x);
+          v.push_back(TrsmLItem{L.a, L.m, L.m, V.p, V.ld, V.cols, 0});
+          mc = std::max(mc, V.cols.v);
+          if (ldl) c.push_back(cpy(V.p, V.ld, V, V.cols, 0, 1.0, dseg(rb(l)), 2));
+        }
+        launch_trsm_left(sg.put(v), (int)v.size(), mc, st);
+        copy(c);
+      }
+      if (!dn.empty()) {
+        std::vector<MV> d;
+        for (int x : dn) d.push_back(Dv(x));
+        trsm_dense(d, l);
+      }
+      if (!br.empty()) {
+        std::vector<int> ch;
+        for (int x : br)
+          for (int i = 0; i < N(x).kr; ++i) ch.push_back(kid(x, i, 0));
+        trsm(ch, l);
+      }
+      return;
+    }
+    if (!lr.empty()) {
+      compress(lr);
+      std::vector<MV> vs;
+      for (int x : lr) vs.push_back(Vv(x));
+      solve_lower_multi(l, vs);
+      if (ldl) {
+        std::vector<CopyScaleItem> c;
+        for (const MV& V : vs) c.push_back(cpy(V.p, V.ld, V, V.cols, 0, 1.0, dseg(rb(l)), 2));
+        copy(c);
+      }
+    }
+    if (!dn.empty()) {
+      std::vector<MV> d;
+      for (int x : dn) d.push_back(Dv(x));
+      trsm_dense(d, l);
+    }
+    if (!br.empty()) {
+      std::vector<int> l0, l1;
+      std::vector<Trip> tr;
+      for (int x : br)
+        for (int i = 0; i < N(x).kr; ++i) {
+          l0.push_back(kid(x, i, 0));
+          l1.push_back(kid(x, i, 1));
+          tr.push_back(Trip{kid(x, i, 1), kid(x, i, 0), kid(l, 1, 0)});
+        }
+      trsm(l0, kid(l, 0, 0));
+      subprod(tr);
+      trsm(l1, kid(l, 1, 1));
+    }
+  }
+
+  // ------------------------------------------------------ add_low_rank ---
+  struct Add {
+    int c;
+    MV p, q;  // p: rows at absolute row0, q: rows at absolute col0
+    double alpha;
+    int row0, col0;
+  };
+  void add_lr(const std::vector<Add>& its) {
+    if (its.empty()) return;
+    std::vector<GemmItem> g;
+    std::vector<TruncItem> t;
+    std::vector<Add> br;
+    const size_t mk = ar.mark();
+    for (const Add& a : its) {
+      const int k = kind(a.c);
+      if (k == DENSE) {  // hblock.cpp:181-184
+        const LeafDev& l = LF(a.c);
+        GemmItem gi{};
+        gi.A = a.p.p;
+        gi.lda = a.p.ld;
+        gi.B = a.q.p;
+        gi.ldb = a.q.ld;
+        gi.tb = 1;
+        gi.C = l.a + (size_t)(a.col0 - cb(a.c)) * l.m + (a.row0 - rb(a.c));
+        gi.ldc = l.m;
+        gi.M = dimv(a.p.rows);
+        gi.N = dimv(a.q.rows);
+        gi.K = a.p.cols;
+        gi.alpha = a.alpha;
+        g.push_back(gi);
+      } else if (k == LOWRANK) {  // hblock.cpp:185-203
+        const LeafDev& l = LF(a.c);
+        t.push_back(lritem(l.a, l.b, l.m, l.n, rankp(a.c), compp(a.c), 2, l.cap, &a.p, &a.q,
+                           a.row0 - rb(a.c), a.col0 - cb(a.c), a.alpha, l.cap + a.p.cols.v));
+      } else {
+        br.push_back(a);
+      }
+    }
+    gemm(g);
+    lrupd_ws(t);
+    ar.release(mk);
+    if (!br.empty()) {  // hblock.cpp:205-216
+      std::vector<Add> sub;
+      for (const Add& a : br) {
+        const HNode& nd = N(a.c);
+        for (int pos = 0; pos < nd.kr * nd.kc; ++pos) {
+          const int ch = nd.kids[pos];
+          if (ch < 0) continue;
+          const int r0 = std::max(a.row0, rb(ch)), r1 = std::min(a.row0 + a.p.rows, rb(ch) + nr(ch));
+          const int c0 = std::max(a.col0, cb(ch)), c1 = std::min(a.col0 + a.q.rows, cb(ch) + nc(ch));
+          if (r0 >= r1 || c0 >= c1) continue;
+          sub.push_back(Add{ch, rows_of(a.p, r0 - a.row0, r1 - r0), rows_of(a.q, c0 - a.col0, c1 - c0),
+                            a.alpha, r0, c0});
+        }
+      }
+      add_lr(sub);
+    }
+  }
+
+  // scaled copies: V (rows) * d over a column cluster
+  MV scaled_copy_rows(MV src, int dbegin) {
+    MV t = temp(src.rows, src.cols);
+    std::vector<CopyScaleItem> c{cpy(src.p, src.ld, t, src.cols, 0, 1.0, dseg(dbegin), 1)};
+    copy(c);
+    return t;
+  }
+
+  // --------------------------------------------------- product_low_rank --
+  struct Pair {
+    MV p, q;
+  };
+  // Results are allocated on the arena BEFORE any internal temporary so the
+  // caller can release them with its own mark.
+  std::vector<Pair> product_lr(const std::vector<std::pair<int, int>>& abs) {
+    const size_t n = abs.size();
+    std::vector<Pair> out(n);
+    std::vector<int> cls(n);  // 0 aLR, 1 bLR, 2 aDense, 3 bDense, 4 branch
+    int nbr = 0;
+    for (size_t i = 0; i < n; ++i) {
+      const int a = abs[i].first, b = abs[i].second;
+      nbr += !(kind(a) == LOWRANK || kind(b) == LOWRANK || kind(a) == DENSE || kind(b) == DENSE);
+    }
+    int* wcs = nbr ? ar.ints(nbr) : nullptr;
+    if (nbr) HMGP_CUDA(cudaMemsetAsync(wcs, 0, 4ull * nbr, st));
+    int wci = 0;
+    for (size_t i = 0; i < n; ++i) {
+      const int a = abs[i].first, b = abs[i].second;
+      cls[i] = kind(a) == LOWRANK ? 0 : kind(b) == LOWRANK ? 1 : kind(a) == DENSE ? 2
+               : kind(b) == DENSE ? 3 : 4;
+      switch (cls[i]) {
+        case 0:
+          out[i].p = Uv(a);
+          out[i].q = temp(nr(b), Uv(a).cols);
+          break;
+        case 1:
+          out[i].p = temp(nr(a), Uv(b).cols);
+          out[i].q = Uv(b);
+          break;
+        case 2:
+          out[i].p = temp(nr(a), dimv(nc(a)));
+          out[i].q = kind(b) == DENSE ? Dv(b) : temp(nr(b), dimv(nc(b)));
+          break;
+        case 3:
+          out[i].p = temp(nr(a), dimv(nr(b)));
+          out[i].q = temp(nr(b), dimv(nr(b)));
+          break;
+        default: {
+          int* wc = wcs + wci++;
+          out[i].p = temp(nr(a), dimp(wc, TCAP));
+          out[i].q = temp(nr(b), dimp(wc, TCAP));
+        }
+      }
+    }
+    const size_t mk = ar.mark();
+    // simple cases
+    {
+      std::vector<int> mb;
+      std::vector<MV> mx, my;
+      std::vector<CopyScaleItem> c;
+      for (size_t i = 0; i < n; ++i) {
+        const int a = abs[i].first, b = abs[i].second;
+        switch (cls[i]) {
+          case 0: {  // {U_a, B (V_a d)}
+            MV va = Vv(a);
+            if (ldl) {
+              MV t = temp(va.rows, va.cols);
+              c.push_back(cpy(va.p, va.ld, t, va.cols, 0, 1.0, dseg(cb(a)), 1));
+              va = t;
+            }
+            mb.push_back(b);
+            mx.push_back(va);
+            my.push_back(out[i].q);
+            break;
+          }
+          case 1: {  // {A (V_b d), U_b}
+            MV vb = Vv(b);
+            if (ldl) {
+              MV t = temp(vb.rows, vb.cols);
+              c.push_back(cpy(vb.p, vb.ld, t, vb.cols, 0, 1.0, dseg(cb(b)), 1));
+              vb = t;
+            }
+            mb.push_back(a);
+            mx.push_back(vb);
+            my.push_back(out[i].p);
+            break;
+          }
+          case 2: {  // {A.D diag(d), B materialised}
+            c.push_back(cpy(LF(a).a, LF(a).m, out[i].p, dimv(nc(a)), 0, 1.0, dseg(cb(a)), 3));
+            if (kind(b) != DENSE) {
+              MV e = temp(nc(b), dimv(nc(b)));
+              c.push_back(cpy(nullptr, 0, e, dimv(nc(b)), 0, 1.0, nullptr, 0));
+              c.back().mode = 0;
+              mb.push_back(b);
+              mx.push_back(e);
+              my.push_back(out[i].q);
+            }
+            break;
+          }
+          case 3: {  // {A (B.D^T d), I}
+            MV x = temp(nc(b), dimv(nr(b)));
+            c.push_back(cpy(LF(b).a, LF(b).m, x, dimv(nr(b)), 1, 1.0, dseg(cb(b)), 1));
+            CopyScaleItem e = cpy(nullptr, 0, out[i].q, dimv(nr(b)), 0, 1.0, nullptr, 0);
+            e.mode = 0;
+            c.push_back(e);
+            mb.push_back(a);
+            mx.push_back(x);
+            my.push_back(out[i].p);
+            break;
+          }
+          default:
+            break;
+        }
+      }
+      copy(c);
+      if (!mb.empty()) multiply_into(mb, mx, my);
+    }
+    // branch x branch (hfactor.cpp:150-190)
+    std::vector<size_t> bi;
+    for (size_t i = 0; i < n; ++i)
+      if (cls[i] == 4) bi.push_back(i);
+    if (!bi.empty()) {
+      struct Part {
+        size_t item;
+        int ii, jj, a0, b0;
+        MV p, q;
+        int* cols;
+      };
+      std::vector<Part> parts;
+      size_t npart = 0;
+      for (size_t i : bi) npart += (size_t)N(abs[i].first).kr * N(abs[i].second).kr;
+      int* pcols = ar.ints(npart);
+      HMGP_CUDA(cudaMemsetAsync(pcols, 0, 4 * npart, st));
+      for (size_t i : bi) {
+        const int a = abs[i].first, b = abs[i].second;
+        for (int ii = 0; ii < N(a).kr; ++ii)
+          for (int jj = 0; jj < N(b).kr; ++jj) {
+            Part pt;
+            pt.item = i;
+            pt.ii = ii;
+            pt.jj = jj;
+            pt.a0 = kid(a, ii, 0);
+            pt.b0 = kid(b, jj, 0);
+            pt.cols = pcols + parts.size();
+            pt.p = temp(nr(pt.a0), dimp(pt.cols, TCAP));
+            pt.q = temp(nr(pt.b0), dimp(pt.cols, TCAP));
+            parts.push_back(pt);
+          }
+      }
+      const int kcmax = 2;
+      for (int kk = 0; kk < kcmax; ++kk) {
+        std::vector<std::pair<int, int>> sub;
+        std::vector<size_t> who;
+        for (size_t t = 0; t < parts.size(); ++t) {
+          const int a = abs[parts[t].item].first, b = abs[parts[t].item].second;
+          if (kk >= N(a).kc) continue;
+          sub.push_back({kid(a, parts[t].ii, kk), kid(b, parts[t].jj, kk)});
+          who.push_back(t);
+        }
+        if (sub.empty()) continue;
+        const size_t mk2 = ar.mark();
+        std::vector<Pair> tp = product_lr(sub);
+        std::vector<TruncItem> upd;
+        for (size_t s = 0; s < sub.size(); ++s) {
+          Part& pt = parts[who[s]];
+          upd.push_back(lritem(pt.p.p, pt.q.p, pt.p.rows, pt.q.rows, pt.cols, nullptr, 3, TCAP,
+                               &tp[s].p, &tp[s].q, 0, 0, 1.0, TCAP + tp[s].p.cols.v));
+        }
+        lrupd_ws(upd);
+        ar.release(mk2);
+      }
+      // embed parts into out (pure appends; one launch per part index so the
+      // same target is never appended to concurrently), then truncate once
+      size_t maxparts = 0;
+      std::vector<std::vector<size_t>> byitem(n);
+      for (size_t t = 0; t < parts.size(); ++t) byitem[parts[t].item].push_back(t);
+      for (size_t i : bi) maxparts = std::max(maxparts, byitem[i].size());
+      for (size_t q = 0; q < maxparts; ++q) {
+        std::vector<TruncItem> ap;
+        for (size_t i : bi) {
+          if (q >= byitem[i].size()) continue;
+          const Part& pt = parts[byitem[i][q]];
+          const int a = abs[i].first, b = abs[i].second;
+          ap.push_back(lritem(out[i].p.p, out[i].q.p, nr(a), nr(b), const_cast<int*>(out[i].p.cols.p),
+                              nullptr, 4, TCAP, &pt.p, &pt.q, rb(pt.a0) - rb(a), rb(pt.b0) - rb(b), 1.0,
+                              TCAP));
+        }
+        lrupd(ap);
+      }
+      std::vector<TruncItem> tr;
+      for (size_t i : bi) {
+        const int a = abs[i].first, b = abs[i].second;
+        tr.push_back(lritem(out[i].p.p, out[i].q.p, nr(a), nr(b), const_cast<int*>(out[i].p.cols.p),
+                            nullptr, 0, TCAP, nullptr, nullptr, 0, 0, 1.0, TCAP));
+      }
+      lrupd_ws(tr);
+    }
+    ar.release(mk);
+    return out;
+  }
+
+  // --------------------------------------------------------- sub_product -
+  // C -= A diag(d_K) B^T (hfactor.cpp:236-285)
+  void subprod(const std::vector<Trip>& ts) {
+    if (ts.empty()) return;
+    const size_t mk = ar.mark();
+    std::vector<Add> adds;
+    std::vector<int> mb;
+    std::vector<MV> mx, my;
+    std::vector<CopyScaleItem> c;
+    std::vector<Trip> brc, leafc;
+    for (const Trip& t : ts) {
+      const int C = t.c, a = t.a, b = t.b;
+      if (kind(a) == LOWRANK) {
+        MV va = Vv(a);
+        if (ldl) {
+          MV s = temp(va.rows, va.cols);
+          c.push_back(cpy(va.p, va.ld, s, va.cols, 0, 1.0, dseg(cb(a)), 1));
+          va = s;
+        }
+        MV w = temp(nr(b), va.cols);
+        mb.push_back(b);
+        mx.push_back(va);
+        my.push_back(w);
+        adds.push_back(Add{C, Uv(a), w, -1.0, rb(a), rb(b)});
+      } else if (kind(b) == LOWRANK) {
+        MV vb = Vv(b);
+        if (ldl) {
+          MV s = temp(vb.rows, vb.cols);
+          c.push_back(cpy(vb.p, vb.ld, s, vb.cols, 0, 1.0, dseg(cb(b)), 1));
+          vb = s;
+        }
+        MV w = temp(nr(a), vb.cols);
+        mb.push_back(a);
+        mx.push_back(vb);
+        my.push_back(w);
+        adds.push_back(Add{C, w, Uv(b), -1.0, rb(a), rb(b)});
+      } else if (kind(a) == DENSE) {
+        MV p = temp(nr(a), dimv(nc(a)));
+        c.push_back(cpy(LF(a).a, LF(a).m, p, dimv(nc(a)), 0, 1.0, dseg(cb(a)), 3));
+        MV q;
+        if (kind(b) == DENSE) {
+          q = Dv(b);
+        } else {
+          q = temp(nr(b), dimv(nc(b)));
+          MV e = temp(nc(b), dimv(nc(b)));
+          CopyScaleItem ei = cpy(nullptr, 0, e, dimv(nc(b)), 0, 1.0, nullptr, 0);
+          ei.mode = 0;
+          c.push_back(ei);
+          mb.push_back(b);
+          mx.push_back(e);
+          my.push_back(q);
+        }
+        adds.push_back(Add{C, p, q, -1.0, rb(a), rb(b)});
+      } else if (kind(b) == DENSE) {
+        MV x = temp(nc(b), dimv(nr(b)));
+        c.push_back(cpy(LF(b).a, LF(b).m, x, dimv(nr(b)), 1, 1.0, dseg(cb(b)), 1));
+        MV w = temp(nr(a), dimv(nr(b)));
+        MV e = temp(nr(b), dimv(nr(b)));
+        CopyScaleItem ei = cpy(nullptr, 0, e, dimv(nr(b)), 0, 1.0, nullptr, 0);
+        ei.mode = 0;
+        c.push_back(ei);
+        mb.push_back(a);
+        mx.push_back(x);
+        my.push_back(w);
+        adds.push_back(Add{C, w, e, -1.0, rb(a), rb(b)});
+      } else if (kind(C) == BRANCH) {
+        brc.push_back(t);
+      } else {
+        leafc.push_back(t);
+      }
+    }
+    copy(c);
+    if (!mb.empty()) multiply_into(mb, mx, my);
+    if (!leafc.empty()) {
+      std::vector<std::pair<int, int>> ab;
+      for (const Trip& t : leafc) ab.push_back({t.a, t.b});
+      std::vector<Pair> pr = product_lr(ab);
+      for (size_t i = 0; i < leafc.size(); ++i)
+        adds.push_back(Add{leafc[i].c, pr[i].p, pr[i].q, -1.0, rb(leafc[i].a), rb(leafc[i].b)});
+    }
+    add_lr(adds);
+    ar.release(mk);
+    if (!brc.empty()) {
+      for (int kk = 0; kk < 2; ++kk) {
+        std::vector<Trip> sub;
+        for (const Trip& t : brc) {
+          if (kk >= N(t.a).kc) continue;
+          for (int ii = 0; ii < N(t.a).kr; ++ii)
+            for (int jj = 0; jj < N(t.b).kr; ++jj) {
+              const int tg = kid(t.c, ii, jj);
+              if (tg < 0) continue;
+              sub.push_back(Trip{tg, kid(t.a, ii, kk), kid(t.b, jj, kk)});
+            }
+        }
+        subprod(sub);
+      }
+    }
+  }
+
+  // --------------------------------------------------------- factor_diag -
+  void factor_diag(int a) {
+    if (kind(a) == DENSE) {
+      const LeafDev& l = LF(a);
+      launch_leaf_factor(l.a, l.m, rb(a), ldl ? 1 : 0, F.d_d, F.clamp_tol, F.d_status, st);
+      return;
+    }
+    factor_diag(kid(a, 0, 0));
+    trsm({kid(a, 1, 0)}, kid(a, 0, 0));
+    subprod({Trip{kid(a, 1, 1), kid(a, 1, 0), kid(a, 1, 0)}});
+    factor_diag(kid(a, 1, 1));
+  }
+};
+
+// ------------------------------------------------------ solve schedules ---
+__global__ void k_trsv_leaf(const double* __restrict__ L, int b, double* __restrict__ x, int trans) {
+  // one warp; x has b entries (tree-order segment)
+  const int lane = threadIdx.x;
+  if (!trans) {
+    for (int j = 0; j < b; ++j) {
+      const double xj = x[j] / L[(size_t)j * b + j];
+      __syncwarp();
+      if (lane == 0) x[j] = xj;
+      for (int i = j + 1 + lane; i < b; i += 32) x[i] -= L[(size_t)j * b + i] * xj;
+      __syncwarp();
+    }
+  } else {
+    for (int j = b - 1; j >= 0; --j) {
+      double s = 0.0;
+      for (int i = j + 1 + lane; i < b; i += 32) s += L[(size_t)j * b + i] * x[i];
+      s = warp_sum(s);
+      if (lane == 0) x[j] = (x[j] - s) / L[(size_t)j * b + j];
+      __syncwarp();
+    }
+  }
+}
+
+struct SolveBlk {
+  int leaf;
+  int r0, c0;
+};
+
+// y[rows] -= B x[cols]  (trans = 0)   or   y[cols] -= B^T x[rows]  (trans = 1)
+__global__ void k_solve_apply(const SolveBlk* __restrict__ blks, const LeafDev* __restrict__ lf,
+                              const int* __restrict__ rank, double* __restrict__ v, int trans) {
+  const SolveBlk sb = blks[blockIdx.x];
+  const LeafDev L = lf[sb.leaf];
+  __shared__ double t[1024];
+  const int in0 = trans ? sb.r0 : sb.c0, out0 = trans ? sb.c0 : sb.r0;
+  if (L.kind == DENSE) {
+    if (!trans) {
+      for (int i = threadIdx.x; i < L.m; i += blockDim.x) {
+        double s = 0.0;
+        for (int j = 0; j < L.n; ++j) s += L.a[(size_t)j * L.m + i] * v[in0 + j];
+        atomicAdd(&v[out0 + i], -s);
+      }
+    } else {
+      for (int j = threadIdx.x; j < L.n; j += blockDim.x) {
+        double s = 0.0;
+        for (int i = 0; i < L.m; ++i) s += L.a[(size_t)j * L.m + i] * v[in0 + i];
+        atomicAdd(&v[out0 + j], -s);
+      }
+    }
+    return;
+  }
+  const int r = rank[sb.leaf];
+  if (r <= 0) return;
+  const double* A = trans ? L.a : L.b;  // contract over the input side
+  const double* Bm = trans ? L.b : L.a;
+  const int nin = trans ? L.m : L.n, nout = trans ? L.n : L.m;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int l = w; l < r; l += nw) {
+    double s = 0.0;
+    for (int j = lane; j < nin; j += 32) s += A[(size_t)l * nin + j] * v[in0 + j];
+    s = warp_sum(s);
+    if (lane == 0) t[l] = s;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nout; i += blockDim.x) {
+    double s = 0.0;
+    for (int l = 0; l < r; ++l) s += Bm[(size_t)l * nout + i] * t[l];
+    atomicAdd(&v[out0 + i], -s);
+  }
+}
+
+__global__ void k_gather(const double* __restrict__ src, const int* __restrict__ perm, int n,
+                         double* __restrict__ dst) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) dst[k] = src[perm[k]];
+}
+__global__ void k_scatter(const double* __restrict__ src, const int* __restrict__ perm, int n,
+                          double* __restrict__ dst) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) dst[perm[k]] = src[k];
+}
+__global__ void k_div(double* __restrict__ v, const double* __restrict__ d, int n) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) v[k] /= d[k];
+}
+
+// deterministic two-pass reductions: sum v^2/d (ldl) or v^2; sum log d
+__global__ void k_reduce_partial(const double* __restrict__ v, const double* __restrict__ d, int n,
+                                 int mode, double* __restrict__ part) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    if (mode == 0)
+      s += v[k] * v[k];
+    else if (mode == 1)
+      s += v[k] * v[k] / d[k];
+    else
+      s += log(d[k]);
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+__global__ void k_reduce_final(const double* __restrict__ part, int n, double* out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) s += part[k];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) *out = s;
+}
+__global__ void k_count_nonpos(const double* __restrict__ d, int n, int* out) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+    if (!(d[k] > 0.0)) atomicAdd(out, 1);
+}
+// Cholesky: diag_ = L_ii of dense diagonal leaves (hfactor.cpp:302-310)
+__global__ void k_collect_diag(const LeafDev* __restrict__ lf, const int* __restrict__ leaves,
+                               const int* __restrict__ base, int count, double* __restrict__ d) {
+  const int t = blockIdx.x;
+  if (t >= count) return;
+  const LeafDev L = lf[leaves[t]];
+  for (int i = threadIdx.x; i < L.m; i += blockDim.x) d[base[t] + i] = L.a[(size_t)i * L.m + i];
+}
+
+// ------------------------------------------------------------ Factor API --
+Factor::~Factor() {
+  cudaFree(pool);
+  cudaFree(d_leaf);
+  cudaFree(d_rank);
+  cudaFree(d_compact);
+  cudaFree(d_d);
+  cudaFree(d_status);
+  cudaFree(d_fwd);
+  cudaFree(d_bwd);
+  cudaFree(d_work);
+}
+
+void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size_t arena_bytes) {
+  const Geometry& G = *H.g;
+  F.g = H.g;
+  F.ldl = ldl;
+  F.eps = eps_f;
+  F.nodes = H.nodes;
+  F.leaf_node = H.leaf_node;
+  const int L = (int)H.leaf.size();
+  // clone payload (hblock.cpp:17-28): same layout, new pool; compact_cols = 0
+  HMGP_CUDA(cudaMalloc(&F.pool, std::max<size_t>(1, H.pool_doubles) * 8));
+  HMGP_CUDA(cudaMemcpyAsync(F.pool, H.pool, H.pool_doubles * 8, cudaMemcpyDeviceToDevice, st));
+  F.leaf = H.leaf;
+  for (auto& l : F.leaf) {
+    l.a = F.pool + (l.a - H.pool);
+    if (l.b) l.b = F.pool + (l.b - H.pool);
+  }
+  HMGP_CUDA(cudaMalloc(&F.d_leaf, sizeof(LeafDev) * std::max(L, 1)));
+  HMGP_CUDA(cudaMemcpyAsync(F.d_leaf, F.leaf.data(), sizeof(LeafDev) * L, cudaMemcpyHostToDevice, st));
+  HMGP_CUDA(cudaMalloc(&F.d_rank, 4 * std::max(L, 1)));
+  HMGP_CUDA(cudaMemcpyAsync(F.d_rank, H.d_rank, 4ull * L, cudaMemcpyDeviceToDevice, st));
+  HMGP_CUDA(cudaMalloc(&F.d_compact, 4 * std::max(L, 1)));
+  HMGP_CUDA(cudaMemsetAsync(F.d_compact, 0, 4ull * L, st));
+  HMGP_CUDA(cudaMalloc(&F.d_d, 8ull * G.n));
+  HMGP_CUDA(cudaMemsetAsync(F.d_d, 0, 8ull * G.n, st));
+  HMGP_CUDA(cudaMalloc(&F.d_status, sizeof(LeafFactorStatus)));
+  LeafFactorStatus s0{INT_MAX, 0, 0, 0, 0.0, INFINITY};
+  HMGP_CUDA(cudaMemcpyAsync(F.d_status, &s0, sizeof(s0), cudaMemcpyHostToDevice, st));
+  F.clamp_tol = 1e-14 * H.max_diag;  // hfactor.cpp:349
+
+  {
+    Engine E(F, st, arena_bytes);
+    E.factor_diag(0);
+    // compress_all (hfactor.cpp:321-328): every LR leaf, independent
+    std::vector<int> lr;
+    for (int k = 0; k < L; ++k)
+      if (F.leaf[k].kind == LOWRANK) lr.push_back(F.leaf_node[k]);
+    E.compress(lr);
+    int err = 0;
+    HMGP_CUDA(cudaMemcpyAsync(&err, E.d_err, 4, cudaMemcpyDeviceToHost, st));
+    HMGP_CUDA(cudaStreamSynchronize(st));
+    F.arena_peak = E.ar.peak;
+    if (err) throw Error(6, "factorize: low-rank capacity exceeded (code " + std::to_string(err) + ")");
+  }
+  LeafFactorStatus s{};
+  HMGP_CUDA(cudaMemcpyAsync(&s, F.d_status, sizeof(s), cudaMemcpyDeviceToHost, st));
+  HMGP_CUDA(cudaStreamSynchronize(st));
+  F.clamped = s.clamped;
+  F.negative = s.negative;
+  F.min_pivot = s.min_pivot;
+  F.fail_pos = s.fail_pos;
+  F.fail_val = s.fail_val;
+
+  // Cholesky diagonal
+  std::vector<int> dl, db;
+  for (int k = 0; k < L; ++k) {
+    const HNode& nd = F.nodes[F.leaf_node[k]];
+    if (nd.row == nd.col) {
+      dl.push_back(k);
+      db.push_back(G.nbeg[nd.row]);
+    }
+  }
+  F.diag_leaf = dl;
+  if (!ldl) {
+    int *d1, *d2;
+    HMGP_CUDA(cudaMalloc(&d1, 4 * dl.size()));
+    HMGP_CUDA(cudaMalloc(&d2, 4 * dl.size()));
+    HMGP_CUDA(cudaMemcpyAsync(d1, dl.data(), 4 * dl.size(), cudaMemcpyHostToDevice, st));
+    HMGP_CUDA(cudaMemcpyAsync(d2, db.data(), 4 * db.size(), cudaMemcpyHostToDevice, st));
+    k_collect_diag<<<(int)dl.size(), 128, 0, st>>>(F.d_leaf, d1, d2, (int)dl.size(), F.d_d);
+    HMGP_LAUNCH_CHECK();
+    HMGP_CUDA(cudaStreamSynchronize(st));
+    cudaFree(d1);
+    cudaFree(d2);
+  }
+  F.rank_host.resize(L);
+  HMGP_CUDA(cudaMemcpyAsync(F.rank_host.data(), F.d_rank, 4ull * L, cudaMemcpyDeviceToHost, st));
+  HMGP_CUDA(cudaStreamSynchronize(st));
+
+  // ---- solve schedules (column sweep) ----
+  // forward: block applied right after the diagonal leaf holding its last column
+  // backward: block applied right after the diagonal leaf holding its first row
+  const int nd = (int)dl.size();
+  std::vector<int> leaf_of_pos(G.n);
+  for (int t = 0; t < nd; ++t) {
+    const LeafDev& l = F.leaf[dl[t]];
+    for (int i = 0; i < l.m; ++i) leaf_of_pos[db[t] + i] = t;
+  }
+  std::vector<std::vector<SolveBlk>> fw(nd), bw(nd);
+  for (int k = 0; k < L; ++k) {
+    const HNode& nn = F.nodes[F.leaf_node[k]];
+    if (nn.row == nn.col) continue;
+    const int r0 = G.nbeg[nn.row], c0 = G.nbeg[nn.col], c1 = G.nend[nn.col];
+    fw[leaf_of_pos[c1 - 1]].push_back(SolveBlk{k, r0, c0});
+    bw[leaf_of_pos[r0]].push_back(SolveBlk{k, r0, c0});
+  }
+  std::vector<SolveBlk> flat_f, flat_b;
+  F.fwd_off.assign(nd + 1, 0);
+  F.bwd_off.assign(nd + 1, 0);
+  for (int t = 0; t < nd; ++t) {
+    F.fwd_off[t] = (int)flat_f.size();
+    flat_f.insert(flat_f.end(), fw[t].begin(), fw[t].end());
+    F.bwd_off[t] = (int)flat_b.size();
+    flat_b.insert(flat_b.end(), bw[t].begin(), bw[t].end());
+  }
+  F.fwd_off[nd] = (int)flat_f.size();
+  F.bwd_off[nd] = (int)flat_b.size();
+  F.diag_base = db;
+  HMGP_CUDA(cudaMalloc(&F.d_fwd, sizeof(SolveBlk) * std::max<size_t>(1, flat_f.size())));
+  HMGP_CUDA(cudaMalloc(&F.d_bwd, sizeof(SolveBlk) * std::max<size_t>(1, flat_b.size())));
+  HMGP_CUDA(cudaMemcpyAsync(F.d_fwd, flat_f.data(), sizeof(SolveBlk) * flat_f.size(), cudaMemcpyHostToDevice, st));
+  HMGP_CUDA(cudaMemcpyAsync(F.d_bwd, flat_b.data(), sizeof(SolveBlk) * flat_b.size(), cudaMemcpyHostToDevice, st));
+  HMGP_CUDA(cudaMalloc(&F.d_work, 8ull * (2 * G.n + 1024)));
+  HMGP_CUDA(cudaStreamSynchronize(st));
+}
+
+// v (tree order, device) <- L^{-1} v
+void forward_solve(const Factor& F, double* v, cudaStream_t st) {
+  const int nd = (int)F.diag_leaf.size();
+  for (int t = 0; t < nd; ++t) {
+    const LeafDev& l = F.leaf[F.diag_leaf[t]];
+    k_trsv_leaf<<<1, 32, 0, st>>>(l.a, l.m, v + F.diag_base[t], 0);
+    HMGP_LAUNCH_CHECK();
+    const int cnt = F.fwd_off[t + 1] - F.fwd_off[t];
+    if (cnt > 0) {
+      k_solve_apply<<<cnt, 128, 0, st>>>(static_cast<const SolveBlk*>(F.d_fwd) + F.fwd_off[t],
+                                         F.d_leaf, F.d_rank, v, 0);
+      HMGP_LAUNCH_CHECK();
+    }
+  }
+}
+// v <- L^{-T} v
+void backward_solve(const Factor& F, double* v, cudaStream_t st) {
+  const int nd = (int)F.diag_leaf.size();
+  for (int t = nd - 1; t >= 0; --t) {
+    const LeafDev& l = F.leaf[F.diag_leaf[t]];
+    k_trsv_leaf<<<1, 32, 0, st>>>(l.a, l.m, v + F.diag_base[t], 1);
+    HMGP_LAUNCH_CHECK();
+    const int cnt = F.bwd_off[t + 1] - F.bwd_off[t];
+    if (cnt > 0) {
+      k_solve_apply<<<cnt, 128, 0, st>>>(static_cast<const SolveBlk*>(F.d_bwd) + F.bwd_off[t],
+                                         F.d_leaf, F.d_rank, v, 1);
+      HMGP_LAUNCH_CHECK();
+    }
+  }
+}
+
+static double reduce(const Factor& F, const double* v, int mode, cudaStream_t st) {
+  const int n = F.g->n;
+  double* part = F.d_work + 2 * (size_t)n;
+  const int nb = 148;
+  k_reduce_partial<<<nb, 256, 0, st>>>(v, F.d_d, n, mode, part);
+  HMGP_LAUNCH_CHECK();
+  k_reduce_final<<<1, 256, 0, st>>>(part, nb, part + 512);
+  HMGP_LAUNCH_CHECK();
+  double out = 0;
+  HMGP_CUDA(cudaMemcpyAsync(&out, part + 512, 8, cudaMemcpyDeviceToHost, st));
+  HMGP_CUDA(cudaStreamSynchronize(st));
+  return out;
+}
+
+// HFactor::log_det (hfactor.cpp:399-403)
+double factor_log_det(const Factor& F, cudaStream_t st) {
+  const int n = F.g->n;
+  if (F.ldl) {
+    int* cnt = reinterpret_cast<int*>(F.d_work + 2 * (size_t)n + 600);
+    HMGP_CUDA(cudaMemsetAsync(cnt, 0, 4, st));
+    k_count_nonpos<<<148, 256, 0, st>>>(F.d_d, n, cnt);
+    HMGP_LAUNCH_CHECK();
+    int h = 0;
+    HMGP_CUDA(cudaMemcpyAsync(&h, cnt, 4, cudaMemcpyDeviceToHost, st));
+    HMGP_CUDA(cudaStreamSynchronize(st));
+    if (h) throw std::domain_error("indefinite factor");
+    return reduce(F, F.d_d, 2, st);
+  }
+  return 2.0 * reduce(F, F.d_d, 2, st);
+}
+
+// HFactor::quad_form with b in original order on device (hfactor.cpp:389-397)
+double factor_quad_form_dev(const Factor& F, const double* d_b, cudaStream_t st) {
+  const int n = F.g->n;
+  double* v = F.d_work;
+  k_gather<<<(n + 255) / 256, 256, 0, st>>>(d_b, F.g->d_perm, n, v);
+  HMGP_LAUNCH_CHECK();
+  forward_solve(F, v, st);
+  return reduce(F, v, F.ldl ? 1 : 0, st);
+}
+
+// solve_factored / solve_lower with device b, x in original order
+void factor_solve_dev(const Factor& F, const double* d_b, double* d_x, bool full, cudaStream_t st) {
+  const int n = F.g->n;
+  double* v = F.d_work;
+  k_gather<<<(n + 255) / 256, 256, 0, st>>>(d_b, F.g->d_perm, n, v);
+  HMGP_LAUNCH_CHECK();
+  forward_solve(F, v, st);
+  if (full) {
+    if (F.ldl) {
+      k_div<<<(n + 255) / 256, 256, 0, st>>>(v, F.d_d, n);
+      HMGP_LAUNCH_CHECK();
+    }
+    backward_solve(F, v, st);
+  }
+  k_scatter<<<(n + 255) / 256, 256, 0, st>>>(v, F.g->d_perm, n, d_x);
+  HMGP_LAUNCH_CHECK();
+}
+
+double factor_storage_bytes(const Factor& F) {  // hfactor.cpp:412-419
+  double b = 0;
+  for (size_t k = 0; k < F.leaf.size(); ++k) {
+    const LeafDev& l = F.leaf[k];
+    b += l.kind == DENSE ? 8.0 * l.m * l.n : 8.0 * (l.m + l.n) * F.rank_host[k];
+  }
+  if (F.ldl) b += 8.0 * F.g->n;
+  return b;
+}
+
+}  // namespace hmgp_gpu

@@ -1,0 +1,50 @@
+// H-factor object and entry points (hfactor.hpp:34-77).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "hmgp_internal.h"
+#include "linalg.cuh"
+
+namespace hmgp_gpu {
+
+struct Trip {  // sub_product target and operands: C -= A diag(d) B^T
+  int c, a, b;
+};
+
+struct Factor {
+  Geometry* g = nullptr;  // non-owning, like HFactor::tree_ (hfactor.hpp:63)
+  bool ldl = true;
+  double eps = 1e-6;
+  std::vector<HNode> nodes;
+  std::vector<int> leaf_node;
+  std::vector<LeafDev> leaf;
+  double* pool = nullptr;
+  LeafDev* d_leaf = nullptr;
+  int* d_rank = nullptr;
+  int* d_compact = nullptr;
+  double* d_d = nullptr;  // D (LDL) or L_ii (Cholesky), tree order
+  LeafFactorStatus* d_status = nullptr;
+  double clamp_tol = 0.0;
+  int clamped = 0, negative = 0, fail_pos = 0;
+  double min_pivot = 0.0, fail_val = 0.0;
+  std::vector<int> rank_host;
+  std::vector<int> diag_leaf, diag_base, fwd_off, bwd_off;
+  void* d_fwd = nullptr;
+  void* d_bwd = nullptr;
+  double* d_work = nullptr;
+  size_t arena_peak = 0;
+  ~Factor();
+};
+
+void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size_t arena_bytes);
+void forward_solve(const Factor& F, double* v, cudaStream_t st);
+void backward_solve(const Factor& F, double* v, cudaStream_t st);
+double factor_log_det(const Factor& F, cudaStream_t st);
+double factor_quad_form_dev(const Factor& F, const double* d_b, cudaStream_t st);
+void factor_solve_dev(const Factor& F, const double* d_b, double* d_x, bool full, cudaStream_t st);
+double factor_storage_bytes(const Factor& F);
+
+}  // namespace hmgp_gpu

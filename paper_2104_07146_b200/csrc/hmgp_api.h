@@ -1,0 +1,45 @@
+// Opaque handle definitions behind include/hmgp_cuda.h and the internal entry
+// points the C ABI dispatches to.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <vector>
+
+#include "../../include/hmgp_cuda.h"
+#include "hmgp_internal.h"
+
+struct hmgp_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+};
+struct hmgp_geom {
+  hmgp_gpu::Geometry g;
+};
+struct hmgp_hmat {
+  hmgp_gpu::HMat h;
+};
+namespace hmgp_gpu {
+struct Factor;
+}
+struct hmgp_factor {
+  std::unique_ptr<hmgp_gpu::Factor> f;
+  ~hmgp_factor();
+};
+
+void hmgp_set_pivot(int idx, double v);
+void hmgp_validate_matern(const hmgp_matern* p);
+
+namespace hmgp_gpu {
+double normal_quantile_host(double p);
+bool device_all_finite(const double* d_x, size_t count, cudaStream_t st);
+void kernel_pairs(cudaStream_t st, const double* coords, int n, int dim, const MaternDev& p,
+                  const int32_t* ii, const int32_t* jj, int64_t count, double* out);
+void at_distance(cudaStream_t st, const MaternDev& p, const double* h, int64_t count, double* out);
+void bessel_batch(cudaStream_t st, const double* nu, const double* x, int64_t count, int generic,
+                  double* out);
+void hmat_matvec(cudaStream_t st, const HMat& h, const double* x, double* y);
+// K12: d_out[i] = sum_j at_distance(|test_i - train_j|) d_w[j] (all device, AoS coords)
+void cross_apply(cudaStream_t st, const double* d_train, int n, int dim, const double* d_w,
+                 const double* d_test, int m, const MaternDev& p, double* d_out);
+}  // namespace hmgp_gpu

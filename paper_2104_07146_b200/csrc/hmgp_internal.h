@@ -1,0 +1,127 @@
+// Internal (non-ABI) data structures of the hmgp B200 library.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <array>
+#include <memory>
+#include <vector>
+
+#include "matern.cuh"
+
+namespace hmgp_gpu {
+
+// Block-tree node as emitted by the device frontier expansion (K2).
+struct BlockNodeRec {
+  int row, col;
+  int tag;  // 0 admissible, 1 dense, 2 split
+  int depth;
+  uint64_t key;  // base-4 DFS path key
+};
+
+// Cluster tree + block tree for one point set (θ-independent).
+struct Geometry {
+  int n = 0, dim = 2, leaf_size = 32, depth = 0;
+  double eta = 2.0;
+  // host tree (pre-order node ids, same numbering as the reference recursion)
+  std::vector<int> nbeg, nend, nleft, nright, nlevel, axis;
+  std::vector<double> box;  // 6 per node: lo[3], hi[3]
+  std::vector<int> perm, iperm;
+  // block tree in DFS pre-order; bkids[i] row-major children
+  std::vector<BlockNodeRec> bnodes;
+  std::vector<std::vector<int>> bkids;
+  std::vector<int> leaves;  // indices into bnodes, DFS order
+  int n_adm = 0, n_dense = 0;
+  // device
+  double* d_x = nullptr;   // AoS input coordinates (original order)
+  double* d_xt = nullptr;  // SoA coordinates in tree order: xt[d*n + k]
+  int *d_perm = nullptr, *d_iperm = nullptr;
+  double* d_box = nullptr;
+  int *d_nbeg = nullptr, *d_nend = nullptr, *d_left = nullptr, *d_right = nullptr;
+};
+
+void geometry_build(Geometry& g, cudaStream_t st);
+void geometry_free(Geometry& g);
+
+// ---------------------------------------------------------------- H-matrix --
+enum Kind { BRANCH = 0, DENSE = 1, LOWRANK = 2 };
+
+// Device-side description of one stored leaf.  Dense: a = D (m x n, ld m).
+// Low-rank: a = U (m x cap, ld m), b = V (n x cap, ld n); rank/compact live in
+// separate device int arrays so kernels can grow/shrink them without the host.
+struct LeafDev {
+  double* a;
+  double* b;
+  int m, n;
+  int kind;
+  int cap;
+};
+
+// Host payload node (mirror of HBlock, hblock.hpp:17-45).
+struct HNode {
+  int kind = BRANCH;
+  int row = 0, col = 0;     // cluster node ids
+  int kids[4] = {-1, -1, -1, -1};  // row-major, -1 = null (upper mirror)
+  int kr = 1, kc = 1;
+  int leaf = -1;  // index into the leaf table (stored leaves)
+};
+
+struct DeviceArena;
+
+struct HMat {
+  Geometry* g = nullptr;
+  MaternDev p{};
+  double eps = 1e-6;
+  bool fixed_rank = false;
+  int rank_k = 16, max_rank = 256;
+  std::vector<HNode> nodes;  // node 0 = root
+  std::vector<int> leaf_node;  // stored leaf -> node id (DFS order)
+  std::vector<LeafDev> leaf;   // host copy of the table
+  LeafDev* d_leaf = nullptr;   // device copy
+  int* d_rank = nullptr;       // per stored leaf (low-rank: rank; dense: -1)
+  int* d_compact = nullptr;
+  std::vector<int> rank_host;  // snapshot after assembly
+  double* pool = nullptr;      // one allocation for all payload
+  size_t pool_doubles = 0;
+  double max_diag = 0.0;
+  int n_dense_leaves = 0, n_lr_leaves = 0;
+  ~HMat();
+};
+
+// Assembly (K3 dense leaves, K4 batched ACA + K5 truncation), hmatrix.cpp:174-221.
+void assemble(HMat& h, Geometry& g, const MaternDev& p, double eps, bool fixed_rank, int rank_k,
+              int max_rank, cudaStream_t st, double* stats);
+
+MaternDev make_matern(double sigma2, double ell, double nu, double tau2);
+
+// ------------------------------------------------------------ kernels API --
+// Batched low-rank update / recompression item (one CTA each).  The target
+// holds U (m x cap, ld m), V (n x cap, ld n) with *rank current columns.  Optional
+// appended columns alpha*P (rows [pro, pro+pr) of U) and Q (rows [qro, qro+qr) of V)
+// with `add` columns (hblock.cpp:186-199).  With cols = rank + add the condition
+// decides between a plain append and a recompression of the concatenation
+// (hblock.cpp:127-162 with empty P, Q — every reference call site):
+//   cond 0: cols > 0 (compress_low_rank)   1: cols > 16 (fill_leaf)
+//   cond 2: cols > compact + 16 (watermark) 3: cols > 48 (product accumulation)
+//   cond 4: never (pure append)
+struct TruncItem {
+  double* U;
+  double* V;
+  int m, n;
+  int* rank;
+  int* compact;  // optional; set to the new column count after the op when cond 0/2
+  int cond;
+  int cap;  // target column capacity
+  const double* P;
+  const double* Q;
+  int ldp, ldq, pr, qr, pro, qro;
+  const int* addp;  // device column count of P (nullptr -> addv)
+  int addv;
+  double alpha;
+  int rcap;    // workspace column capacity (>= rank + add)
+  double* ws;  // trunc_ws_doubles(m, n, rcap)
+};
+size_t trunc_ws_doubles(int m, int n, int rcap);
+void launch_truncate(const TruncItem* d_items, int count, double eps, int* d_err, cudaStream_t st);
+
+}  // namespace hmgp_gpu

@@ -1,0 +1,337 @@
+// Batched FP64 building blocks of the H-factorization (see linalg.cuh).
+//   GEMM      hblk::apply / multiply / add_low_rank dense update (hblock.cpp:46-92,181-184)
+//   TRSM      solveInPlace variants (hfactor.cpp:78,92,109,201,205)
+//   leaf LDL  dense_ldl_leaf / dense_cholesky_leaf (hfactor.cpp:22-73)
+#include <climits>
+
+#include "common.cuh"
+#include "linalg.cuh"
+
+namespace hmgp_gpu {
+
+// ----------------------------------------------------------------- GEMM ---
+// 64x64 output tile per CTA iteration, k-slabs of 16 staged in shared memory,
+// 256 threads x (4 x 4) register micro-tile.  Dimensions may live on device.
+constexpr int GT = 64, GK = 16;
+
+__global__ void __launch_bounds__(256) k_gemm(const GemmItem* __restrict__ items) {
+  const GemmItem it = items[blockIdx.x];
+  const int M = it.M.get(), N = it.N.get(), K = it.K.get();
+  if (M <= 0 || N <= 0) return;
+  const int tm = (M + GT - 1) / GT, tn = (N + GT - 1) / GT;
+  __shared__ double sA[GK][GT + 1];
+  __shared__ double sB[GK][GT + 1];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  for (int tile = blockIdx.y; tile < tm * tn; tile += gridDim.y) {
+    const int i0 = (tile % tm) * GT, j0 = (tile / tm) * GT;
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    for (int k0 = 0; k0 < K; k0 += GK) {
+      __syncthreads();
+      for (int e = threadIdx.x; e < GK * GT; e += 256) {
+        int kk, ii;
+        // A tile: op(A)[i0+ii, k0+kk]
+        if (!it.ta) {
+          ii = e % GT;
+          kk = e / GT;
+        } else {
+          kk = e % GK;
+          ii = e / GK;
+        }
+        const int gi = i0 + ii, gk = k0 + kk;
+        double v = 0.0;
+        if (gi < M && gk < K)
+          v = it.ta ? it.A[(size_t)gi * it.lda + gk] : it.A[(size_t)gk * it.lda + gi];
+        sA[kk][ii] = v;
+        // B tile: op(B)[k0+kk, j0+jj]
+        int jj;
+        if (!it.tb) {
+          kk = e % GK;
+          jj = e / GK;
+        } else {
+          jj = e % GT;
+          kk = e / GT;
+        }
+        const int gj = j0 + jj, gk2 = k0 + kk;
+        double w = 0.0;
+        if (gj < N && gk2 < K)
+          w = it.tb ? it.B[(size_t)gk2 * it.ldb + gj] : it.B[(size_t)gj * it.ldb + gk2];
+        sB[kk][jj] = w;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < GK; ++kk) {
+        double a[4], b[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          a[q] = sA[kk][tx + 16 * q];
+          b[q] = sB[kk][ty + 16 * q];
+        }
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[p][q] += a[p] * b[q];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int gj = j0 + ty + 16 * q;
+      if (gj >= N) continue;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const int gi = i0 + tx + 16 * p;
+        if (gi < M) it.C[(size_t)gj * it.ldc + gi] += it.alpha * acc[p][q];
+      }
+    }
+  }
+}
+
+void launch_gemm(const GemmItem* d_items, int count, int max_tiles, cudaStream_t st) {
+  if (count <= 0) return;
+  const int ty = max(1, min(max_tiles, 64));
+  k_gemm<<<dim3(count, ty), 256, 0, st>>>(d_items);
+  HMGP_LAUNCH_CHECK();
+}
+
+// ----------------------------------------------------------------- TRSM ---
+// Left: one warp per right-hand-side column, lanes over rows (coalesced).
+__global__ void k_trsm_left(const TrsmLItem* __restrict__ items) {
+  const TrsmLItem it = items[blockIdx.x];
+  const int cols = it.cols.get();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int b = it.b;
+  for (int c = blockIdx.y * nw + w; c < cols; c += gridDim.y * nw) {
+    double* x = it.M + (size_t)c * it.ldm;
+    if (!it.trans) {
+      for (int j = 0; j < b; ++j) {
+        const double xj = x[j] / it.L[(size_t)j * it.ldl + j];
+        __syncwarp();
+        if (lane == 0) x[j] = xj;
+        const double* lc = it.L + (size_t)j * it.ldl;
+        for (int i = j + 1 + lane; i < b; i += 32) x[i] -= lc[i] * xj;
+        __syncwarp();
+      }
+    } else {
+      for (int j = b - 1; j >= 0; --j) {
+        const double* lc = it.L + (size_t)j * it.ldl;
+        double s = 0.0;
+        for (int i = j + 1 + lane; i < b; i += 32) s += lc[i] * x[i];
+        s = warp_sum(s);
+        if (lane == 0) x[j] = (x[j] - s) / lc[j];
+        __syncwarp();
+      }
+    }
+  }
+}
+
+void launch_trsm_left(const TrsmLItem* d_items, int count, int max_cols, cudaStream_t st) {
+  if (count <= 0) return;
+  const int gy = max(1, min((max_cols + 7) / 8, 32));
+  k_trsm_left<<<dim3(count, gy), 256, 0, st>>>(d_items);
+  HMGP_LAUNCH_CHECK();
+}
+
+// Right: X <- X L^{-T}, one thread per row of X.
+__global__ void k_trsm_right(const TrsmRItem* __restrict__ items) {
+  const TrsmRItem it = items[blockIdx.x];
+  for (int r = blockIdx.y * blockDim.x + threadIdx.x; r < it.s; r += gridDim.y * blockDim.x) {
+    for (int j = 0; j < it.t; ++j) {
+      const double xj = it.X[(size_t)j * it.ldx + r] / it.L[(size_t)j * it.ldl + j];
+      it.X[(size_t)j * it.ldx + r] = xj;
+      const double* lc = it.L + (size_t)j * it.ldl;
+      for (int c = j + 1; c < it.t; ++c) it.X[(size_t)c * it.ldx + r] -= xj * lc[c];
+    }
+  }
+}
+
+void launch_trsm_right(const TrsmRItem* d_items, int count, int max_rows, cudaStream_t st) {
+  if (count <= 0) return;
+  const int gy = max(1, min((max_rows + 127) / 128, 64));
+  k_trsm_right<<<dim3(count, gy), 128, 0, st>>>(d_items);
+  HMGP_LAUNCH_CHECK();
+}
+
+// ----------------------------------------------------------- copy/scale ---
+__global__ void k_copy_scale(const CopyScaleItem* __restrict__ items) {
+  const CopyScaleItem it = items[blockIdx.x];
+  const int cols = it.cols.get();
+  if (it.set_cols && blockIdx.y == 0 && threadIdx.x == 0) *it.set_cols = cols;
+  const size_t tot = (size_t)it.rows * cols;
+  for (size_t e = blockIdx.y * (size_t)blockDim.x + threadIdx.x; e < tot;
+       e += (size_t)gridDim.y * blockDim.x) {
+    const int i = (int)(e % it.rows), j = (int)(e / it.rows);
+    double v;
+    if (it.src)
+      v = it.trans ? it.src[(size_t)i * it.lds + j] : it.src[(size_t)j * it.lds + i];
+    else
+      v = (i == j) ? 1.0 : 0.0;
+    v *= it.alpha;
+    switch (it.mode) {
+      case 1:
+        v *= it.d[i];
+        break;
+      case 2:
+        v /= it.d[i];
+        break;
+      case 3:
+        v *= it.d[j];
+        break;
+      case 4:
+        v /= it.d[j];
+        break;
+      default:
+        break;
+    }
+    if (it.accum)
+      it.dst[(size_t)j * it.ldd + i] += v;
+    else
+      it.dst[(size_t)j * it.ldd + i] = v;
+  }
+}
+
+void launch_copy_scale(const CopyScaleItem* d_items, int count, int max_elems, cudaStream_t st) {
+  if (count <= 0) return;
+  const int gy = max(1, min((max_elems + 255) / 256, 64));
+  k_copy_scale<<<dim3(count, gy), 256, 0, st>>>(d_items);
+  HMGP_LAUNCH_CHECK();
+}
+
+// --------------------------------------------------------------- append ---
+// hblock.cpp:186-199: U(:, r0:r0+add) = [0; alpha P; 0], V(:, r0:r0+add) = [0; Q; 0]
+__global__ void k_append(const AppendItem* __restrict__ items, int* err) {
+  const AppendItem it = items[blockIdx.x];
+  const int r0 = *it.rank, add = it.add.get();
+  if (add <= 0) return;
+  if (r0 + add > it.cap) {
+    if (blockIdx.y == 0 && threadIdx.x == 0) atomicOr(err, 2);
+    return;
+  }
+  const size_t tu = (size_t)it.um * add, tv = (size_t)it.vn * add;
+  for (size_t e = blockIdx.y * (size_t)blockDim.x + threadIdx.x; e < tu + tv;
+       e += (size_t)gridDim.y * blockDim.x) {
+    if (e < tu) {
+      const int i = (int)(e % it.um), k = (int)(e / it.um);
+      const int pi = i - it.pro;
+      const double v = (pi >= 0 && pi < it.pr) ? it.alpha * it.P[(size_t)k * it.ldp + pi] : 0.0;
+      it.U[(size_t)(r0 + k) * it.um + i] = v;
+    } else {
+      const size_t f = e - tu;
+      const int i = (int)(f % it.vn), k = (int)(f / it.vn);
+      const int qi = i - it.qro;
+      const double v = (qi >= 0 && qi < it.qr) ? it.Q[(size_t)k * it.ldq + qi] : 0.0;
+      it.V[(size_t)(r0 + k) * it.vn + i] = v;
+    }
+  }
+}
+
+// rank update after all CTAs of the item are done: separate tiny kernel
+__global__ void k_append_commit(const AppendItem* __restrict__ items, int count) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  const AppendItem it = items[t];
+  const int r0 = *it.rank, add = it.add.get();
+  if (add > 0 && r0 + add <= it.cap) *it.rank = r0 + add;
+}
+
+void launch_append(const AppendItem* d_items, int count, int max_elems, int* d_err, cudaStream_t st) {
+  if (count <= 0) return;
+  const int gy = max(1, min((max_elems + 255) / 256, 64));
+  k_append<<<dim3(count, gy), 256, 0, st>>>(d_items, d_err);
+  HMGP_LAUNCH_CHECK();
+  k_append_commit<<<(count + 127) / 128, 128, 0, st>>>(d_items, count);
+  HMGP_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------------ leaf LDL ----
+__device__ __forceinline__ void atomic_min_double(double* addr, double v) {
+  unsigned long long* a = reinterpret_cast<unsigned long long*>(addr);
+  unsigned long long old = *a;
+  while (v < __longlong_as_double(old)) {
+    const unsigned long long prev = atomicCAS(a, old, __double_as_longlong(v));
+    if (prev == old) break;
+    old = prev;
+  }
+}
+
+// Unblocked left-looking column factorization, the reference's loop order
+// (hfactor.cpp:22-73); the leaf lives in dynamic shared memory when it fits.
+__global__ void k_leaf_factor(double* __restrict__ Dg, int b, int base, int ldl, double* __restrict__ d,
+                              double clamp_tol, LeafFactorStatus* st, int use_smem) {
+  extern __shared__ double sm[];
+  __shared__ double red[32];
+  __shared__ double s_piv;
+  double* A = use_smem ? sm : Dg;
+  if (use_smem)
+    for (int e = threadIdx.x; e < b * b; e += blockDim.x) A[e] = Dg[e];
+  __syncthreads();
+  for (int j = 0; j < b; ++j) {
+    double part = 0.0;
+    for (int k = threadIdx.x; k < j; k += blockDim.x) {
+      const double l = A[(size_t)k * b + j];
+      part += ldl ? l * l * d[base + k] : l * l;
+    }
+    const double sum = block_sum(part, red);
+    if (threadIdx.x == 0) {
+      double s = A[(size_t)j * b + j] - sum;
+      atomic_min_double(&st->min_pivot, s);
+      bool failed;
+      if (ldl) {
+        failed = (s == 0.0);
+        if (s < 0.0) {
+          if (-s <= clamp_tol) {
+            s = clamp_tol;
+            atomicAdd(&st->clamped, 1);
+          } else {
+            atomicAdd(&st->negative, 1);
+          }
+        }
+      } else {
+        failed = !(s > 0.0);
+      }
+      if (failed) {
+        const int pos = base + j;
+        if (atomicMin(&st->fail_pos, pos) > pos) st->fail_val = s;
+      }
+      s_piv = s;
+    }
+    __syncthreads();
+    const double s = s_piv;
+    const double piv = ldl ? s : sqrt(s);
+    if (threadIdx.x == 0) {
+      if (ldl) d[base + j] = s;
+      A[(size_t)j * b + j] = ldl ? 1.0 : piv;
+    }
+    for (int i = j + 1 + threadIdx.x; i < b; i += blockDim.x) {
+      double v = A[(size_t)j * b + i];
+      for (int k = 0; k < j; ++k) {
+        const double t = A[(size_t)k * b + i] * A[(size_t)k * b + j];
+        v -= ldl ? t * d[base + k] : t;
+      }
+      A[(size_t)j * b + i] = v / piv;
+    }
+    __syncthreads();
+  }
+  // zero the strict upper triangle (hfactor.cpp:41,72)
+  for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
+    const int i = e % b, j = e / b;
+    const double v = i < j ? 0.0 : A[e];
+    Dg[e] = v;
+  }
+}
+
+void launch_leaf_factor(double* D, int b, int base, int ldl, double* d, double clamp_tol,
+                        LeafFactorStatus* status, cudaStream_t st) {
+  const size_t bytes = (size_t)b * b * 8;
+  const int use_smem = bytes <= 200 * 1024;
+  if (use_smem && bytes > 48 * 1024)
+    HMGP_CUDA(cudaFuncSetAttribute(k_leaf_factor, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)bytes));
+  k_leaf_factor<<<1, 256, use_smem ? bytes : 0, st>>>(D, b, base, ldl, d, clamp_tol, status,
+                                                       use_smem);
+  HMGP_LAUNCH_CHECK();
+}
+
+}  // namespace hmgp_gpu

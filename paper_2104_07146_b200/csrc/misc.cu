@@ -1,0 +1,251 @@
+// Entry-level kernels (parity hooks), H-matvec, K12 kriging cross-covariance,
+// and host-side input utilities.
+#include <cmath>
+#include <stdexcept>
+#include <vector>
+
+#include "common.cuh"
+#include "hmgp_api.h"
+#include "hmgp_internal.h"
+
+namespace hmgp_gpu {
+
+namespace {
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  explicit DBuf(size_t n) { HMGP_CUDA(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T))); }
+  ~DBuf() { cudaFree(p); }
+};
+}  // namespace
+
+__global__ void k_all_finite(const double* __restrict__ x, size_t count, int* bad) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count;
+       i += (size_t)gridDim.x * blockDim.x)
+    if (!isfinite(x[i])) *bad = 1;
+}
+
+bool device_all_finite(const double* d_x, size_t count, cudaStream_t st) {
+  DBuf<int> bad(1);
+  HMGP_CUDA(cudaMemsetAsync(bad.p, 0, 4, st));
+  k_all_finite<<<kSMs * 4, 256, 0, st>>>(d_x, count, bad.p);
+  HMGP_LAUNCH_CHECK();
+  int h = 0;
+  HMGP_CUDA(cudaMemcpyAsync(&h, bad.p, 4, cudaMemcpyDeviceToHost, st));
+  HMGP_CUDA(cudaStreamSynchronize(st));
+  return h == 0;
+}
+
+__global__ void k_kernel_pairs(const double* __restrict__ x, int dim, MaternDev p,
+                               const int* __restrict__ ii, const int* __restrict__ jj,
+                               int64_t count, double* __restrict__ out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int a = ii[t], b = jj[t];
+    if (a == b) {
+      out[t] = p.sigma2 + p.tau2;
+      continue;
+    }
+    const double* pa = x + (size_t)a * dim;
+    const double* pb = x + (size_t)b * dim;
+    const double h = dim == 2 ? dist2d(pa[0], pa[1], pb[0], pb[1])
+                              : dist3d(pa[0], pa[1], pa[2], pb[0], pb[1], pb[2]);
+    out[t] = matern_at(p, h);
+  }
+}
+
+void kernel_pairs(cudaStream_t st, const double* coords, int n, int dim, const MaternDev& p,
+                  const int32_t* ii, const int32_t* jj, int64_t count, double* out) {
+  if (count <= 0) return;
+  DBuf<double> dx((size_t)n * dim), dout(count);
+  DBuf<int> di(count), dj(count);
+  HMGP_CUDA(cudaMemcpyAsync(dx.p, coords, 8ull * n * dim, cudaMemcpyHostToDevice, st));
+  HMGP_CUDA(cudaMemcpyAsync(di.p, ii, 4ull * count, cudaMemcpyHostToDevice, st));
+  HMGP_CUDA(cudaMemcpyAsync(dj.p, jj, 4ull * count, cudaMemcpyHostToDevice, st));
+  k_kernel_pairs<<<kSMs * 8, 256, 0, st>>>(dx.p, dim, p, di.p, dj.p, count, dout.p);
+  HMGP_LAUNCH_CHECK();
+  HMGP_CUDA(cudaMemcpyAsync(out, dout.p, 8ull * count, cudaMemcpyDeviceToHost, st));
+  HMGP_CUDA(cudaStreamSynchronize(st));
+}
+
+__global__ void k_at_distance(MaternDev p, const double* __restrict__ h, int64_t count,
+                              double* __restrict__ out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count;
+       t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = matern_at(p, h[t]);
+}
+
+void at_distance(cudaStream_t st, const MaternDev& p, const double* h, int64_t count, double* out) {
+  if (count <= 0) return;
+  DBuf<double> dh(count), dout(count);
+  HMGP_CUDA(cudaMemcpyAsync(dh.p, h, 8ull * count, cudaMemcpyHostToDevice, st));
+  k_at_distance<<<kSMs * 8, 256, 0, st>>>(p, dh.p, count, dout.p);
+  HMGP_LAUNCH_CHECK();
+  HMGP_CUDA(cudaMemcpyAsync(out, dout.p, 8ull * count, cudaMemcpyDeviceToHost, st));
+  HMGP_CUDA(cudaStreamSynchronize(st));
+}
+
+__global__ void k_bessel(const double* __restrict__ nu, const double* __restrict__ x, int64_t count,
+                         int generic, double* __restrict__ out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const double v = nu[t], z = x[t];
+    const double hs = v - 0.5;
+    if (!generic && hs == floor(hs) && hs >= 0.0)  // covkernel.cpp:200-202
+      out[t] = bessel_half((int)hs, z);
+    else
+      out[t] = bessel_k_generic_dev(v, z);
+  }
+}
+
+void bessel_batch(cudaStream_t st, const double* nu, const double* x, int64_t count, int generic,
+                  double* out) {
+  if (count <= 0) return;
+  DBuf<double> dn(count), dx(count), dout(count);
+  HMGP_CUDA(cudaMemcpyAsync(dn.p, nu, 8ull * count, cudaMemcpyHostToDevice, st));
+  HMGP_CUDA(cudaMemcpyAsync(dx.p, x, 8ull * count, cudaMemcpyHostToDevice, st));
+  k_bessel<<<kSMs * 8, 256, 0, st>>>(dn.p, dx.p, count, generic, dout.p);
+  HMGP_LAUNCH_CHECK();
+  HMGP_CUDA(cudaMemcpyAsync(out, dout.p, 8ull * count, cudaMemcpyDeviceToHost, st));
+  HMGP_CUDA(cudaStreamSynchronize(st));
+}
+
+// ------------------------------------------------------------- H-matvec ---
+// One CTA per stored leaf; y (tree order) accumulated with FP64 atomics.
+__global__ void k_leaf_matvec(const LeafDev* __restrict__ lf, const int* __restrict__ rank,
+                              const int* __restrict__ r0, const int* __restrict__ c0,
+                              const double* __restrict__ xt, double* __restrict__ yt,
+                              double* __restrict__ scratch, int sym_stride) {
+  const int k = blockIdx.x;
+  const LeafDev L = lf[k];
+  const int rb = r0[k], cb = c0[k];
+  const bool mirror = rb != cb;
+  double* t = scratch + (size_t)k * sym_stride;  // 2 * cap doubles
+  if (L.kind == DENSE) {
+    for (int i = threadIdx.x; i < L.m; i += blockDim.x) {
+      double s = 0.0;
+      for (int j = 0; j < L.n; ++j) s += L.a[(size_t)j * L.m + i] * xt[cb + j];
+      atomicAdd(&yt[rb + i], s);
+    }
+    if (mirror)
+      for (int j = threadIdx.x; j < L.n; j += blockDim.x) {
+        double s = 0.0;
+        for (int i = 0; i < L.m; ++i) s += L.a[(size_t)j * L.m + i] * xt[rb + i];
+        atomicAdd(&yt[cb + j], s);
+      }
+    return;
+  }
+  const int r = rank[k];
+  if (r <= 0) return;
+  for (int l = threadIdx.x; l < r; l += blockDim.x) {
+    double s = 0.0, s2 = 0.0;
+    for (int j = 0; j < L.n; ++j) s += L.b[(size_t)l * L.n + j] * xt[cb + j];
+    for (int i = 0; i < L.m; ++i) s2 += L.a[(size_t)l * L.m + i] * xt[rb + i];
+    t[l] = s;
+    t[L.cap + l] = s2;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < L.m; i += blockDim.x) {
+    double s = 0.0;
+    for (int l = 0; l < r; ++l) s += L.a[(size_t)l * L.m + i] * t[l];
+    atomicAdd(&yt[rb + i], s);
+  }
+  if (mirror)
+    for (int j = threadIdx.x; j < L.n; j += blockDim.x) {
+      double s = 0.0;
+      for (int l = 0; l < r; ++l) s += L.b[(size_t)l * L.n + j] * t[L.cap + l];
+      atomicAdd(&yt[cb + j], s);
+    }
+}
+
+__global__ void k_permute_in(const double* __restrict__ x, const int* __restrict__ perm, int n,
+                             double* __restrict__ xt) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) xt[k] = x[perm[k]];
+}
+__global__ void k_permute_out(const double* __restrict__ yt, const int* __restrict__ perm, int n,
+                              double* __restrict__ y) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) y[perm[k]] = yt[k];
+}
+
+void hmat_matvec(cudaStream_t st, const HMat& h, const double* x, double* y) {
+  const Geometry& G = *h.g;
+  const int n = G.n, L = (int)h.leaf.size();
+  std::vector<int> r0(L), c0(L);
+  int maxcap = 1;
+  for (int k = 0; k < L; ++k) {
+    const HNode& nd = h.nodes[h.leaf_node[k]];
+    r0[k] = G.nbeg[nd.row];
+    c0[k] = G.nbeg[nd.col];
+    maxcap = std::max(maxcap, h.leaf[k].cap);
+  }
+  DBuf<double> dx(n), dxt(n), dyt(n), scratch((size_t)L * 2 * maxcap);
+  DBuf<int> dr0(L), dc0(L);
+  HMGP_CUDA(cudaMemcpyAsync(dx.p, x, 8ull * n, cudaMemcpyHostToDevice, st));
+  HMGP_CUDA(cudaMemcpyAsync(dr0.p, r0.data(), 4ull * L, cudaMemcpyHostToDevice, st));
+  HMGP_CUDA(cudaMemcpyAsync(dc0.p, c0.data(), 4ull * L, cudaMemcpyHostToDevice, st));
+  HMGP_CUDA(cudaMemsetAsync(dyt.p, 0, 8ull * n, st));
+  k_permute_in<<<(n + 255) / 256, 256, 0, st>>>(dx.p, G.d_perm, n, dxt.p);
+  HMGP_LAUNCH_CHECK();
+  k_leaf_matvec<<<L, 128, 0, st>>>(h.d_leaf, h.d_rank, dr0.p, dc0.p, dxt.p, dyt.p, scratch.p,
+                                   2 * maxcap);
+  HMGP_LAUNCH_CHECK();
+  k_permute_out<<<(n + 255) / 256, 256, 0, st>>>(dyt.p, G.d_perm, n, dx.p);
+  HMGP_LAUNCH_CHECK();
+  HMGP_CUDA(cudaMemcpyAsync(y, dx.p, 8ull * n, cudaMemcpyDeviceToHost, st));
+  HMGP_CUDA(cudaStreamSynchronize(st));
+}
+
+// ------------------------------------------------------- AS241 (host) -----
+// Wichura AS241 PPND16 (simgen.cpp:9-106); published coefficients.
+double normal_quantile_host(double p) {
+  if (!(p > 0.0 && p < 1.0)) throw std::domain_error("std_normal_quantile: p must be in (0, 1)");
+  const double q = p - 0.5;
+  auto horner = [](const double* c, double r) {
+    double v = c[7];
+    for (int k = 6; k >= 0; --k) v = v * r + c[k];
+    return v;
+  };
+  if (std::fabs(q) <= 0.425) {
+    static const double a[8] = {3.3871328727963666080e+0, 1.3314166789178437745e+2,
+                                1.9715909503065514427e+3, 1.3731693765509461125e+4,
+                                4.5921953931549871457e+4, 6.7265770927008700853e+4,
+                                3.3430575583588128105e+4, 2.5090809287301226727e+3};
+    static const double b[8] = {1.0, 4.2313330701600911252e+1, 6.8718700749205790830e+2,
+                                5.3941960214247511077e+3, 2.1213794301586595867e+4,
+                                3.9307895800092710610e+4, 2.8729085735721942674e+4,
+                                5.226495278852545609e+3};
+    const double r = 0.180625 - q * q;
+    return q * horner(a, r) / horner(b, r);
+  }
+  double r = q < 0.0 ? p : 1.0 - p;
+  r = std::sqrt(-std::log(r));
+  double x;
+  if (r <= 5.0) {
+    static const double c[8] = {1.42343711074968357734e+0, 4.63033784615654529590e+0,
+                                5.76949722146069140550e+0, 3.64784832476320460504e+0,
+                                1.27045825245236838258e+0, 2.41780725177450611770e-1,
+                                2.27238449892691845833e-2, 7.74545014278341407640e-4};
+    static const double d[8] = {1.0, 2.05319162663775882187e+0, 1.67638483018380384940e+0,
+                                6.89767334985100004550e-1, 1.48103976427480074590e-1,
+                                1.51986665636164571966e-2, 5.47593808499534494600e-4,
+                                1.05075007164441684324e-9};
+    r -= 1.6;
+    x = horner(c, r) / horner(d, r);
+  } else {
+    static const double e[8] = {6.65790464350110377720e+0, 5.46378491116411436990e+0,
+                                1.78482653991729133580e+0, 2.96560571828504891230e-1,
+                                2.65321895265761230930e-2, 1.24266094738807843860e-3,
+                                2.71155556874348757815e-5, 2.01033439929228813265e-7};
+    static const double f[8] = {1.0, 5.99832206555887937690e-1, 1.36929880922735805310e-1,
+                                1.48753612908506148525e-2, 7.868691311456132591e-4,
+                                1.8463183175100546818e-5, 1.4215117583164458887e-7,
+                                2.04426310338993978564e-15};
+    r -= 5.0;
+    x = horner(e, r) / horner(f, r);
+  }
+  return q < 0.0 ? -x : x;
+}
+
+}  // namespace hmgp_gpu

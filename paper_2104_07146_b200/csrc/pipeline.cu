@@ -1,0 +1,315 @@
+// Pipeline entry points of the C ABI: factorize / solves / L(θ) / θ-batch /
+// predict, and K12 (the streamed kriging cross-covariance product).
+//   evaluate_loglik  loglik.cpp:18-38      predict  krige.cpp:9-44
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "../../include/hmgp_cuda.h"
+#include "common.cuh"
+#include "factor.h"
+#include "hmgp_api.h"
+
+using namespace hmgp_gpu;
+
+hmgp_factor::~hmgp_factor() = default;
+
+namespace {
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  explicit DBuf(size_t n) { HMGP_CUDA(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T))); }
+  ~DBuf() { cudaFree(p); }
+};
+
+size_t arena_bytes_for(const HMat& h) {
+  size_t fr = 0, tot = 0;
+  cudaMemGetInfo(&fr, &tot);
+  // room for the factor copy of the payload + solve work, keep 2 GiB spare
+  const size_t need = h.pool_doubles * 8 + ((size_t)2 << 30);
+  const size_t avail = fr > need + ((size_t)1 << 30) ? fr - need : ((size_t)1 << 30);
+  const size_t want = std::max<size_t>((size_t)8 << 30, h.pool_doubles * 8 * 3);
+  return std::min(avail, want);
+}
+
+double factor_eps(const hmgp_config* c) {  // pipeline.hpp:21-24
+  if (c->eps_factor > 0.0) return c->eps_factor;
+  return c->rank.mode == 0 ? c->rank.eps : 1e-6;
+}
+
+// run factorize and translate a failing pivot into FactorError semantics
+std::unique_ptr<Factor> do_factorize(HMat& h, double eps_f, bool ldl, cudaStream_t st) {
+  if (!(eps_f > 0.0)) throw std::invalid_argument("factorize: eps_f must be positive");
+  auto f = std::make_unique<Factor>();
+  factorize(*f, h, eps_f, ldl, st, arena_bytes_for(h));
+  if (f->fail_pos != INT_MAX) {
+    hmgp_set_pivot(h.g->perm[f->fail_pos], f->fail_val);
+    throw Error(HMGP_ENOTSPD, "matrix not numerically SPD; increase nugget tau2");
+  }
+  return f;
+}
+
+double now() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// L(θ) on a built geometry with device z (original order)
+void loglik_on_geom(hmgp_ctx* ctx, Geometry& g, const double* d_z, const hmgp_matern* th,
+                    const hmgp_config* cfg, hmgp_loglik_result* res) {
+  hmgp_validate_matern(th);
+  if (cfg->rank.mode == 0 && !(cfg->rank.eps > 0.0))
+    throw std::invalid_argument("assemble: eps must be positive");
+  HMat h;
+  assemble(h, g, make_matern(th->sigma2, th->ell, th->nu, th->tau2), cfg->rank.eps,
+           cfg->rank.mode == 1, cfg->rank.rank, cfg->rank.max_rank > 0 ? cfg->rank.max_rank : 256,
+           ctx->stream, nullptr);
+  auto f = do_factorize(h, factor_eps(cfg), cfg->form == 1, ctx->stream);
+  const int n = g.n;
+  res->n = n;
+  res->logdet = factor_log_det(*f, ctx->stream);
+  res->quad_form = factor_quad_form_dev(*f, d_z, ctx->stream);
+  res->loglik = -0.5 * n * std::log(2.0 * M_PI) - 0.5 * res->logdet - 0.5 * res->quad_form;
+  res->status = f->clamped > 0 ? 1 : 0;
+}
+}  // namespace
+
+#define API_GUARD2(...)                                     \
+  try {                                                     \
+    __VA_ARGS__;                                            \
+    return HMGP_OK;                                         \
+  } catch (const hmgp_gpu::Error& e) {                      \
+    return hmgp_fail(e.code, e.what());                     \
+  } catch (const std::invalid_argument& e) {                \
+    return hmgp_fail(HMGP_EINVAL, e.what());                \
+  } catch (const std::domain_error& e) {                    \
+    return hmgp_fail(HMGP_EDOMAIN, e.what());               \
+  } catch (const std::out_of_range& e) {                    \
+    return hmgp_fail(HMGP_ERANGE, e.what());                \
+  } catch (const std::exception& e) {                       \
+    return hmgp_fail(HMGP_ECUDA, e.what());                 \
+  }
+
+int hmgp_fail(int code, const char* msg);
+
+namespace hmgp_gpu {
+// ------------------------------------------------------------------- K12 --
+// Each CTA: 256 test points (one per thread) x one slice of the training set,
+// training points streamed through shared memory in tiles of 512 (coordinates
+// + weights); partial sums per slice, reduced in a fixed order afterwards.
+constexpr int kCrossTile = 512;
+
+__global__ void __launch_bounds__(256) k_cross_apply(const double* __restrict__ train, int n, int dim,
+                                                     const double* __restrict__ w,
+                                                     const double* __restrict__ test, int m,
+                                                     MaternDev p, int slice, double* __restrict__ part) {
+  __shared__ double sx[kCrossTile], sy[kCrossTile], sz[kCrossTile], sw[kCrossTile];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j0 = blockIdx.y * slice, j1 = min(n, j0 + slice);
+  double tx = 0, ty = 0, tz = 0;
+  if (i < m) {
+    tx = test[(size_t)i * dim];
+    ty = test[(size_t)i * dim + 1];
+    if (dim == 3) tz = test[(size_t)i * dim + 2];
+  }
+  double acc = 0.0;
+  for (int b = j0; b < j1; b += kCrossTile) {
+    const int cnt = min(kCrossTile, j1 - b);
+    __syncthreads();
+    for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
+      sx[t] = train[(size_t)(b + t) * dim];
+      sy[t] = train[(size_t)(b + t) * dim + 1];
+      sz[t] = dim == 3 ? train[(size_t)(b + t) * dim + 2] : 0.0;
+      sw[t] = w[b + t];
+    }
+    __syncthreads();
+    if (i < m)
+      for (int t = 0; t < cnt; ++t) {
+        const double h = dim == 2 ? dist2d(tx, ty, sx[t], sy[t]) : dist3d(tx, ty, tz, sx[t], sy[t], sz[t]);
+        acc += matern_at(p, h) * sw[t];
+      }
+  }
+  if (i < m) part[(size_t)blockIdx.y * m + i] = acc;
+}
+
+__global__ void k_cross_reduce(const double* __restrict__ part, int m, int slices,
+                               double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  double s = 0.0;
+  for (int q = 0; q < slices; ++q) s += part[(size_t)q * m + i];
+  out[i] = s;
+}
+
+void cross_apply(cudaStream_t st, const double* d_train, int n, int dim, const double* d_w,
+                 const double* d_test, int m, const MaternDev& p, double* d_out) {
+  if (m <= 0) return;
+  const int bx = (m + 255) / 256;
+  int slices = std::max(1, (kSMs * 4 + bx - 1) / bx);
+  slices = std::min(slices, std::max(1, n / kCrossTile));
+  const int slice = (n + slices - 1) / slices;
+  DBuf<double> part((size_t)slices * m);
+  k_cross_apply<<<dim3(bx, slices), 256, 0, st>>>(d_train, n, dim, d_w, d_test, m, p, slice, part.p);
+  HMGP_LAUNCH_CHECK();
+  k_cross_reduce<<<bx, 256, 0, st>>>(part.p, m, slices, d_out);
+  HMGP_LAUNCH_CHECK();
+  HMGP_CUDA(cudaStreamSynchronize(st));
+}
+}  // namespace hmgp_gpu
+
+extern "C" {
+
+int hmgp_factorize(hmgp_ctx* ctx, hmgp_hmat* h, double eps_f, int form, hmgp_factor** out,
+                   hmgp_factor_info* info) {
+  API_GUARD2({
+    HMGP_CUDA(cudaSetDevice(ctx->device));
+    auto f = do_factorize(h->h, eps_f, form == 1, ctx->stream);
+    if (info) {
+      info->eps = eps_f;
+      info->clamped = f->clamped;
+      info->negative = f->negative;
+      info->min_pivot = f->min_pivot;
+      info->storage_bytes = factor_storage_bytes(*f);
+    }
+    auto r = new hmgp_factor();
+    r->f = std::move(f);
+    *out = r;
+  })
+}
+
+int hmgp_log_det(hmgp_ctx* ctx, const hmgp_factor* f, double* out) {
+  API_GUARD2({ *out = factor_log_det(*f->f, ctx->stream); })
+}
+
+int hmgp_quad_form(hmgp_ctx* ctx, const hmgp_factor* f, const double* b, double* out) {
+  API_GUARD2({
+    const int n = f->f->g->n;
+    DBuf<double> db(n);
+    HMGP_CUDA(cudaMemcpyAsync(db.p, b, 8ull * n, cudaMemcpyHostToDevice, ctx->stream));
+    *out = factor_quad_form_dev(*f->f, db.p, ctx->stream);
+  })
+}
+
+static int solve_common(hmgp_ctx* ctx, const hmgp_factor* f, const double* b, double* x, bool full) {
+  API_GUARD2({
+    const int n = f->f->g->n;
+    DBuf<double> db(n), dx(n);
+    HMGP_CUDA(cudaMemcpyAsync(db.p, b, 8ull * n, cudaMemcpyHostToDevice, ctx->stream));
+    factor_solve_dev(*f->f, db.p, dx.p, full, ctx->stream);
+    HMGP_CUDA(cudaMemcpyAsync(x, dx.p, 8ull * n, cudaMemcpyDeviceToHost, ctx->stream));
+    HMGP_CUDA(cudaStreamSynchronize(ctx->stream));
+  })
+}
+int hmgp_solve_factored(hmgp_ctx* ctx, const hmgp_factor* f, const double* b, double* x) {
+  return solve_common(ctx, f, b, x, true);
+}
+int hmgp_solve_lower(hmgp_ctx* ctx, const hmgp_factor* f, const double* b, double* x) {
+  return solve_common(ctx, f, b, x, false);
+}
+
+int hmgp_factor_diagonal(hmgp_ctx* ctx, const hmgp_factor* f, double* out) {
+  API_GUARD2({
+    const Factor& F = *f->f;
+    const int n = F.g->n;
+    std::vector<double> d(n);
+    HMGP_CUDA(cudaMemcpyAsync(d.data(), F.d_d, 8ull * n, cudaMemcpyDeviceToHost, ctx->stream));
+    HMGP_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int k = 0; k < n; ++k) out[F.g->perm[k]] = d[k];
+  })
+}
+
+void hmgp_factor_destroy(hmgp_factor* f) { delete f; }
+
+int hmgp_loglik(hmgp_ctx* ctx, const double* coords, int n, int dim, const double* z,
+                const hmgp_matern* theta, const hmgp_config* cfg, hmgp_loglik_result* res) {
+  API_GUARD2({
+    hmgp_validate_matern(theta);  // loglik.cpp:20-23
+    if (n < 1) throw std::invalid_argument("evaluate_loglik: empty dataset");
+    HMGP_CUDA(cudaSetDevice(ctx->device));
+    const double t0 = now();
+    hmgp_geom* g = nullptr;
+    const int rc = hmgp_geometry_build(ctx, coords, n, dim, cfg->leaf_size, cfg->eta, &g);
+    if (rc != HMGP_OK) return rc;
+    std::unique_ptr<hmgp_geom, void (*)(hmgp_geom*)> guard(g, hmgp_geometry_destroy);
+    DBuf<double> dz(n);
+    HMGP_CUDA(cudaMemcpyAsync(dz.p, z, 8ull * n, cudaMemcpyHostToDevice, ctx->stream));
+    loglik_on_geom(ctx, g->g, dz.p, theta, cfg, res);
+    res->seconds = now() - t0;
+  })
+}
+
+int hmgp_loglik_geom(hmgp_ctx* ctx, hmgp_geom* g, const double* d_z, const hmgp_matern* theta,
+                     const hmgp_config* cfg, hmgp_loglik_result* res) {
+  API_GUARD2({
+    HMGP_CUDA(cudaSetDevice(ctx->device));
+    const double t0 = now();
+    loglik_on_geom(ctx, g->g, d_z, theta, cfg, res);
+    res->seconds = now() - t0;
+  })
+}
+
+int hmgp_loglik_batch(hmgp_ctx* ctx, hmgp_geom* g, const double* d_z, const hmgp_matern* thetas,
+                      int ntheta, const hmgp_config* cfg, hmgp_loglik_result* res) {
+  API_GUARD2({
+    HMGP_CUDA(cudaSetDevice(ctx->device));
+    for (int t = 0; t < ntheta; ++t) {
+      const double t0 = now();
+      try {  // fit() maps any failure to -inf (mle.cpp:152-158)
+        loglik_on_geom(ctx, g->g, d_z, &thetas[t], cfg, &res[t]);
+      } catch (const hmgp_gpu::Error& e) {
+        if (e.code != HMGP_ENOTSPD && e.code != HMGP_ECAPACITY) throw;
+        res[t] = hmgp_loglik_result{-std::numeric_limits<double>::infinity(), 0, 0, g->g.n, 0, -1};
+      } catch (const std::domain_error&) {
+        res[t] = hmgp_loglik_result{-std::numeric_limits<double>::infinity(), 0, 0, g->g.n, 0, -1};
+      }
+      res[t].seconds = now() - t0;
+    }
+  })
+}
+
+int hmgp_predict(hmgp_ctx* ctx, const double* train, int n, int dim, const double* z1,
+                 const double* test, int m, const hmgp_matern* theta, const hmgp_config* cfg,
+                 double* out, double* seconds) {
+  API_GUARD2({
+    hmgp_validate_matern(theta);  // krige.cpp:12-15
+    if (n < 1) throw std::invalid_argument("predict: empty training set");
+    const double t0 = now();
+    if (m == 0) {
+      if (seconds) *seconds = now() - t0;
+      return HMGP_OK;
+    }
+    HMGP_CUDA(cudaSetDevice(ctx->device));
+    hmgp_geom* g = nullptr;
+    const int rc = hmgp_geometry_build(ctx, train, n, dim, cfg->leaf_size, cfg->eta, &g);
+    if (rc != HMGP_OK) return rc;
+    std::unique_ptr<hmgp_geom, void (*)(hmgp_geom*)> guard(g, hmgp_geometry_destroy);
+    HMat h;
+    assemble(h, g->g, make_matern(theta->sigma2, theta->ell, theta->nu, theta->tau2), cfg->rank.eps,
+             cfg->rank.mode == 1, cfg->rank.rank, cfg->rank.max_rank > 0 ? cfg->rank.max_rank : 256,
+             ctx->stream, nullptr);
+    auto f = do_factorize(h, factor_eps(cfg), cfg->form == 1, ctx->stream);
+    DBuf<double> dz(n), dw(n), dtest((size_t)m * dim), dout(m);
+    HMGP_CUDA(cudaMemcpyAsync(dz.p, z1, 8ull * n, cudaMemcpyHostToDevice, ctx->stream));
+    HMGP_CUDA(cudaMemcpyAsync(dtest.p, test, 8ull * m * dim, cudaMemcpyHostToDevice, ctx->stream));
+    factor_solve_dev(*f, dz.p, dw.p, true, ctx->stream);
+    cross_apply(ctx->stream, g->g.d_x, n, dim, dw.p, dtest.p, m,
+                make_matern(theta->sigma2, theta->ell, theta->nu, theta->tau2), dout.p);
+    HMGP_CUDA(cudaMemcpyAsync(out, dout.p, 8ull * m, cudaMemcpyDeviceToHost, ctx->stream));
+    HMGP_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (seconds) *seconds = now() - t0;
+  })
+}
+
+int hmgp_cross_apply_device(hmgp_ctx* ctx, const double* d_train, int n, int dim, const double* d_w,
+                            const double* d_test, int m, const hmgp_matern* theta, double* d_out) {
+  API_GUARD2({
+    hmgp_validate_matern(theta);
+    HMGP_CUDA(cudaSetDevice(ctx->device));
+    cross_apply(ctx->stream, d_train, n, dim, d_w, d_test, m,
+                make_matern(theta->sigma2, theta->ell, theta->nu, theta->tau2), d_out);
+  })
+}
+
+}  // extern "C"
