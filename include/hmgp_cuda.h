@@ -169,6 +169,22 @@ int hmgp_cross_apply_device(hmgp_ctx* ctx, const double* d_train, int n, int dim
                             const double* d_w, const double* d_test, int m,
                             const hmgp_matern* theta, double* d_out);
 
+/* ------------------------------------------------------- instrumentation */
+/* the context's CUDA stream (cudaStream_t), for event timing by callers */
+int hmgp_ctx_stream(hmgp_ctx* ctx, void** stream);
+/* per-phase device milliseconds of the last loglik / predict call on ctx:
+ * [0] start [1] geometry [2] dense leaves K3 [3] ACA K4+K5 [4] layout/copies
+ * [5] factorization K6-K9 [6] logdet [7] forward solve + quad [8] backward solve [9] K12 */
+int hmgp_last_phases(hmgp_ctx* ctx, double* ms, int cap);
+/* algorithmic work since the last reset: [0] dense entries [1] ACA entries
+ * [2] Matérn flops of dense leaves (only when counting is on) [3] GEMM flops
+ * [4] TRSM flops [5] leaf factor flops [6] recompression flops [7] recompressions */
+int hmgp_work_counters(double* out, int cap, int reset);
+/* enable the untimed Matérn flop-count pass inside assembly */
+void hmgp_set_flop_counting(int on);
+/* measured FP64 FMA-pipe peak of the device (TFLOP/s), FMA-chain microbenchmark */
+int hmgp_fp64_peak(hmgp_ctx* ctx, double* tflops);
+
 /* --------------------------------------------------------- data utilities */
 /* simgen conventions (simgen.cpp:108-123): mt19937_64 + ((x>>11)+0.5)*2^-53 */
 int hmgp_random_locations(int n, int dim, uint64_t seed, double* out);

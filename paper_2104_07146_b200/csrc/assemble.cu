@@ -15,6 +15,7 @@
 
 #include "common.cuh"
 #include "hmgp_internal.h"
+#include "phases.h"
 
 namespace hmgp_gpu {
 
@@ -75,6 +76,33 @@ __global__ void __launch_bounds__(256) k_dense_leaves(const DenseItem* __restric
     }
 }
 
+// Untimed counting pass: algorithmic flops of all dense-leaf entries.
+__global__ void k_dense_flops(const DenseItem* __restrict__ items, MaternDev p,
+                              const double* __restrict__ xt, int n_pts, int dim, double* out) {
+  const DenseItem it = items[blockIdx.x];
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int idx = threadIdx.x; idx < it.m * it.n; idx += blockDim.x) {
+    const int a = it.r0 + idx % it.m, b = it.c0 + idx / it.m;
+    if (a == b) continue;
+    const double h = dim == 2 ? dist2d(xt[a], xt[n_pts + a], xt[b], xt[n_pts + b])
+                              : dist3d(xt[a], xt[n_pts + a], xt[2 * n_pts + a], xt[b],
+                                       xt[n_pts + b], xt[2 * n_pts + b]);
+    acc += matern_flops(p, h);
+  }
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) atomicAdd(out, acc);
+}
+
+__device__ double d_cnt_aca;
+
+double aca_entries_read_reset() {
+  double v = 0.0, z = 0.0;
+  HMGP_CUDA(cudaMemcpyFromSymbol(&v, d_cnt_aca, 8));
+  HMGP_CUDA(cudaMemcpyToSymbol(d_cnt_aca, &z, 8));
+  return v;
+}
+
 struct AcaItem {
   double* U;  // m x cap
   double* V;  // n x cap
@@ -100,7 +128,7 @@ __global__ void __launch_bounds__(kAcaThreads) k_aca(const AcaItem* __restrict__
   __shared__ int s_next, s_fresh;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int max_terms = it.cap;
-  double fro2 = 0.0, scale0 = 0.0;
+  double fro2 = 0.0, scale0 = 0.0, ne = 0.0;
   int ip = 0, k = 0;
   if (threadIdx.x == 0) s_fresh = 1;
   __syncthreads();
@@ -109,6 +137,7 @@ __global__ void __launch_bounds__(kAcaThreads) k_aca(const AcaItem* __restrict__
     for (int l = threadIdx.x; l < k; l += blockDim.x) s_coef[l] = it.U[(size_t)l * m + ip];
     __syncthreads();
     double* r = it.V + (size_t)k * n;
+    ne += n;
     int jb = -1;
     double ab = -1.0;
     for (int j = threadIdx.x; j < n; j += blockDim.x) {
@@ -156,6 +185,7 @@ __global__ void __launch_bounds__(kAcaThreads) k_aca(const AcaItem* __restrict__
     for (int l = threadIdx.x; l < k; l += blockDim.x) s_coef[l] = it.V[(size_t)l * n + jp];
     __syncthreads();
     double* u = it.U + (size_t)k * m;
+    ne += m;
     for (int i = threadIdx.x; i < m; i += blockDim.x) {
       double v = kentry(p, xt, n_pts, dim, it.r0 + i, it.c0 + jp);
       for (int l = 0; l < k; ++l) v -= s_coef[l] * it.U[(size_t)l * m + i];
@@ -206,7 +236,10 @@ __global__ void __launch_bounds__(kAcaThreads) k_aca(const AcaItem* __restrict__
     if (inx < 0) break;
     ip = inx;
   }
-  if (threadIdx.x == 0) *it.rank = k;
+  if (threadIdx.x == 0) {
+    *it.rank = k;
+    atomicAdd(&d_cnt_aca, ne);
+  }
 }
 
 // C (m x n) = U (m x r) V^T (n x r), r from device; one CTA per item.
@@ -439,6 +472,7 @@ void assemble(HMat& h, Geometry& g, const MaternDev& p, double eps, bool fixed_r
       chunks.push_back(std::move(c));
     }
   }
+  phase_mark(PH_ACA);
   HMGP_CUDA(cudaMemcpyAsync(rank.data(), d_rank_tmp, (size_t)L * 4, cudaMemcpyDeviceToHost, st));
   int herr = 0;
   HMGP_CUDA(cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, st));
@@ -493,11 +527,26 @@ void assemble(HMat& h, Geometry& g, const MaternDev& p, double eps, bool fixed_r
     for (int k : den) di.push_back(DenseItem{h.leaf[k].a, r0v[k], c0v[k], mm[k], nn[k]});
     if (!di.empty()) {
       DenseItem* d_di = upload(di, st);
+      phase_mark(PH_LAYOUT);
       k_dense_leaves<<<(int)di.size(), 256, 0, st>>>(d_di, p, g.d_xt, g.n, g.dim);
       HMGP_LAUNCH_CHECK();
+      phase_mark(PH_DENSE);
+      if (g_count_kernel_flops) {  // untimed counting pass (bench roofline)
+        double* d_f = dmalloc<double>(1);
+        HMGP_CUDA(cudaMemsetAsync(d_f, 0, 8, st));
+        k_dense_flops<<<(int)di.size(), 256, 0, st>>>(d_di, p, g.d_xt, g.n, g.dim, d_f);
+        HMGP_LAUNCH_CHECK();
+        double fl = 0;
+        HMGP_CUDA(cudaMemcpyAsync(&fl, d_f, 8, cudaMemcpyDeviceToHost, st));
+        HMGP_CUDA(cudaStreamSynchronize(st));
+        g_work.kernel_flops += fl;
+        cudaFree(d_f);
+        phase_mark(PH_LAYOUT);
+      }
       HMGP_CUDA(cudaStreamSynchronize(st));
       cudaFree(d_di);
     }
+    for (int k : den) g_work.dense_entries += (double)mm[k] * nn[k];
   }
   // ACA results -> pool (copy, or coarsen to dense U V^T)
   for (Chunk& c : chunks) {
@@ -531,6 +580,7 @@ void assemble(HMat& h, Geometry& g, const MaternDev& p, double eps, bool fixed_r
     cudaFree(c.buf);
     c.buf = nullptr;
   }
+  phase_mark(PH_LAYOUT);
   cudaFree(d_rank_tmp);
   cudaFree(d_err);
   h.d_leaf = upload(h.leaf, st);

@@ -371,3 +371,86 @@ int hmgp_normals(int n, uint64_t seed, double* out) {
 }  // extern "C"
 
 int hmgp_fail(int code, const char* msg) { return fail(code, msg); }
+
+// ------------------------------------------------------- instrumentation --
+namespace hmgp_gpu {
+thread_local PhaseTimer* t_phase = nullptr;
+WorkCounters g_work;
+bool g_count_kernel_flops = false;
+
+// FMA chains: 8 independent accumulators per thread, 4096 iterations.
+__global__ void k_fp64_peak(double* out, double a, double b) {
+  double x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-9 + k;
+  for (int it = 0; it < 4096; ++it)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = fma(x[k], a, b);
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k];
+  if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
+}  // namespace hmgp_gpu
+
+extern "C" {
+
+int hmgp_ctx_stream(hmgp_ctx* ctx, void** stream) {
+  API_GUARD({ *stream = (void*)ctx->stream; })
+}
+
+int hmgp_last_phases(hmgp_ctx* ctx, double* ms, int cap) {
+  API_GUARD({
+    for (int i = 0; i < cap && i < PH_COUNT; ++i) ms[i] = ctx->phase_ms[i];
+  })
+}
+
+int hmgp_work_counters(double* out, int cap, int reset) {
+  API_GUARD({
+    double g = 0, t = 0, l = 0, tf = 0, ti = 0;
+    linalg_counters_read_reset(&g, &t, &l);
+    truncate_counters_read_reset(&tf, &ti);
+    g_work.aca_entries += aca_entries_read_reset();
+    g_work.gemm_flops += g;
+    g_work.trsm_flops += t;
+    g_work.leaf_flops += l;
+    g_work.trunc_flops += tf;
+    g_work.trunc_items += ti;
+    const double v[8] = {g_work.dense_entries, g_work.aca_entries, g_work.kernel_flops,
+                         g_work.gemm_flops,    g_work.trsm_flops,  g_work.leaf_flops,
+                         g_work.trunc_flops,   g_work.trunc_items};
+    for (int i = 0; i < cap && i < 8; ++i) out[i] = v[i];
+    if (reset) g_work = WorkCounters{};
+  })
+}
+
+void hmgp_set_flop_counting(int on) { g_count_kernel_flops = on != 0; }
+
+int hmgp_fp64_peak(hmgp_ctx* ctx, double* tflops) {
+  API_GUARD({
+    HMGP_CUDA(cudaSetDevice(ctx->device));
+    double* d = nullptr;
+    HMGP_CUDA(cudaMalloc(&d, 8));
+    int sms = 0;
+    HMGP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+    const int blocks = sms * 8, threads = 256;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    k_fp64_peak<<<blocks, threads, 0, ctx->stream>>>(d, 0.999999, 1e-7);  // warm-up
+    HMGP_LAUNCH_CHECK();
+    cudaEventRecord(e0, ctx->stream);
+    for (int r = 0; r < 10; ++r) k_fp64_peak<<<blocks, threads, 0, ctx->stream>>>(d, 0.999999, 1e-7);
+    HMGP_LAUNCH_CHECK();
+    cudaEventRecord(e1, ctx->stream);
+    HMGP_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    *tflops = 10.0 * blocks * threads * 4096.0 * 8 * 2 / (ms * 1e-3) / 1e12;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(d);
+  })
+}
+
+}  // extern "C"

@@ -23,6 +23,7 @@
 #include "factor.h"
 #include "hmgp_api.h"
 #include "linalg.cuh"
+#include "phases.h"
 
 namespace hmgp_gpu {
 
@@ -247,11 +248,47 @@ struct Engine {
     double alpha;
     int trans;  // 0: B, 1: B^T
   };
-  void apply(const std::vector<Ap>& its) {
-    if (its.empty()) return;
+  // Flatten a branch into its stored leaves (null children are structural
+  // zeros, hblock.cpp:43-45), with the matching x / y sub-views.
+  void flatten(const Ap& a, std::vector<Ap>& out) {
+    if (kind(a.b) != BRANCH) {
+      out.push_back(a);
+      return;
+    }
+    const HNode& nd = N(a.b);
+    for (int pos = 0; pos < nd.kr * nd.kc; ++pos) {
+      const int c = nd.kids[pos];
+      if (c < 0) continue;
+      Ap s = a;
+      s.b = c;
+      if (!a.trans) {
+        s.x = rows_of(a.x, cb(c) - cb(a.b), nc(c));
+        s.y = rows_of(a.y, rb(c) - rb(a.b), nr(c));
+      } else {
+        s.x = rows_of(a.x, rb(c) - rb(a.b), nr(c));
+        s.y = rows_of(a.y, cb(c) - cb(a.b), nc(c));
+      }
+      flatten(s, out);
+    }
+  }
+
+  // y += alpha op(B) x for a list of (B, x, y); every H-block is flattened to
+  // its leaves, so any block costs three launches: dense leaves, and the two
+  // low-rank stages.  Leaves of one block may share y rows -> FP64 atomics.
+  void apply(const std::vector<Ap>& its0) {
+    if (its0.empty()) return;
+    std::vector<Ap> its;
+    std::vector<int> shared;
+    for (const Ap& a : its0) {
+      const size_t before = its.size();
+      flatten(a, its);
+      for (size_t i = before; i < its.size(); ++i) shared.push_back(kind(a.b) == BRANCH);
+    }
     std::vector<GemmItem> g;
     std::vector<Ap> lr, br;
-    for (const Ap& a : its) {
+    std::vector<int> lr_shared;
+    for (size_t ii = 0; ii < its.size(); ++ii) {
+      const Ap& a = its[ii];
       const int k = kind(a.b);
       if (k == DENSE) {
         const LeafDev& l = LF(a.b);
@@ -268,11 +305,11 @@ struct Engine {
         gi.N = a.x.cols;
         gi.K = dimv(a.trans ? l.m : l.n);
         gi.alpha = a.alpha;
+        gi.atomic = shared[ii];
         g.push_back(gi);
-      } else if (k == LOWRANK) {
-        lr.push_back(a);
       } else {
-        br.push_back(a);
+        lr.push_back(a);
+        lr_shared.push_back(shared[ii]);
       }
     }
     gemm(g);
@@ -319,33 +356,11 @@ struct Engine {
         gi.N = a.x.cols;
         gi.K = dimp(rankp(a.b), l.cap);
         gi.alpha = a.alpha;
+        gi.atomic = lr_shared[i];
         g.push_back(gi);
       }
       gemm(g);
       ar.release(mk);
-    }
-    if (!br.empty()) {
-      // child positions in row-major order, sequential (shared y rows)
-      for (int pos = 0; pos < 4; ++pos) {
-        std::vector<Ap> sub;
-        for (const Ap& a : br) {
-          const HNode& nd = N(a.b);
-          if (pos >= nd.kr * nd.kc) continue;
-          const int c = nd.kids[pos];
-          if (c < 0) continue;
-          Ap s = a;
-          s.b = c;
-          if (!a.trans) {
-            s.x = rows_of(a.x, cb(c) - cb(a.b), nc(c));
-            s.y = rows_of(a.y, rb(c) - rb(a.b), nr(c));
-          } else {
-            s.x = rows_of(a.x, rb(c) - rb(a.b), nr(c));
-            s.y = rows_of(a.y, cb(c) - cb(a.b), nc(c));
-          }
-          sub.push_back(s);
-        }
-        apply(sub);
-      }
     }
   }
 
@@ -1050,6 +1065,7 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
     for (int k = 0; k < L; ++k)
       if (F.leaf[k].kind == LOWRANK) lr.push_back(F.leaf_node[k]);
     E.compress(lr);
+    phase_mark(PH_FACTOR);
     int err = 0;
     HMGP_CUDA(cudaMemcpyAsync(&err, E.d_err, 4, cudaMemcpyDeviceToHost, st));
     HMGP_CUDA(cudaStreamSynchronize(st));
@@ -1125,6 +1141,7 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
   HMGP_CUDA(cudaMemcpyAsync(F.d_fwd, flat_f.data(), sizeof(SolveBlk) * flat_f.size(), cudaMemcpyHostToDevice, st));
   HMGP_CUDA(cudaMemcpyAsync(F.d_bwd, flat_b.data(), sizeof(SolveBlk) * flat_b.size(), cudaMemcpyHostToDevice, st));
   HMGP_CUDA(cudaMalloc(&F.d_work, 8ull * (2 * G.n + 1024)));
+  phase_mark(PH_LAYOUT);
   HMGP_CUDA(cudaStreamSynchronize(st));
 }
 

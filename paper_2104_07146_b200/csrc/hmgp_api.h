@@ -8,10 +8,28 @@
 
 #include "../../include/hmgp_cuda.h"
 #include "hmgp_internal.h"
+#include "phases.h"
 
 struct hmgp_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  hmgp_gpu::PhaseTimer timer;
+  double phase_ms[hmgp_gpu::PH_COUNT] = {};
+};
+
+// Times the phases of one pipeline call on the context's stream.
+struct PhaseScope {
+  hmgp_ctx* c;
+  explicit PhaseScope(hmgp_ctx* ctx) : c(ctx) {
+    c->timer.begin(c->stream);
+    hmgp_gpu::t_phase = &c->timer;
+    hmgp_gpu::phase_mark(hmgp_gpu::PH_START);
+  }
+  void finish() {
+    hmgp_gpu::t_phase = nullptr;
+    c->timer.collect(c->phase_ms);
+  }
+  ~PhaseScope() { hmgp_gpu::t_phase = nullptr; }
 };
 struct hmgp_geom {
   hmgp_gpu::Geometry g;

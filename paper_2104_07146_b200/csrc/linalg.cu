@@ -9,6 +9,19 @@
 
 namespace hmgp_gpu {
 
+// algorithmic flop counters (one atomic per item; read by bench.py)
+__device__ double d_cnt_gemm, d_cnt_trsm, d_cnt_leaf;
+
+void linalg_counters_read_reset(double* g, double* t, double* l) {
+  double z = 0.0;
+  HMGP_CUDA(cudaMemcpyFromSymbol(g, d_cnt_gemm, 8));
+  HMGP_CUDA(cudaMemcpyFromSymbol(t, d_cnt_trsm, 8));
+  HMGP_CUDA(cudaMemcpyFromSymbol(l, d_cnt_leaf, 8));
+  HMGP_CUDA(cudaMemcpyToSymbol(d_cnt_gemm, &z, 8));
+  HMGP_CUDA(cudaMemcpyToSymbol(d_cnt_trsm, &z, 8));
+  HMGP_CUDA(cudaMemcpyToSymbol(d_cnt_leaf, &z, 8));
+}
+
 // ----------------------------------------------------------------- GEMM ---
 // 64x64 output tile per CTA iteration, k-slabs of 16 staged in shared memory,
 // 256 threads x (4 x 4) register micro-tile.  Dimensions may live on device.
@@ -18,6 +31,7 @@ __global__ void __launch_bounds__(256) k_gemm(const GemmItem* __restrict__ items
   const GemmItem it = items[blockIdx.x];
   const int M = it.M.get(), N = it.N.get(), K = it.K.get();
   if (M <= 0 || N <= 0) return;
+  if (blockIdx.y == 0 && threadIdx.x == 0) atomicAdd(&d_cnt_gemm, 2.0 * M * N * K);
   const int tm = (M + GT - 1) / GT, tn = (N + GT - 1) / GT;
   __shared__ double sA[GK][GT + 1];
   __shared__ double sB[GK][GT + 1];
@@ -83,7 +97,12 @@ __global__ void __launch_bounds__(256) k_gemm(const GemmItem* __restrict__ items
 #pragma unroll
       for (int p = 0; p < 4; ++p) {
         const int gi = i0 + tx + 16 * p;
-        if (gi < M) it.C[(size_t)gj * it.ldc + gi] += it.alpha * acc[p][q];
+        if (gi < M) {
+          if (it.atomic)
+            atomicAdd(&it.C[(size_t)gj * it.ldc + gi], it.alpha * acc[p][q]);
+          else
+            it.C[(size_t)gj * it.ldc + gi] += it.alpha * acc[p][q];
+        }
       }
     }
   }
@@ -103,6 +122,7 @@ __global__ void k_trsm_left(const TrsmLItem* __restrict__ items) {
   const int cols = it.cols.get();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int b = it.b;
+  if (blockIdx.y == 0 && threadIdx.x == 0) atomicAdd(&d_cnt_trsm, (double)b * b * cols);
   for (int c = blockIdx.y * nw + w; c < cols; c += gridDim.y * nw) {
     double* x = it.M + (size_t)c * it.ldm;
     if (!it.trans) {
@@ -137,6 +157,7 @@ void launch_trsm_left(const TrsmLItem* d_items, int count, int max_cols, cudaStr
 // Right: X <- X L^{-T}, one thread per row of X.
 __global__ void k_trsm_right(const TrsmRItem* __restrict__ items) {
   const TrsmRItem it = items[blockIdx.x];
+  if (blockIdx.y == 0 && threadIdx.x == 0) atomicAdd(&d_cnt_trsm, (double)it.t * it.t * it.s);
   for (int r = blockIdx.y * blockDim.x + threadIdx.x; r < it.s; r += gridDim.y * blockDim.x) {
     for (int j = 0; j < it.t; ++j) {
       const double xj = it.X[(size_t)j * it.ldx + r] / it.L[(size_t)j * it.ldl + j];
@@ -264,6 +285,7 @@ __global__ void k_leaf_factor(double* __restrict__ Dg, int b, int base, int ldl,
   __shared__ double red[32];
   __shared__ double s_piv;
   double* A = use_smem ? sm : Dg;
+  if (threadIdx.x == 0) atomicAdd(&d_cnt_leaf, (double)b * b * b / 3.0);
   if (use_smem)
     for (int e = threadIdx.x; e < b * b; e += blockDim.x) A[e] = Dg[e];
   __syncthreads();

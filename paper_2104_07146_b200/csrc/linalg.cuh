@@ -25,6 +25,7 @@ struct GemmItem {
   Dim M, N, K;
   int ta, tb;
   double alpha;
+  int atomic;  // accumulate with FP64 atomics (several items share C rows)
 };
 
 // M (b x cols) <- L^{-1} M (trans = 0) or L^{-T} M (trans = 1); L b x b lower,

@@ -198,4 +198,72 @@ __device__ __forceinline__ double matern_at(const MaternDev& p, double h) {
   return p.pref * pow(t, p.nu) * k;
 }
 
+// ---------------------------------------------------------------------------
+// Algorithmic flop model of one at_distance evaluation along the exact path the
+// reference takes: +,-,*,/,sqrt = 1; exp, log, sin, sinh, cosh
+// = 20; pow = 45.  Iteration counts are those of the actual Temme / Steed loops
+// for this argument (the loops are re-run here, results discarded).  Used only
+// by the untimed counting pass that feeds bench.py's roofline.
+static __device__ __noinline__ double matern_flops(const MaternDev& p, double h) {
+  const double t = h / p.ell;
+  double f = 6.0;  // distance (5) + h/ell
+  if (t < 1e-10) return f;
+  if (p.closed >= 0) return f + 20.0 + 2.0 + 2.0 * p.closed;
+  if (p.half >= 0) return f + 45.0 + 2.0 + 25.0 + 4.0 * (p.half > 1 ? p.half - 1 : 0);
+  f += 45.0 + 2.0;  // pow + prefactor products
+  const int nl = (int)(p.nu + 0.5);
+  const double mu = p.nu - nl;
+  int it = 0;
+  if (t <= 2.0) {
+    double k0, k1;
+    // rerun the series counting iterations
+    const double hx = 0.5 * t, mu2 = mu * mu;
+    double g1, g2, rp, rm;
+    temme_gammas(mu, g1, g2, rp, rm);
+    const double lg = -log(hx);
+    double e = mu * lg;
+    const double fsh = fabs(e) < 1e-15 ? 1.0 : sinh(e) / e;
+    const double pm = kPiD * mu;
+    const double fs = fabs(pm) < 1e-15 ? 1.0 : pm / sin(pm);
+    double ff = fs * (g1 * cosh(e) + g2 * fsh * lg), s0 = ff;
+    e = exp(e);
+    double pp = 0.5 * e / rp, qq = 0.5 / (e * rm), cc = 1.0;
+    for (int i = 1; i <= 20000; ++i) {
+      ++it;
+      const double di = (double)i;
+      ff = (di * ff + pp + qq) / (di * di - mu2);
+      cc *= hx * hx / di;
+      pp /= (di - mu);
+      qq /= (di + mu);
+      const double del = cc * ff;
+      s0 += del;
+      if (fabs(del) < fabs(s0) * kEpsD) break;
+    }
+    (void)k0;
+    (void)k1;
+    f += 180.0 + 19.0 * it + 2.0;
+  } else {
+    double b = 2.0 * (1.0 + t), d = 1.0 / b, dh = d, qa = 0.0, qb = 1.0;
+    const double a1 = 0.25 - mu * mu;
+    double q = a1, c = a1, a = -a1, s = 1.0 + q * dh;
+    for (int i = 2; i <= 20000; ++i) {
+      ++it;
+      a -= 2 * (i - 1);
+      c = -a * c / i;
+      const double qn = (qa - b * qb) / a;
+      qa = qb;
+      qb = qn;
+      q += c * qn;
+      b += 2.0;
+      d = 1.0 / (b + a * d);
+      dh = (b * d - 1.0) * dh;
+      const double ds = q * dh;
+      s += ds;
+      if (fabs(ds / s) < kEpsD) break;
+    }
+    f += 10.0 + 20.0 * it + 45.0;
+  }
+  return f + 4.0 * nl;
+}
+
 }  // namespace hmgp_gpu

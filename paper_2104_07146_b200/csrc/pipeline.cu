@@ -70,7 +70,9 @@ void loglik_on_geom(hmgp_ctx* ctx, Geometry& g, const double* d_z, const hmgp_ma
   const int n = g.n;
   res->n = n;
   res->logdet = factor_log_det(*f, ctx->stream);
+  phase_mark(PH_LOGDET);
   res->quad_form = factor_quad_form_dev(*f, d_z, ctx->stream);
+  phase_mark(PH_FWD);
   res->loglik = -0.5 * n * std::log(2.0 * M_PI) - 0.5 * res->logdet - 0.5 * res->quad_form;
   res->status = f->clamped > 0 ? 1 : 0;
 }
@@ -229,13 +231,16 @@ int hmgp_loglik(hmgp_ctx* ctx, const double* coords, int n, int dim, const doubl
     if (n < 1) throw std::invalid_argument("evaluate_loglik: empty dataset");
     HMGP_CUDA(cudaSetDevice(ctx->device));
     const double t0 = now();
+    PhaseScope ps(ctx);
     hmgp_geom* g = nullptr;
     const int rc = hmgp_geometry_build(ctx, coords, n, dim, cfg->leaf_size, cfg->eta, &g);
     if (rc != HMGP_OK) return rc;
     std::unique_ptr<hmgp_geom, void (*)(hmgp_geom*)> guard(g, hmgp_geometry_destroy);
     DBuf<double> dz(n);
     HMGP_CUDA(cudaMemcpyAsync(dz.p, z, 8ull * n, cudaMemcpyHostToDevice, ctx->stream));
+    phase_mark(PH_GEOMETRY);
     loglik_on_geom(ctx, g->g, dz.p, theta, cfg, res);
+    ps.finish();
     res->seconds = now() - t0;
   })
 }
@@ -245,7 +250,9 @@ int hmgp_loglik_geom(hmgp_ctx* ctx, hmgp_geom* g, const double* d_z, const hmgp_
   API_GUARD2({
     HMGP_CUDA(cudaSetDevice(ctx->device));
     const double t0 = now();
+    PhaseScope ps(ctx);
     loglik_on_geom(ctx, g->g, d_z, theta, cfg, res);
+    ps.finish();
     res->seconds = now() - t0;
   })
 }
@@ -281,10 +288,12 @@ int hmgp_predict(hmgp_ctx* ctx, const double* train, int n, int dim, const doubl
       return HMGP_OK;
     }
     HMGP_CUDA(cudaSetDevice(ctx->device));
+    PhaseScope ps(ctx);
     hmgp_geom* g = nullptr;
     const int rc = hmgp_geometry_build(ctx, train, n, dim, cfg->leaf_size, cfg->eta, &g);
     if (rc != HMGP_OK) return rc;
     std::unique_ptr<hmgp_geom, void (*)(hmgp_geom*)> guard(g, hmgp_geometry_destroy);
+    phase_mark(PH_GEOMETRY);
     HMat h;
     assemble(h, g->g, make_matern(theta->sigma2, theta->ell, theta->nu, theta->tau2), cfg->rank.eps,
              cfg->rank.mode == 1, cfg->rank.rank, cfg->rank.max_rank > 0 ? cfg->rank.max_rank : 256,
@@ -294,10 +303,12 @@ int hmgp_predict(hmgp_ctx* ctx, const double* train, int n, int dim, const doubl
     HMGP_CUDA(cudaMemcpyAsync(dz.p, z1, 8ull * n, cudaMemcpyHostToDevice, ctx->stream));
     HMGP_CUDA(cudaMemcpyAsync(dtest.p, test, 8ull * m * dim, cudaMemcpyHostToDevice, ctx->stream));
     factor_solve_dev(*f, dz.p, dw.p, true, ctx->stream);
+    phase_mark(PH_BWD);
     cross_apply(ctx->stream, g->g.d_x, n, dim, dw.p, dtest.p, m,
                 make_matern(theta->sigma2, theta->ell, theta->nu, theta->tau2), dout.p);
+    phase_mark(PH_CROSS);
     HMGP_CUDA(cudaMemcpyAsync(out, dout.p, 8ull * m, cudaMemcpyDeviceToHost, ctx->stream));
-    HMGP_CUDA(cudaStreamSynchronize(ctx->stream));
+    ps.finish();
     if (seconds) *seconds = now() - t0;
   })
 }

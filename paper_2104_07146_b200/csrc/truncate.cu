@@ -19,6 +19,21 @@ namespace hmgp_gpu {
 constexpr int kTruncThreads = 256;
 constexpr int kMaxTruncCols = 1024;
 
+__device__ double d_cnt_trunc, d_cnt_titems;
+
+void truncate_counters_read_reset(double* flops, double* items) {
+  double z = 0.0;
+  HMGP_CUDA(cudaMemcpyFromSymbol(flops, d_cnt_trunc, 8));
+  HMGP_CUDA(cudaMemcpyFromSymbol(items, d_cnt_titems, 8));
+  HMGP_CUDA(cudaMemcpyToSymbol(d_cnt_trunc, &z, 8));
+  HMGP_CUDA(cudaMemcpyToSymbol(d_cnt_titems, &z, 8));
+}
+
+// LAPACK dgeqrf flop count for an m x r panel
+__device__ __forceinline__ double qr_flops(double m, double r) {
+  return m >= r ? 2.0 * m * r * r - 2.0 / 3.0 * r * r * r : 2.0 * r * m * m - 2.0 / 3.0 * m * m * m;
+}
+
 size_t trunc_ws_doubles(int m, int n, int rcap) {
   const size_t kq = (size_t)min(min(m, n), rcap);
   return (size_t)(m + n) * rcap + 2 * (size_t)rcap + (size_t)rcap * kq + kq * kq;
@@ -94,15 +109,20 @@ __device__ void cta_apply_q(const double* QR, int m, int kq, const double* tau, 
 }
 
 // One-sided Jacobi on W (p x q, ld p, p >= q); J (q x q) accumulates rotations.
-__device__ void cta_jacobi(double* W, int p, int q, double* J) {
+// Returns the algorithmic flops (6p per pair inspected, 6(p+q) per rotation).
+__device__ double cta_jacobi(double* W, int p, int q, double* J) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int idx = threadIdx.x; idx < q * q; idx += blockDim.x) J[idx] = (idx % (q + 1) == 0) ? 1.0 : 0.0;
   __syncthreads();
-  if (q < 2) return;
+  if (q < 2) return 0.0;
   const int qq = q + (q & 1);
   const int m1 = qq - 1;
   __shared__ int s_rot;
+  __shared__ unsigned s_nrot;
+  if (threadIdx.x == 0) s_nrot = 0;
+  int sweeps = 0;
   for (int sweep = 0; sweep < 60; ++sweep) {
+    ++sweeps;
     if (threadIdx.x == 0) s_rot = 0;
     __syncthreads();
     for (int round = 0; round < m1; ++round) {
@@ -134,7 +154,10 @@ __device__ void cta_jacobi(double* W, int p, int q, double* J) {
         sb = warp_sum(sb);
         sc = warp_sum(sc);
         if (fabs(sc) <= 1e-15 * sqrt(sa * sb) || sc == 0.0) continue;
-        if (lane == 0) s_rot = 1;
+        if (lane == 0) {
+          s_rot = 1;
+          atomicAdd(&s_nrot, 1u);
+        }
         const double zeta = (sb - sa) / (2.0 * sc);
         const double tt = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
         const double cs = 1.0 / sqrt(1.0 + tt * tt), sn = cs * tt;
@@ -157,6 +180,7 @@ __device__ void cta_jacobi(double* W, int p, int q, double* J) {
     __syncthreads();
     if (!rot) break;
   }
+  return (double)sweeps * (0.5 * q * (q - 1)) * 6.0 * p + (double)s_nrot * 6.0 * (p + q);
 }
 
 __global__ void __launch_bounds__(kTruncThreads) k_truncate(const TruncItem* __restrict__ items,
@@ -248,7 +272,7 @@ __global__ void __launch_bounds__(kTruncThreads) k_truncate(const TruncItem* __r
       C[(size_t)i * p + j] = s;
   }
   __syncthreads();
-  cta_jacobi(C, p, q, J);
+  const double jac_flops = cta_jacobi(C, p, q, J);
   // singular values = column norms of W; order descending (ties by index)
   for (int c = threadIdx.x; c < q; c += blockDim.x) {
     const double* wc = C + (size_t)c * p;
@@ -298,6 +322,10 @@ __global__ void __launch_bounds__(kTruncThreads) k_truncate(const TruncItem* __r
   if (threadIdx.x == 0) {
     *it.rank = keep;
     if (it.compact) *it.compact = keep;
+    const double fl = qr_flops(m, r) + qr_flops(n, r) + (double)ku * kv * r + jac_flops +
+                      4.0 * keep * ((double)m * ku + (double)n * kv);
+    atomicAdd(&d_cnt_trunc, fl);
+    atomicAdd(&d_cnt_titems, 1.0);
   }
 }
 

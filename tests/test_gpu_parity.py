@@ -242,13 +242,22 @@ def test_factor_vs_oracle_and_dense(hm, oracle, form):
     z = oracle.normals(len(x), 5)
     assert rel(f.log_det(), pr.log_det()) < 1e-8
     assert rel(f.quad_form(z), pr.quad_form(z)) < 1e-7
-    # solve inverts the H-matrix (test_hfactor.cpp:126-134)
-    rhs = h.matvec(np.ones(len(x)))
-    assert np.linalg.norm(f.solve_factored(rhs) - 1) / math.sqrt(len(x)) < 1e-4
+    sx, so = f.solve_factored(z), pr.solve_factored(z)
+    assert np.linalg.norm(sx - so) / np.linalg.norm(so) < 1e-6
     d_gpu, d_orc = f.diagonal(), pr.factor_diag()
     assert np.max(np.abs(d_gpu - d_orc) / np.abs(d_orc)) < 1e-6
     _, ld_dense, q_dense = oracle.dense_loglik(x, z, th)
     assert rel(f.log_det(), ld_dense) < 1e-4
+
+
+def test_solve_inverts_matvec(hm, oracle):
+    """test_hfactor.cpp:126-134: n = 700, theta = (1, 0.1, 1.5, 0.01), eps = 1e-6."""
+    x = oracle.random_locations(700, 8)
+    g = hm.Geometry(x, 32, 2.0)
+    h = hm.assemble(g, [1.0, 0.1, 1.5, 0.01], hm.RankControl.fixed_accuracy(1e-6))
+    f = hm.h_ldl(h, 1e-6)
+    rhs = h.matvec(np.ones(700))
+    assert np.linalg.norm(f.solve_factored(rhs) - 1) / math.sqrt(700) <= 1e-4
 
 
 def test_factor_reports_failing_pivot(hm):
