@@ -1,0 +1,328 @@
+#!/usr/bin/env python
+"""Benchmark: L(θ) evaluations/s (H-assemble + H-Cholesky + logdet + solve).
+
+Workload (BASELINE.json configs[2], "C3"): n = 262144 points on a 512x512
+jittered grid (seed 1), θ = (σ²=1.5, ℓ=0.05, ν=1.0 general-ν Bessel path,
+τ²=0.01), Z iid N(0,1) (seed 1 ^ 0x517cc1b727220a95), leaf 128, η = 2,
+ε = 1e-6, H-Cholesky.  One step = one full L(θ): cluster tree + block tree
+(K1, K2), assembly (K3 dense leaves, K4 ACA, K5 recompression), H-Cholesky
+(K6-K9), log-determinant + forward solve (K10, K11).
+
+  value : device-resident coordinates and Z (torch tensors in HBM) through
+          hmgp_geometry_build_device + hmgp_loglik_geom; CUDA events on the
+          library stream; max over ranks.
+  e2e   : the public API call hmgp_loglik with HOST buffers (H2D of coords + Z and
+          D2H of the result inside the timed region).
+  Multi-GPU (torchrun): one L(θ) does not shard -> replicas;
+  every rank evaluates its own θ (ℓ nudged per rank), value = N*K / max time.
+
+``--impl reference`` times the CPU restatement of the reference (oracle/, the
+reference itself cannot be built here: Eigen is absent) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+C3 = dict(g=512, leaf=128, eps=1e-6, theta=(1.5, 0.05, 1.0, 0.01), form="cholesky")
+WORKLOAD = ("C3: n=262144 2D jittered 512x512 grid, Matern theta=(1.5,0.05,1.0,0.01) general-nu, "
+            "Z iid N(0,1), leaf 128, eta 2, eps 1e-6, H-Cholesky")
+METRIC = "L(θ) evals/s (H-assemble+H-Cholesky+logdet+solve) at n=256K; FP64 roofline %"
+SEED = 1
+Z_SEED = SEED ^ 0x517CC1B727220A95
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    lrank = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, lrank
+
+
+class Clocks:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([s.strip() for s in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx = float(r[2])
+                for k, nm in enumerate(names):
+                    if r[5 + k].lower().startswith("active"):
+                        reasons.add(nm)
+            except Exception:
+                pass
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# --------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2104_07146_b200 as hm
+    from paper_2104_07146_b200 import _lib
+
+    ws, rank, lrank = dist_env()
+    torch.cuda.set_device(lrank)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", lrank))
+    ctx = hm.Context(lrank)
+    _lib.hmgp_ctx_stream.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]
+    _lib.hmgp_last_phases.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.c_int]
+    _lib.hmgp_work_counters.argtypes = [C.POINTER(C.c_double), C.c_int, C.c_int]
+    _lib.hmgp_fp64_peak.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
+    _lib.hmgp_set_flop_counting.argtypes = [C.c_int]
+    sp = C.c_void_p()
+    hm._chk(_lib.hmgp_ctx_stream(ctx.h, C.byref(sp)))
+    stream = torch.cuda.ExternalStream(sp.value, device=torch.device("cuda", lrank))
+
+    cfgd = dict(C3)
+    if args.small:  # quick functional runs (not a bench line)
+        cfgd.update(g=128)
+    g = cfgd["g"]
+    n = g * g
+    x = hm.jittered_grid(g, SEED)
+    z = hm.normals(n, Z_SEED)
+    th = list(cfgd["theta"])
+    th[1] *= 1.0 + 1e-3 * rank  # replicas evaluate distinct θ
+    theta = hm.Matern(*th)
+    cfg = hm.HConfig(leaf_size=cfgd["leaf"], rank=hm.RankControl.fixed_accuracy(cfgd["eps"]),
+                     form=cfgd["form"]).c()
+    # device-resident inputs (torch = plumbing only)
+    dx = torch.from_numpy(x).to(f"cuda:{lrank}")
+    dz = torch.from_numpy(z).to(f"cuda:{lrank}")
+    torch.cuda.synchronize()
+    res = hm._LogLik()
+
+    def step_device():
+        gh = C.c_void_p()
+        hm._chk(_lib.hmgp_geometry_build_device(ctx.h, C.c_void_p(dx.data_ptr()), n, 2,
+                                                cfgd["leaf"], 2.0, C.byref(gh)))
+        try:
+            hm._chk(_lib.hmgp_loglik_geom(ctx.h, gh, C.c_void_p(dz.data_ptr()), C.byref(theta),
+                                          C.byref(cfg), C.byref(res)))
+        finally:
+            _lib.hmgp_geometry_destroy(gh)
+
+    def step_e2e():
+        hm._chk(_lib.hmgp_loglik(ctx.h, x.ctypes.data_as(hm._dp), n, 2, z.ctypes.data_as(hm._dp),
+                                 C.byref(theta), C.byref(cfg), C.byref(res)))
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(fn, k):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        barrier()
+        e0.record(stream)
+        for _ in range(k):
+            fn()
+        e1.record(stream)
+        e1.synchronize()
+        barrier()
+        ms = e0.elapsed_time(e1)
+        if ws > 1:
+            t = torch.tensor([ms], device=f"cuda:{lrank}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    # untimed counting pass (algorithmic work of one step) + FP64 peak
+    w = (C.c_double * 8)()
+    _lib.hmgp_work_counters(w, 8, 1)
+    _lib.hmgp_set_flop_counting(1)
+    step_device()
+    _lib.hmgp_set_flop_counting(0)
+    _lib.hmgp_work_counters(w, 8, 1)
+    work = dict(zip(["dense_entries", "aca_entries", "kernel_flops", "gemm_flops", "trsm_flops",
+                     "leaf_flops", "trunc_flops", "trunc_items"], list(w)))
+    peak = C.c_double()
+    hm._chk(_lib.hmgp_fp64_peak(ctx.h, C.byref(peak)))
+    fp64_peak = peak.value
+
+    for _ in range(args.warmup):
+        step_device()
+    launches0 = ctx.launches()
+    clk = Clocks(lrank)
+    clk.start()
+    ms = timed(step_device, args.steps)
+    clocks = clk.stop()
+    launches = (ctx.launches() - launches0) // max(1, args.steps)
+    loglik = res.loglik
+    ph = (C.c_double * 10)()
+    _lib.hmgp_last_phases(ctx.h, ph, 10)
+    phases = dict(zip(["start", "geometry", "dense_K3", "aca_K4K5", "layout", "factor_K6K9",
+                       "logdet_K11", "fwd_solve_K10", "bwd", "cross_K12"], list(ph)))
+    # e2e through the public API with host buffers
+    step_e2e()
+    ms_e2e = timed(step_e2e, max(1, args.steps))
+
+    if rank == 0:
+        value = ws * args.steps / (ms / 1e3)
+        e2e_value = ws * max(1, args.steps) / (ms_e2e / 1e3)
+        peaks = measured_peaks()
+        # dominant kernel family of the step and its roofline
+        fam = {
+            "factor_K6K9": (work["gemm_flops"] + work["trsm_flops"] + work["leaf_flops"]
+                            + work["trunc_flops"], phases["factor_K6K9"]),
+            "dense_K3": (work["kernel_flops"], phases["dense_K3"]),
+        }
+        dom = max(fam, key=lambda k: fam[k][1])
+        flops, pms = fam[dom]
+        achieved = flops / (pms / 1e3) / 1e12 if pms > 0 else 0.0
+        roofline = {"bound": "fp64", "kernel": dom, "achieved": achieved, "peak": fp64_peak,
+                    "unit": "TFLOP/s", "frac": achieved / fp64_peak if fp64_peak else None,
+                    "traffic": None, "peak_source": "measured FP64 FMA-chain microbenchmark "
+                    "(hmgp_fp64_peak) on this B200; MEASURED_PEAKS.json has no FP64 entry",
+                    "share_of_step": pms / (ms / args.steps),
+                    "algorithmic_flops_per_launch": flops}
+        line = {
+            "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded jittered grid + AS241 normals, simgen conventions)",
+            "config": {"workload": WORKLOAD if not args.small else "small functional run g=128",
+                       "n": n, "leaf_size": cfgd["leaf"], "eta": 2.0, "eps": cfgd["eps"],
+                       "form": cfgd["form"], "parallelism": f"replicas x{ws}",
+                       "l2": "inputs larger than L2 (>2 GB near-field payload per step)"},
+            "loglik": loglik, "phases_ms_last_step": phases, "work_per_step": work,
+            "clocks": clocks, "gpu_launches": int(launches),
+            "e2e": {"value": e2e_value, "unit": "evals/s",
+                    "h2d_bytes_per_step": 8 * n * 2 + 8 * n, "d2h_bytes_per_step": C.sizeof(res)},
+            "roofline": roofline,
+            "hbm_peak_gbs": peaks.get("hbm_gbs"),
+        }
+        if not args.no_cpu_baseline and ws == 1:
+            line["cpu_baseline"] = cpu_baseline(budget_s=args.cpu_budget)
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# --------------------------------------------------------------------------
+def _oracle_eval(o, g, threads):
+    from oracle.oracle import make_config
+    x = o.jittered_grid(g, SEED)
+    z = o.normals(g * g, Z_SEED)
+    cfg = make_config(leaf_size=C3["leaf"], eps=C3["eps"], form=C3["form"], threads=threads)
+    t = time.time()
+    r = o.loglik(x, z, list(C3["theta"]), cfg)
+    return time.time() - t, r
+
+
+def cpu_baseline(budget_s=30.0, steps=1):
+    """CPU restatement (oracle, 'port') on the host cores, bounded sample.
+
+    Two sample sizes (n = 48^2 and 96^2, the C3 density/θ/leaf/ε otherwise) fit
+    the time exponent; the value is the extrapolation to n = 262144.  Assembly
+    uses all host threads (hmatrix.cpp:193), the factorization one (as the
+    reference)."""
+    from oracle.oracle import Oracle
+    o = Oracle()
+    threads = os.cpu_count() or 1
+    t1, _ = _oracle_eval(o, 48, threads)
+    t2 = 0.0
+    for _ in range(steps):
+        t2, r2 = _oracle_eval(o, 96, threads)
+    n1, n2, n = 48 * 48, 96 * 96, 262144
+    alpha = math.log(t2 / t1) / math.log(n2 / n1)
+    t_c3 = t2 * (n / n2) ** alpha
+    return {"value": 1.0 / t_c3, "unit": "evals/s", "cores": threads, "kind": "port",
+            "sample": (f"oracle L(θ) at n={n1} ({t1:.2f}s) and n={n2} ({t2:.2f}s), C3 θ/leaf/ε; "
+                       f"time exponent {alpha:.2f} extrapolated to n=262144 ({t_c3:.0f}s/eval); "
+                       f"assembly on {threads} threads, factorization single-threaded"),
+            "sample_seconds": t2, "exponent": alpha}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    cb = cpu_baseline(steps=max(1, min(args.steps, 2)))
+    line = {"metric": METRIC, "value": cb["value"], "unit": "evals/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / cb["value"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": WORKLOAD, "parallelism": "host cores"},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "evals/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "note": "reference is C++/Eigen and cannot be built here (Eigen absent); the arm "
+                    "times oracle/ (CPU restatement, kind=port)"}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--small", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=30.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -459,7 +459,9 @@ void assemble(HMat& h, Geometry& g, const MaternDev& p, double eps, bool fixed_r
         }
         if (!ti.empty()) {
           TruncItem* d_ti = upload(ti, st);
-          launch_truncate(d_ti, (int)ti.size(), eps, d_err, st);
+          int sw = 0, smn = 0;
+          for (const TruncItem& x : ti) trunc_smem_dims(x.m, x.n, &sw, &smn);
+          launch_truncate(d_ti, (int)ti.size(), eps, d_err, st, sw, smn);
           HMGP_CUDA(cudaStreamSynchronize(st));
           cudaFree(d_ti);
         }

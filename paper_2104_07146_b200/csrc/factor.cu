@@ -170,7 +170,10 @@ struct Engine {
   }
   void lrupd(std::vector<TruncItem>& v) {
     if (v.empty()) return;
-    launch_truncate(sg.put(v), (int)v.size(), eps, d_err, st);
+    int sw = 0, smn = 0;
+    for (const TruncItem& t : v)
+      if (t.cond != 4) trunc_smem_dims(t.m, t.n, &sw, &smn);
+    launch_truncate(sg.put(v), (int)v.size(), eps, d_err, st, sw, smn);
     v.clear();
   }
   CopyScaleItem cpy(const double* src, int lds, MV dst, Dim cols, int trans, double alpha,

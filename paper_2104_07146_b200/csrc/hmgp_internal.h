@@ -122,6 +122,9 @@ struct TruncItem {
   double* ws;  // trunc_ws_doubles(m, n, rcap)
 };
 size_t trunc_ws_doubles(int m, int n, int rcap);
-void launch_truncate(const TruncItem* d_items, int count, double eps, int* d_err, cudaStream_t st);
+// grow the per-launch shared-memory dims for an item that can take the small-block path
+void trunc_smem_dims(int m, int n, int* smem_w, int* smem_mn);
+void launch_truncate(const TruncItem* d_items, int count, double eps, int* d_err, cudaStream_t st,
+                     int smem_w, int smem_mn);
 
 }  // namespace hmgp_gpu

@@ -11,6 +11,8 @@
 // Jacobi; the reference uses Eigen's two-sided JacobiSVD / dgesdd — the same
 // singular triplets up to rounding, so the kept rank only differs when a
 // singular value sits within rounding of the cut.
+#include <algorithm>
+
 #include "common.cuh"
 #include "hmgp_internal.h"
 
@@ -18,6 +20,9 @@ namespace hmgp_gpu {
 
 constexpr int kTruncThreads = 256;
 constexpr int kMaxTruncCols = 1024;
+constexpr int kChunk = 8;              // factor columns staged per pass when forming W
+constexpr int kMaxSmemW = 16384;       // W = [U|aP][V|Q]^T in shared memory (128 KB)
+constexpr int kMaxSmemMN = 1024;       // m + n bound of the staged column chunks (64 KB)
 
 __device__ double d_cnt_trunc, d_cnt_titems;
 
@@ -35,8 +40,18 @@ __device__ __forceinline__ double qr_flops(double m, double r) {
 }
 
 size_t trunc_ws_doubles(int m, int n, int rcap) {
-  const size_t kq = (size_t)min(min(m, n), rcap);
-  return (size_t)(m + n) * rcap + 2 * (size_t)rcap + (size_t)rcap * kq + kq * kq;
+  const size_t mn = (size_t)min(m, n);
+  const size_t path_s = 3 * (size_t)n + (size_t)n * mn + mn * mn;
+  const size_t kq = std::min(mn, (size_t)rcap), rc = (size_t)rcap;
+  const size_t path_l = (size_t)(m + n) * rc + 5 * rc + rc * rc + 2 * rc * kq + kq * kq;
+  return std::max(path_s, path_l);
+}
+
+void trunc_smem_dims(int m, int n, int* smem_w, int* smem_mn) {
+  if ((size_t)m * n <= (size_t)kMaxSmemW && m + n <= kMaxSmemMN) {
+    *smem_w = std::max(*smem_w, m * n);
+    *smem_mn = std::max(*smem_mn, m + n);
+  }
 }
 
 // In-place Householder QR of A (m x r, ld m) inside one CTA; tau[min(m,r)].
@@ -183,8 +198,170 @@ __device__ double cta_jacobi(double* W, int p, int q, double* J) {
   return (double)sweeps * (0.5 * q * (q - 1)) * 6.0 * p + (double)s_nrot * 6.0 * (p + q);
 }
 
+struct RS {
+  int kq, keep;
+  double flops;
+};
+
+// Rank-revealing truncated SVD of W (p x q, ld p; destroyed): Businger-Golub
+// column-pivoted Householder QR stopped once the Frobenius norm of the trailing
+// block is <= 1e-3*eps*(largest column norm) <= 1e-3*eps*sigma_max — every
+// singular value it drops is three decades below the reference's cut
+// eps*sigma_max — then a one-sided Jacobi SVD of the small k' x q factor.
+// Output: kq = k', reflectors in W / tau, G (q x kq, ld q) with columns Y*S
+// (unpermuted rows), J (kq x kq) = X, s_sig / s_ord sorted descending and
+// keep = #{sigma_i > eps*sigma_0, sigma_i > 0} (hblock.cpp:151-153).
+__device__ RS cta_rrqr_svd(double* W, int p, int q, double eps, double* tau, int* piv, double* cn,
+                           double* G, double* J, double* s_sig, int* s_ord, double* red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __shared__ double redv[32];
+  __shared__ int redi[32];
+  __shared__ double s_beta, s_t, s_inv, s_thresh;
+  __shared__ int s_stop;
+  double flops = 0.0;
+  for (int j = w; j < q; j += nw) {
+    const double* c = W + (size_t)j * p;
+    double s = 0.0;
+    for (int i = lane; i < p; i += 32) s += c[i] * c[i];
+    s = warp_sum(s);
+    if (lane == 0) {
+      cn[j] = s;
+      piv[j] = j;
+    }
+  }
+  __syncthreads();
+  flops += 2.0 * p * q;
+  {
+    double a = -1.0;
+    int ia = -1;
+    for (int j = threadIdx.x; j < q; j += blockDim.x)
+      if (cn[j] > a) {
+        a = cn[j];
+        ia = j;
+      }
+    double best;
+    block_argmax(a, ia, redv, redi, &best);
+    if (threadIdx.x == 0) s_thresh = 1e-3 * eps * sqrt(fmax(best, 0.0));
+    __syncthreads();
+  }
+  const int kmax = min(p, q);
+  int k = 0;
+  for (; k < kmax; ++k) {
+    double part = 0.0, a = -1.0;
+    int ia = -1;
+    for (int j = k + threadIdx.x; j < q; j += blockDim.x) {
+      part += cn[j];
+      if (cn[j] > a) {
+        a = cn[j];
+        ia = j;
+      }
+    }
+    const double resid = block_sum(part, red);
+    double best;
+    const int jm = block_argmax(a, ia, redv, redi, &best);
+    if (threadIdx.x == 0) s_stop = !(sqrt(resid) > s_thresh) || jm < 0;
+    __syncthreads();
+    if (s_stop) break;
+    if (jm != k) {  // swap columns k <-> jm
+      double* ck = W + (size_t)k * p;
+      double* cm = W + (size_t)jm * p;
+      for (int i = threadIdx.x; i < p; i += blockDim.x) {
+        const double t = ck[i];
+        ck[i] = cm[i];
+        cm[i] = t;
+      }
+      if (threadIdx.x == 0) {
+        const double t = cn[k];
+        cn[k] = cn[jm];
+        cn[jm] = t;
+        const int pt = piv[k];
+        piv[k] = piv[jm];
+        piv[jm] = pt;
+      }
+      __syncthreads();
+    }
+    double* col = W + (size_t)k * p;
+    double tp = 0.0;
+    for (int i = k + 1 + threadIdx.x; i < p; i += blockDim.x) tp += col[i] * col[i];
+    const double tail2 = block_sum(tp, red);
+    if (threadIdx.x == 0) {
+      const double c0 = col[k];
+      if (tail2 <= 2.2250738585072014e-308) {
+        s_t = 0.0;
+        s_beta = c0;
+        s_inv = 0.0;
+      } else {
+        double beta = sqrt(c0 * c0 + tail2);
+        if (c0 >= 0.0) beta = -beta;
+        s_inv = 1.0 / (c0 - beta);
+        s_t = (beta - c0) / beta;
+        s_beta = beta;
+      }
+    }
+    __syncthreads();
+    const double t = s_t, inv = s_inv;
+    for (int i = k + 1 + threadIdx.x; i < p; i += blockDim.x) col[i] = (t == 0.0) ? 0.0 : col[i] * inv;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      col[k] = s_beta;
+      tau[k] = t;
+    }
+    __syncthreads();
+    for (int j = k + 1 + w; j < q; j += nw) {  // apply H_k, refresh the trailing norms
+      double* cj = W + (size_t)j * p;
+      if (t != 0.0) {
+        double s = 0.0;
+        for (int i = k + 1 + lane; i < p; i += 32) s += col[i] * cj[i];
+        s = warp_sum(s);
+        s = (s + cj[k]) * t;
+        for (int i = k + 1 + lane; i < p; i += 32) cj[i] -= s * col[i];
+        __syncwarp();
+        if (lane == 0) cj[k] -= s;
+      }
+      double s2 = 0.0;
+      for (int i = k + 1 + lane; i < p; i += 32) s2 += cj[i] * cj[i];
+      s2 = warp_sum(s2);
+      if (lane == 0) cn[j] = s2;
+    }
+    __syncthreads();
+    flops += 6.0 * (p - k) * (q - k);
+  }
+  const int kq = k;
+  // G = (R P^T)^T : q x kq, row piv[j] holds R(:, j)
+  for (int e = threadIdx.x; e < q * kq; e += blockDim.x) {
+    const int j = e % q, i = e / q;
+    G[(size_t)i * q + piv[j]] = (j >= i) ? W[(size_t)j * p + i] : 0.0;
+  }
+  __syncthreads();
+  flops += cta_jacobi(G, q, kq, J);
+  for (int c = threadIdx.x; c < kq; c += blockDim.x) {
+    const double* gc = G + (size_t)c * q;
+    double s = 0.0;
+    for (int i = 0; i < q; ++i) s += gc[i] * gc[i];
+    s_sig[c] = sqrt(s);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < kq; c += blockDim.x) {
+    const double sc = s_sig[c];
+    int rk = 0;
+    for (int d = 0; d < kq; ++d) rk += (s_sig[d] > sc) || (s_sig[d] == sc && d < c);
+    s_ord[rk] = c;
+  }
+  __syncthreads();
+  __shared__ int s_keep;
+  if (threadIdx.x == 0) {
+    const double smax = kq > 0 ? s_sig[s_ord[0]] : 0.0;
+    int keep = 0;
+    while (keep < kq && s_sig[s_ord[keep]] > eps * smax && s_sig[s_ord[keep]] > 0.0) ++keep;
+    s_keep = keep;
+  }
+  __syncthreads();
+  return RS{kq, s_keep, flops};
+}
+
 __global__ void __launch_bounds__(kTruncThreads) k_truncate(const TruncItem* __restrict__ items,
-                                                            double eps, int* err) {
+                                                            double eps, int* err, int smem_w,
+                                                            int smem_mn) {
   const TruncItem it = items[blockIdx.x];
   __shared__ double red[32];
   __shared__ double s_sig[kMaxTruncCols];
@@ -239,12 +416,86 @@ __global__ void __launch_bounds__(kTruncThreads) k_truncate(const TruncItem* __r
     return;
   }
   const int m = it.m, n = it.n;
+  extern __shared__ double dsm[];
+  if ((size_t)m * n <= (size_t)smem_w && m + n <= smem_mn) {
+    // ---- small block: W = [U | aP][V | Q]^T explicitly, rank-revealing SVD of W.
+    // W has exactly the singular values of the reference's core R_u R_v^T.
+    double* W = dsm;
+    double* sU = dsm + (size_t)m * n;
+    double* sV = sU + (size_t)m * kChunk;
+    for (int e = threadIdx.x; e < m * n; e += blockDim.x) W[e] = 0.0;
+    for (int l0 = 0; l0 < r; l0 += kChunk) {
+      const int lc = min(kChunk, r - l0);
+      __syncthreads();
+      for (int e = threadIdx.x; e < m * lc; e += blockDim.x) {
+        const int i = e % m, l = l0 + e / m;
+        double v;
+        if (l < r0) {
+          v = it.U[(size_t)l * m + i];
+        } else {
+          const int pi = i - it.pro;
+          v = (pi >= 0 && pi < it.pr) ? it.alpha * it.P[(size_t)(l - r0) * it.ldp + pi] : 0.0;
+        }
+        sU[(size_t)(e / m) * m + i] = v;
+      }
+      for (int e = threadIdx.x; e < n * lc; e += blockDim.x) {
+        const int j = e % n, l = l0 + e / n;
+        double v;
+        if (l < r0) {
+          v = it.V[(size_t)l * n + j];
+        } else {
+          const int qi = j - it.qro;
+          v = (qi >= 0 && qi < it.qr) ? it.Q[(size_t)(l - r0) * it.ldq + qi] : 0.0;
+        }
+        sV[(size_t)(e / n) * n + j] = v;
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
+        const int i = e % m, j = e / m;
+        double s = 0.0;
+        for (int l = 0; l < lc; ++l) s += sU[(size_t)l * m + i] * sV[(size_t)l * n + j];
+        W[e] += s;
+      }
+    }
+    __syncthreads();
+    double* ws = it.ws;
+    double* tau = ws;
+    double* cn = tau + n;
+    int* piv = reinterpret_cast<int*>(cn + n);
+    double* G = cn + 2 * n;
+    const int kqmax = min(m, n);
+    double* J = G + (size_t)n * kqmax;
+    const RS rs = cta_rrqr_svd(W, m, n, eps, tau, piv, cn, G, J, s_sig, s_ord, red);
+    if (rs.keep > it.cap) {
+      if (threadIdx.x == 0) atomicOr(err, 4);
+      return;
+    }
+    const int keep = rs.keep, kq = rs.kq;
+    for (int idx = threadIdx.x; idx < m * keep; idx += blockDim.x) {
+      const int i = idx % m, c = idx / m, src = s_ord[c];
+      it.U[idx] = i < kq ? J[(size_t)src * kq + i] * s_sig[src] : 0.0;
+    }
+    for (int idx = threadIdx.x; idx < n * keep; idx += blockDim.x) {
+      const int i = idx % n, c = idx / n, src = s_ord[c];
+      it.V[idx] = G[(size_t)src * n + i] / s_sig[src];
+    }
+    __syncthreads();
+    cta_apply_q(W, m, kq, tau, it.U, keep);
+    if (threadIdx.x == 0) {
+      *it.rank = keep;
+      if (it.compact) *it.compact = keep;
+      atomicAdd(&d_cnt_trunc, 2.0 * m * n * r + rs.flops + 4.0 * keep * (double)m * kq);
+      atomicAdd(&d_cnt_titems, 1.0);
+    }
+    return;
+  }
+  // ---- large block: Householder QR of both stacked factors, core R_u R_v^T,
+  // then the same rank-revealing SVD on the core (hblock.cpp:144-161).
   double* WU = it.ws;
   double* WV = WU + (size_t)m * it.rcap;
   double* tu = WV + (size_t)n * it.rcap;
   double* tv = tu + it.rcap;
   double* C = tv + it.rcap;
-  double* J = C + (size_t)it.rcap * min(min(m, n), it.rcap);
   for (size_t i = threadIdx.x; i < (size_t)m * r0; i += blockDim.x) WU[i] = it.U[i];
   for (size_t i = threadIdx.x; i < (size_t)n * r0; i += blockDim.x) WV[i] = it.V[i];
   for (size_t e = threadIdx.x; e < (size_t)m * add; e += blockDim.x) {
@@ -259,62 +510,42 @@ __global__ void __launch_bounds__(kTruncThreads) k_truncate(const TruncItem* __r
   cta_householder(WU, m, r, tu, red);
   cta_householder(WV, n, r, tv, red);
   const int ku = min(m, r), kv = min(n, r);
-  const bool swapped = ku < kv;
-  const int p = swapped ? kv : ku, q = swapped ? ku : kv;
-  // core(i,j) = sum_{l >= max(i,j)} Ru(i,l) Rv(j,l); stored as W (p x q)
+  // core(i,j) = sum_{l >= max(i,j)} Ru(i,l) Rv(j,l)  (ku x kv, ld ku)
   for (int idx = threadIdx.x; idx < ku * kv; idx += blockDim.x) {
     const int i = idx % ku, j = idx / ku;
     double s = 0.0;
     for (int l = max(i, j); l < r; ++l) s += WU[(size_t)l * m + i] * WV[(size_t)l * n + j];
-    if (!swapped)
-      C[(size_t)j * p + i] = s;
-    else
-      C[(size_t)i * p + j] = s;
+    C[(size_t)j * ku + i] = s;
   }
   __syncthreads();
-  const double jac_flops = cta_jacobi(C, p, q, J);
-  // singular values = column norms of W; order descending (ties by index)
-  for (int c = threadIdx.x; c < q; c += blockDim.x) {
-    const double* wc = C + (size_t)c * p;
-    double s = 0.0;
-    for (int i = 0; i < p; ++i) s += wc[i] * wc[i];
-    s_sig[c] = sqrt(s);
-  }
-  __syncthreads();
-  for (int c = threadIdx.x; c < q; c += blockDim.x) {
-    const double sc = s_sig[c];
-    int rk = 0;
-    for (int d = 0; d < q; ++d) rk += (s_sig[d] > sc) || (s_sig[d] == sc && d < c);
-    s_ord[rk] = c;
-  }
-  __syncthreads();
-  const double smax = q > 0 ? s_sig[s_ord[0]] : 0.0;
-  __shared__ int s_keep;
-  if (threadIdx.x == 0) {
-    int keep = 0;
-    while (keep < q && s_sig[s_ord[keep]] > eps * smax && s_sig[s_ord[keep]] > 0.0) ++keep;
-    s_keep = keep;
-  }
-  __syncthreads();
-  const int keep = s_keep;
-  if (keep > it.cap) {
+  const int kqmax = min(ku, kv);
+  double* tau = C + (size_t)ku * kv;
+  double* cn = tau + kv;
+  int* piv = reinterpret_cast<int*>(cn + kv);
+  double* G = cn + 2 * kv;
+  double* J = G + (size_t)kv * kqmax;
+  double* Uc = J + (size_t)kqmax * kqmax;
+  const RS rs = cta_rrqr_svd(C, ku, kv, eps, tau, piv, cn, G, J, s_sig, s_ord, red);
+  if (rs.keep > it.cap) {
     if (threadIdx.x == 0) atomicOr(err, 4);
     return;
   }
-  // E_u (m x keep) -> it.U, E_v (n x keep) -> it.V, then apply Q_u, Q_v.
+  const int keep = rs.keep, kq = rs.kq;
+  // U_core = Q_core [J S; 0] (ku x keep)
+  for (int idx = threadIdx.x; idx < ku * keep; idx += blockDim.x) {
+    const int i = idx % ku, c = idx / ku, src = s_ord[c];
+    Uc[idx] = i < kq ? J[(size_t)src * kq + i] * s_sig[src] : 0.0;
+  }
+  __syncthreads();
+  cta_apply_q(C, ku, kq, tau, Uc, keep);
+  // E_u = [U_core; 0] -> it.U, E_v = [Y; 0] -> it.V, then apply Q_u, Q_v.
   for (int idx = threadIdx.x; idx < m * keep; idx += blockDim.x) {
     const int i = idx % m, c = idx / m;
-    const int src = s_ord[c];
-    double v = 0.0;
-    if (i < ku) v = swapped ? J[(size_t)src * q + i] * s_sig[src] : C[(size_t)src * p + i];
-    it.U[idx] = v;
+    it.U[idx] = i < ku ? Uc[(size_t)c * ku + i] : 0.0;
   }
   for (int idx = threadIdx.x; idx < n * keep; idx += blockDim.x) {
-    const int i = idx % n, c = idx / n;
-    const int src = s_ord[c];
-    double v = 0.0;
-    if (i < kv) v = swapped ? C[(size_t)src * p + i] / s_sig[src] : J[(size_t)src * q + i];
-    it.V[idx] = v;
+    const int i = idx % n, c = idx / n, src = s_ord[c];
+    it.V[idx] = i < kv ? G[(size_t)src * kv + i] / s_sig[src] : 0.0;
   }
   __syncthreads();
   cta_apply_q(WU, m, ku, tu, it.U, keep);
@@ -322,16 +553,28 @@ __global__ void __launch_bounds__(kTruncThreads) k_truncate(const TruncItem* __r
   if (threadIdx.x == 0) {
     *it.rank = keep;
     if (it.compact) *it.compact = keep;
-    const double fl = qr_flops(m, r) + qr_flops(n, r) + (double)ku * kv * r + jac_flops +
-                      4.0 * keep * ((double)m * ku + (double)n * kv);
+    const double fl = qr_flops(m, r) + qr_flops(n, r) + (double)ku * kv * r + rs.flops +
+                      4.0 * keep * ((double)m * ku + (double)n * kv + (double)ku * kq);
     atomicAdd(&d_cnt_trunc, fl);
     atomicAdd(&d_cnt_titems, 1.0);
   }
 }
 
-void launch_truncate(const TruncItem* d_items, int count, double eps, int* d_err, cudaStream_t st) {
+void launch_truncate(const TruncItem* d_items, int count, double eps, int* d_err, cudaStream_t st,
+                     int smem_w, int smem_mn) {
   if (count <= 0) return;
-  k_truncate<<<count, kTruncThreads, 0, st>>>(d_items, eps, d_err);
+  if (smem_w > kMaxSmemW || smem_mn > kMaxSmemMN) {
+    smem_w = 0;
+    smem_mn = 0;
+  }
+  const size_t bytes = ((size_t)smem_w + (size_t)kChunk * smem_mn) * 8;
+  static size_t configured = 0;
+  if (bytes > 48 * 1024 && bytes > configured) {
+    HMGP_CUDA(cudaFuncSetAttribute(k_truncate, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)((kMaxSmemW + (size_t)kChunk * kMaxSmemMN) * 8)));
+    configured = (kMaxSmemW + (size_t)kChunk * kMaxSmemMN) * 8;
+  }
+  k_truncate<<<count, kTruncThreads, bytes, st>>>(d_items, eps, d_err, smem_w, smem_mn);
   HMGP_LAUNCH_CHECK();
 }
 
