@@ -27,17 +27,19 @@
 
 namespace hmgp_gpu {
 
-constexpr int TCAP = 512;  // width bound of product temporaries (checked on device)
 
 // ------------------------------------------------------------ utilities ---
 struct Arena {
   char* base = nullptr;
   size_t cap = 0, top = 0, peak = 0;
-  void init(size_t bytes) {
+  void init(size_t bytes) {  // persistent: reallocate only to grow
+    top = peak = 0;
+    if (base && cap >= bytes) return;
+    if (base) cudaFree(base);
+    base = nullptr;
     cap = bytes;
     HMGP_CUDA(cudaMalloc(&base, cap));
   }
-  ~Arena() { cudaFree(base); }
   size_t mark() const { return top; }
   void release(size_t m) { top = m; }
   void* raw(size_t bytes) {
@@ -57,15 +59,13 @@ struct Stager {
   char* d = nullptr;
   size_t cap = 0, off = 0;
   cudaStream_t st = nullptr;
-  void init(size_t bytes, cudaStream_t s) {
-    cap = bytes;
+  void init(size_t bytes, cudaStream_t s) {  // persistent across factorizations
     st = s;
+    off = 0;
+    if (h) return;
+    cap = bytes;
     HMGP_CUDA(cudaMallocHost(&h, cap));
     HMGP_CUDA(cudaMalloc(&d, cap));
-  }
-  ~Stager() {
-    cudaFreeHost(h);
-    cudaFree(d);
   }
   template <class T>
   const T* put(const std::vector<T>& v) {
@@ -101,18 +101,25 @@ static MV cols_of(MV m, int c0, int cnt) {  // structural columns only
 }
 
 // ----------------------------------------------------------- the engine ---
+// Per host thread (evaluate_loglik is reentrant): device
+// temporaries reused by every factorization of the thread (grows), and the
+// item-descriptor ring.
+thread_local Arena g_arena;
+thread_local Stager g_stager;
+
 struct Engine {
   Factor& F;
   const Geometry& G;
   cudaStream_t st;
-  Arena ar;
-  Stager sg;
+  Arena& ar;
+  Stager& sg;
   bool ldl;
   double eps;
   int* d_err = nullptr;
+  int TCAP;  // width capacity of product temporaries; overflow is detected on device
 
-  Engine(Factor& f, cudaStream_t s, size_t arena_bytes)
-      : F(f), G(*f.g), st(s), ldl(f.ldl), eps(f.eps) {
+  Engine(Factor& f, cudaStream_t s, size_t arena_bytes, int tcap)
+      : F(f), G(*f.g), st(s), ar(g_arena), sg(g_stager), ldl(f.ldl), eps(f.eps), TCAP(tcap) {
     ar.init(arena_bytes);
     sg.init((size_t)64 << 20, s);
     d_err = ar.ints(1);
@@ -1041,7 +1048,6 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
   const int L = (int)H.leaf.size();
   // clone payload (hblock.cpp:17-28): same layout, new pool; compact_cols = 0
   HMGP_CUDA(cudaMalloc(&F.pool, std::max<size_t>(1, H.pool_doubles) * 8));
-  HMGP_CUDA(cudaMemcpyAsync(F.pool, H.pool, H.pool_doubles * 8, cudaMemcpyDeviceToDevice, st));
   F.leaf = H.leaf;
   for (auto& l : F.leaf) {
     l.a = F.pool + (l.a - H.pool);
@@ -1050,30 +1056,39 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
   HMGP_CUDA(cudaMalloc(&F.d_leaf, sizeof(LeafDev) * std::max(L, 1)));
   HMGP_CUDA(cudaMemcpyAsync(F.d_leaf, F.leaf.data(), sizeof(LeafDev) * L, cudaMemcpyHostToDevice, st));
   HMGP_CUDA(cudaMalloc(&F.d_rank, 4 * std::max(L, 1)));
-  HMGP_CUDA(cudaMemcpyAsync(F.d_rank, H.d_rank, 4ull * L, cudaMemcpyDeviceToDevice, st));
   HMGP_CUDA(cudaMalloc(&F.d_compact, 4 * std::max(L, 1)));
-  HMGP_CUDA(cudaMemsetAsync(F.d_compact, 0, 4ull * L, st));
   HMGP_CUDA(cudaMalloc(&F.d_d, 8ull * G.n));
-  HMGP_CUDA(cudaMemsetAsync(F.d_d, 0, 8ull * G.n, st));
   HMGP_CUDA(cudaMalloc(&F.d_status, sizeof(LeafFactorStatus)));
-  LeafFactorStatus s0{INT_MAX, 0, 0, 0, 0.0, INFINITY};
-  HMGP_CUDA(cudaMemcpyAsync(F.d_status, &s0, sizeof(s0), cudaMemcpyHostToDevice, st));
   F.clamp_tol = 1e-14 * H.max_diag;  // hfactor.cpp:349
 
-  {
-    Engine E(F, st, arena_bytes);
-    E.factor_diag(0);
-    // compress_all (hfactor.cpp:321-328): every LR leaf, independent
-    std::vector<int> lr;
-    for (int k = 0; k < L; ++k)
-      if (F.leaf[k].kind == LOWRANK) lr.push_back(F.leaf_node[k]);
-    E.compress(lr);
-    phase_mark(PH_FACTOR);
+  // Temporaries are sized with a width capacity TCAP; a product wider than that
+  // is detected on device (error flag) and the factorization is redone with a
+  // doubled capacity — results never depend on the capacity that succeeded.
+  for (int tcap = 128;; tcap *= 2) {
+    // clone payload (hblock.cpp:17-28): same layout; compact_cols = 0
+    HMGP_CUDA(cudaMemcpyAsync(F.pool, H.pool, H.pool_doubles * 8, cudaMemcpyDeviceToDevice, st));
+    HMGP_CUDA(cudaMemcpyAsync(F.d_rank, H.d_rank, 4ull * L, cudaMemcpyDeviceToDevice, st));
+    HMGP_CUDA(cudaMemsetAsync(F.d_compact, 0, 4ull * L, st));
+    HMGP_CUDA(cudaMemsetAsync(F.d_d, 0, 8ull * G.n, st));
+    LeafFactorStatus s0{INT_MAX, 0, 0, 0, 0.0, INFINITY};
+    HMGP_CUDA(cudaMemcpyAsync(F.d_status, &s0, sizeof(s0), cudaMemcpyHostToDevice, st));
     int err = 0;
-    HMGP_CUDA(cudaMemcpyAsync(&err, E.d_err, 4, cudaMemcpyDeviceToHost, st));
-    HMGP_CUDA(cudaStreamSynchronize(st));
-    F.arena_peak = E.ar.peak;
-    if (err) throw Error(6, "factorize: low-rank capacity exceeded (code " + std::to_string(err) + ")");
+    {
+      Engine E(F, st, arena_bytes, tcap);
+      E.factor_diag(0);
+      // compress_all (hfactor.cpp:321-328): every LR leaf, independent
+      std::vector<int> lr;
+      for (int k = 0; k < L; ++k)
+        if (F.leaf[k].kind == LOWRANK) lr.push_back(F.leaf_node[k]);
+      E.compress(lr);
+      phase_mark(PH_FACTOR);
+      HMGP_CUDA(cudaMemcpyAsync(&err, E.d_err, 4, cudaMemcpyDeviceToHost, st));
+      HMGP_CUDA(cudaStreamSynchronize(st));
+      F.arena_peak = E.ar.peak;
+    }
+    if (!err) break;
+    if (tcap >= 1024 || (err & 4))
+      throw Error(6, "factorize: low-rank capacity exceeded (code " + std::to_string(err) + ")");
   }
   LeafFactorStatus s{};
   HMGP_CUDA(cudaMemcpyAsync(&s, F.d_status, sizeof(s), cudaMemcpyDeviceToHost, st));

@@ -31,7 +31,7 @@ size_t arena_bytes_for(const HMat& h) {
   // room for the factor copy of the payload + solve work, keep 2 GiB spare
   const size_t need = h.pool_doubles * 8 + ((size_t)2 << 30);
   const size_t avail = fr > need + ((size_t)1 << 30) ? fr - need : ((size_t)1 << 30);
-  const size_t want = std::max<size_t>((size_t)8 << 30, h.pool_doubles * 8 * 3);
+  const size_t want = std::max<size_t>((size_t)48 << 30, h.pool_doubles * 8 * 3);
   return std::min(avail, want);
 }
 
