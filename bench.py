@@ -183,14 +183,14 @@ def run_ours(args):
         return ms
 
     # untimed counting pass (algorithmic work of one step) + FP64 peak
-    w = (C.c_double * 8)()
-    _lib.hmgp_work_counters(w, 8, 1)
+    w = (C.c_double * 10)()
+    _lib.hmgp_work_counters(w, 10, 1)
     _lib.hmgp_set_flop_counting(1)
     step_device()
     _lib.hmgp_set_flop_counting(0)
-    _lib.hmgp_work_counters(w, 8, 1)
+    _lib.hmgp_work_counters(w, 10, 1)
     work = dict(zip(["dense_entries", "aca_entries", "kernel_flops", "gemm_flops", "trsm_flops",
-                     "leaf_flops", "trunc_flops", "trunc_items"], list(w)))
+                     "leaf_flops", "trunc_flops", "trunc_items", "arena_peak_bytes", "factor_attempts"], list(w)))
     peak = C.c_double()
     hm._chk(_lib.hmgp_fp64_peak(ctx.h, C.byref(peak)))
     fp64_peak = peak.value

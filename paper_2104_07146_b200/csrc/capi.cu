@@ -416,10 +416,11 @@ int hmgp_work_counters(double* out, int cap, int reset) {
     g_work.leaf_flops += l;
     g_work.trunc_flops += tf;
     g_work.trunc_items += ti;
-    const double v[8] = {g_work.dense_entries, g_work.aca_entries, g_work.kernel_flops,
-                         g_work.gemm_flops,    g_work.trsm_flops,  g_work.leaf_flops,
-                         g_work.trunc_flops,   g_work.trunc_items};
-    for (int i = 0; i < cap && i < 8; ++i) out[i] = v[i];
+    const double v[10] = {g_work.dense_entries, g_work.aca_entries, g_work.kernel_flops,
+                          g_work.gemm_flops,    g_work.trsm_flops,  g_work.leaf_flops,
+                          g_work.trunc_flops,   g_work.trunc_items, g_work.arena_peak,
+                          g_work.factor_attempts};
+    for (int i = 0; i < cap && i < 10; ++i) out[i] = v[i];
     if (reset) g_work = WorkCounters{};
   })
 }

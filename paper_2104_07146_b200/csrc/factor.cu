@@ -1064,7 +1064,7 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
   // Temporaries are sized with a width capacity TCAP; a product wider than that
   // is detected on device (error flag) and the factorization is redone with a
   // doubled capacity — results never depend on the capacity that succeeded.
-  for (int tcap = 128;; tcap *= 2) {
+  for (int tcap = 256;; tcap *= 2) {
     // clone payload (hblock.cpp:17-28): same layout; compact_cols = 0
     HMGP_CUDA(cudaMemcpyAsync(F.pool, H.pool, H.pool_doubles * 8, cudaMemcpyDeviceToDevice, st));
     HMGP_CUDA(cudaMemcpyAsync(F.d_rank, H.d_rank, 4ull * L, cudaMemcpyDeviceToDevice, st));
@@ -1085,9 +1085,11 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
       HMGP_CUDA(cudaMemcpyAsync(&err, E.d_err, 4, cudaMemcpyDeviceToHost, st));
       HMGP_CUDA(cudaStreamSynchronize(st));
       F.arena_peak = E.ar.peak;
+      g_work.arena_peak = std::max(g_work.arena_peak, (double)E.ar.peak);
+      g_work.factor_attempts += 1;
     }
     if (!err) break;
-    if (tcap >= 1024 || (err & 4))
+    if (tcap >= 1024)
       throw Error(6, "factorize: low-rank capacity exceeded (code " + std::to_string(err) + ")");
   }
   LeafFactorStatus s{};

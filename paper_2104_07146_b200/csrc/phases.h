@@ -69,6 +69,7 @@ inline void phase_mark(int i) {
 struct WorkCounters {
   double dense_entries = 0, aca_entries = 0, kernel_flops = 0;
   double gemm_flops = 0, trsm_flops = 0, leaf_flops = 0, trunc_flops = 0, trunc_items = 0;
+  double arena_peak = 0, factor_attempts = 0;
 };
 extern WorkCounters g_work;
 extern bool g_count_kernel_flops;  // run the (untimed) Matérn flop-count pass

@@ -41,10 +41,10 @@ __device__ __forceinline__ double qr_flops(double m, double r) {
 
 size_t trunc_ws_doubles(int m, int n, int rcap) {
   const size_t mn = (size_t)min(m, n);
-  const size_t path_s = 3 * (size_t)n + (size_t)n * mn + mn * mn;
   const size_t kq = std::min(mn, (size_t)rcap), rc = (size_t)rcap;
-  const size_t path_l = (size_t)(m + n) * rc + 5 * rc + rc * rc + 2 * rc * kq + kq * kq;
-  return std::max(path_s, path_l);
+  if ((size_t)m * n <= (size_t)kMaxSmemW && m + n <= kMaxSmemMN)  // small-block path only
+    return 3 * (size_t)n + (size_t)n * kq + kq * kq;
+  return (size_t)(m + n) * rc + 5 * rc + rc * rc + 2 * rc * kq + kq * kq;
 }
 
 void trunc_smem_dims(int m, int n, int* smem_w, int* smem_mn) {
@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(kTruncThreads) k_truncate(const TruncItem* __r
     double* cn = tau + n;
     int* piv = reinterpret_cast<int*>(cn + n);
     double* G = cn + 2 * n;
-    const int kqmax = min(m, n);
+    const int kqmax = min(min(m, n), it.rcap);  // rank(W) <= r <= rcap
     double* J = G + (size_t)n * kqmax;
     const RS rs = cta_rrqr_svd(W, m, n, eps, tau, piv, cn, G, J, s_sig, s_ord, red);
     if (rs.keep > it.cap) {

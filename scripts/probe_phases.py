@@ -14,11 +14,11 @@ form = sys.argv[5] if len(sys.argv) > 5 else "cholesky"
 x = hm.jittered_grid(g, 1); z = hm.normals(g * g, 7)
 cfg = hm.HConfig(leaf_size=leaf, rank=hm.RankControl.fixed_accuracy(eps), form=form)
 ctx = hm.default_context()
-w = (C.c_double * 8)()
-_lib.hmgp_work_counters(w, 8, 1)
+w = (C.c_double * 10)()
+_lib.hmgp_work_counters(w, 10, 1)
 t = time.time(); r = hm.evaluate_loglik(x, z, th, cfg, ctx=ctx); wall = time.time() - t
 ph = (C.c_double * 10)(); _lib.hmgp_last_phases(ctx.h, ph, 10)
-_lib.hmgp_work_counters(w, 8, 1)
+_lib.hmgp_work_counters(w, 10, 1)
 print(f"n={g*g} leaf={leaf} th={th} {form}: wall {wall:.3f}s L={r.loglik:.10f}")
 print("phases_ms", {k: round(v, 2) for k, v in zip(NAMES, ph)})
-print("work", dict(zip(["dense_entries", "aca_entries", "kernel_flops", "gemm", "trsm", "leaf", "trunc_flops", "trunc_items"], [f"{v:.3g}" for v in w])))
+print("work", dict(zip(["dense_entries", "aca_entries", "kernel_flops", "gemm", "trsm", "leaf", "trunc_flops", "trunc_items", "arena_peak", "attempts"], [f"{v:.3g}" for v in w])))
