@@ -537,7 +537,57 @@ struct Engine {
     double alpha;
     int row0, col0;
   };
-  void add_lr(const std::vector<Add>& its) {
+  // hblock.cpp:205-216: distribute an add over a branch target's stored leaves
+  // (child order), keeping the P / Q rows that intersect each child.
+  void expand_add(const Add& a, std::vector<Add>& out) {
+    if (kind(a.c) != BRANCH) {
+      out.push_back(a);
+      return;
+    }
+    const HNode& nd = N(a.c);
+    for (int pos = 0; pos < nd.kr * nd.kc; ++pos) {
+      const int ch = nd.kids[pos];
+      if (ch < 0) continue;
+      const int r0 = std::max(a.row0, rb(ch)), r1 = std::min(a.row0 + a.p.rows, rb(ch) + nr(ch));
+      const int c0 = std::max(a.col0, cb(ch)), c1 = std::min(a.col0 + a.q.rows, cb(ch) + nc(ch));
+      if (r0 >= r1 || c0 >= c1) continue;
+      expand_add(Add{ch, rows_of(a.p, r0 - a.row0, r1 - r0), rows_of(a.q, c0 - a.col0, c1 - c0),
+                     a.alpha, r0, c0},
+                 out);
+    }
+  }
+
+  // add_low_rank for a list of terms IN REFERENCE ORDER; terms may share
+  // targets.  Every term is expanded to leaf-level adds; each leaf receives its
+  // adds in term order (the reference's sequence, so the watermark recompressions
+  // happen at the same points), adds to different leaves run in parallel:
+  // round r applies the r-th add of every leaf in one batched launch.
+  void add_lr(const std::vector<Add>& terms) {
+    if (terms.empty()) return;
+    std::vector<Add> flat;
+    for (const Add& a : terms) expand_add(a, flat);
+    std::vector<std::vector<int>> seq;  // per target leaf: indices into flat
+    std::vector<int> slot(F.nodes.size(), -1);
+    for (int i = 0; i < (int)flat.size(); ++i) {
+      int& s = slot[flat[i].c];
+      if (s < 0) {
+        s = (int)seq.size();
+        seq.emplace_back();
+      }
+      seq[s].push_back(i);
+    }
+    size_t rounds = 0;
+    for (const auto& v : seq) rounds = std::max(rounds, v.size());
+    for (size_t r = 0; r < rounds; ++r) {
+      std::vector<Add> batch;
+      for (const auto& v : seq)
+        if (r < v.size()) batch.push_back(flat[v[r]]);
+      add_leaves(batch);
+    }
+  }
+
+  // distinct leaf targets, one add each
+  void add_leaves(const std::vector<Add>& its) {
     if (its.empty()) return;
     std::vector<GemmItem> g;
     std::vector<TruncItem> t;
@@ -571,22 +621,6 @@ struct Engine {
     gemm(g);
     lrupd_ws(t);
     ar.release(mk);
-    if (!br.empty()) {  // hblock.cpp:205-216
-      std::vector<Add> sub;
-      for (const Add& a : br) {
-        const HNode& nd = N(a.c);
-        for (int pos = 0; pos < nd.kr * nd.kc; ++pos) {
-          const int ch = nd.kids[pos];
-          if (ch < 0) continue;
-          const int r0 = std::max(a.row0, rb(ch)), r1 = std::min(a.row0 + a.p.rows, rb(ch) + nr(ch));
-          const int c0 = std::max(a.col0, cb(ch)), c1 = std::min(a.col0 + a.q.rows, cb(ch) + nc(ch));
-          if (r0 >= r1 || c0 >= c1) continue;
-          sub.push_back(Add{ch, rows_of(a.p, r0 - a.row0, r1 - r0), rows_of(a.q, c0 - a.col0, c1 - c0),
-                            a.alpha, r0, c0});
-        }
-      }
-      add_lr(sub);
-    }
   }
 
   // scaled copies: V (rows) * d over a column cluster
@@ -738,26 +772,35 @@ struct Engine {
             parts.push_back(pt);
           }
       }
-      const int kcmax = 2;
-      for (int kk = 0; kk < kcmax; ++kk) {
-        std::vector<std::pair<int, int>> sub;
-        std::vector<size_t> who;
+      // All child products of every kk in ONE recursive call (they only read A, B);
+      // the accumulation into each part then runs kk = 0, 1 in the reference's
+      // order with the > 48 recompression rule (hfactor.cpp:164-172).
+      std::vector<std::pair<int, int>> sub;
+      std::vector<size_t> who;
+      std::vector<int> whokk;
+      for (int kk = 0; kk < 2; ++kk)
         for (size_t t = 0; t < parts.size(); ++t) {
           const int a = abs[parts[t].item].first, b = abs[parts[t].item].second;
           if (kk >= N(a).kc) continue;
           sub.push_back({kid(a, parts[t].ii, kk), kid(b, parts[t].jj, kk)});
           who.push_back(t);
+          whokk.push_back(kk);
         }
-        if (sub.empty()) continue;
+      if (!sub.empty()) {
         const size_t mk2 = ar.mark();
         std::vector<Pair> tp = product_lr(sub);
-        std::vector<TruncItem> upd;
-        for (size_t s = 0; s < sub.size(); ++s) {
-          Part& pt = parts[who[s]];
-          upd.push_back(lritem(pt.p.p, pt.q.p, pt.p.rows, pt.q.rows, pt.cols, nullptr, 3, TCAP,
-                               &tp[s].p, &tp[s].q, 0, 0, 1.0, TCAP + tp[s].p.cols.v));
+        for (int kk = 0; kk < 2; ++kk) {
+          std::vector<TruncItem> upd;
+          const size_t mk3 = ar.mark();
+          for (size_t s = 0; s < sub.size(); ++s) {
+            if (whokk[s] != kk) continue;
+            Part& pt = parts[who[s]];
+            upd.push_back(lritem(pt.p.p, pt.q.p, pt.p.rows, pt.q.rows, pt.cols, nullptr, 3, TCAP,
+                                 &tp[s].p, &tp[s].q, 0, 0, 1.0, TCAP + tp[s].p.cols.v));
+          }
+          lrupd_ws(upd);
+          ar.release(mk3);
         }
-        lrupd_ws(upd);
         ar.release(mk2);
       }
       // embed parts into out (pure appends; one launch per part index so the
@@ -792,7 +835,59 @@ struct Engine {
 
   // --------------------------------------------------------- sub_product -
   // C -= A diag(d_K) B^T (hfactor.cpp:236-285)
+  // Case 5 of the reference (C, A, B all branches) only recurses over
+  // (kk, ii, jj); flatten it into the ordered list of terminal terms.
+  void collect_terms(const Trip& t, std::vector<Trip>& out) {
+    const int C = t.c, a = t.a, b = t.b;
+    if (kind(a) == BRANCH && kind(b) == BRANCH && kind(C) == BRANCH) {
+      for (int kk = 0; kk < N(a).kc; ++kk)
+        for (int ii = 0; ii < N(a).kr; ++ii)
+          for (int jj = 0; jj < N(b).kr; ++jj) {
+            const int tg = kid(C, ii, jj);
+            if (tg < 0) continue;  // implied upper mirror
+            collect_terms(Trip{tg, kid(a, ii, kk), kid(b, jj, kk)}, out);
+          }
+      return;
+    }
+    out.push_back(t);
+  }
+
+  double term_bytes(const Trip& t) const {
+    const int a = t.a, b = t.b;
+    double d;
+    if (kind(a) == LOWRANK)
+      d = (double)(nr(b) + nc(a)) * LF(a).cap;
+    else if (kind(b) == LOWRANK)
+      d = (double)(nr(a) + nc(b)) * LF(b).cap;
+    else if (kind(a) == DENSE)
+      d = (double)nr(a) * nc(a) + (double)nr(b) * nc(b) + (double)nc(b) * nc(b);
+    else if (kind(b) == DENSE)
+      d = (double)nc(b) * nr(b) + (double)nr(a) * nr(b) + (double)nr(b) * nr(b);
+    else
+      d = 3.0 * (nr(a) + nr(b)) * TCAP;
+    return 8.0 * d;
+  }
+
+  // sub_product for independent targets, two-phase: every product of the
+  // flattened term list is computed in parallel (they only read A, B), then the
+  // adds are applied per target leaf in the reference's order (add_lr rounds).
   void subprod(const std::vector<Trip>& ts) {
+    if (ts.empty()) return;
+    std::vector<Trip> terms;
+    for (const Trip& t : ts) collect_terms(t, terms);
+    const double budget = 6e9;
+    size_t i0 = 0;
+    while (i0 < terms.size()) {
+      size_t i1 = i0;
+      double bytes = 0;
+      while (i1 < terms.size() && (i1 == i0 || (bytes + term_bytes(terms[i1]) < budget && i1 - i0 < 50000)))
+        bytes += term_bytes(terms[i1++]);
+      subprod_terms(std::vector<Trip>(terms.begin() + i0, terms.begin() + i1));
+      i0 = i1;
+    }
+  }
+
+  void subprod_terms(const std::vector<Trip>& ts) {
     if (ts.empty()) return;
     const size_t mk = ar.mark();
     std::vector<Add> adds;
@@ -863,6 +958,7 @@ struct Engine {
     }
     copy(c);
     if (!mb.empty()) multiply_into(mb, mx, my);
+    std::vector<int> leaf_pos(ts.size(), -1);
     if (!leafc.empty()) {
       std::vector<std::pair<int, int>> ab;
       for (const Trip& t : leafc) ab.push_back({t.a, t.b});
@@ -870,23 +966,20 @@ struct Engine {
       for (size_t i = 0; i < leafc.size(); ++i)
         adds.push_back(Add{leafc[i].c, pr[i].p, pr[i].q, -1.0, rb(leafc[i].a), rb(leafc[i].b)});
     }
-    add_lr(adds);
-    ar.release(mk);
-    if (!brc.empty()) {
-      for (int kk = 0; kk < 2; ++kk) {
-        std::vector<Trip> sub;
-        for (const Trip& t : brc) {
-          if (kk >= N(t.a).kc) continue;
-          for (int ii = 0; ii < N(t.a).kr; ++ii)
-            for (int jj = 0; jj < N(t.b).kr; ++jj) {
-              const int tg = kid(t.c, ii, jj);
-              if (tg < 0) continue;
-              sub.push_back(Trip{tg, kid(t.a, ii, kk), kid(t.b, jj, kk)});
-            }
-        }
-        subprod(sub);
+    // restore the reference order of the terms (leafc terms were appended last)
+    std::vector<Add> ordered;
+    ordered.reserve(adds.size());
+    {
+      size_t ia = 0, il = adds.size() - leafc.size();
+      for (const Trip& t : ts) {
+        const bool is_leafc = !(kind(t.a) == LOWRANK || kind(t.b) == LOWRANK || kind(t.a) == DENSE ||
+                                kind(t.b) == DENSE);
+        ordered.push_back(is_leafc ? adds[il++] : adds[ia++]);
       }
     }
+    (void)brc;
+    add_lr(ordered);
+    ar.release(mk);
   }
 
   // --------------------------------------------------------- factor_diag -

@@ -362,3 +362,12 @@ def test_predict_edge_cases(hm, oracle):
     mixed = hm.predict(tr, a * z1 + b * z2, te, th).z2_hat
     combo = a * hm.predict(tr, z1, te, th).z2_hat + b * hm.predict(tr, z2, te, th).z2_hat
     assert np.max(np.abs(mixed - combo)) <= 1e-10
+
+
+def test_kernel_vs_committed_reference_fixture(hm):
+    """Device Matérn vs the reference build's at_distance (tests/golden/kernel_ref.npz)."""
+    import os
+    k = np.load(os.path.join(os.path.dirname(__file__), "golden", "kernel_ref.npz"))
+    for nu, want in zip(k["nu"], k["values"]):
+        got = hm.at_distance([float(k["sigma2"]), float(k["ell"]), float(nu), float(k["tau2"])], k["h"])
+        assert np.max(np.abs(got - want) / np.abs(want)) < 1e-10, nu

@@ -147,3 +147,17 @@ def test_pin_kernel_against_reference_build(oracle):
         assert np.array_equal(a, b), nu  # same compiler, same operations -> bit-identical
     for nu, x, _ in BESSEL_TABLE:
         assert oracle.bessel_k(nu, x) == ref.bessel_k(nu, x)
+
+
+def test_oracle_against_committed_reference_fixtures(oracle):
+    """tests/golden/*.npz were produced by the reference build (make_golden.py)."""
+    import os
+    d = os.path.join(os.path.dirname(__file__), "golden")
+    g = np.load(os.path.join(d, "geometry_c1.npz"))
+    assert np.array_equal(oracle.cluster_perm(g["x"], int(g["leaf"])), g["perm"])
+    b, na, nd = oracle.block_leaves(g["x"], int(g["leaf"]), float(g["eta"]))
+    assert np.array_equal(b, g["blocks"]) and (na, nd) == (int(g["n_adm"]), int(g["n_dense"]))
+    k = np.load(os.path.join(d, "kernel_ref.npz"))
+    for nu, want in zip(k["nu"], k["values"]):
+        got = oracle.at_distance([float(k["sigma2"]), float(k["ell"]), float(nu), float(k["tau2"])], k["h"])
+        assert np.array_equal(got, want)
