@@ -107,8 +107,9 @@ struct AcaItem {
   double* U;  // m x cap
   double* V;  // n x cap
   int r0, c0, m, n;
-  int cap;    // max_terms = min(m, n, max_rank[, k])
-  int* rank;  // out
+  int cap;        // column capacity of U, V in this pass
+  int max_terms;  // min(m, n, max_rank[, k])  (hmatrix.cpp:15-16)
+  int* rank;      // out; -1 = capacity reached before the stopping rule (redo)
   unsigned* flags;  // (m + n) bits: used rows then used cols, zero-initialised
 };
 
@@ -127,12 +128,16 @@ __global__ void __launch_bounds__(kAcaThreads) k_aca(const AcaItem* __restrict__
   __shared__ double s_du[256], s_dv[256];
   __shared__ int s_next, s_fresh;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int max_terms = it.cap;
+  const int max_terms = it.max_terms;
   double fro2 = 0.0, scale0 = 0.0, ne = 0.0;
   int ip = 0, k = 0;
   if (threadIdx.x == 0) s_fresh = 1;
   __syncthreads();
   while (k < max_terms) {
+    if (k >= it.cap) {  // pass capacity reached before the stopping rule: redo later
+      if (threadIdx.x == 0) *it.rank = -1;
+      return;
+    }
     // residual row r_j = A(ip, j) - sum_l U(ip,l) V(j,l)  -> stored in V(:, k)
     for (int l = threadIdx.x; l < k; l += blockDim.x) s_coef[l] = it.U[(size_t)l * m + ip];
     __syncthreads();
@@ -374,34 +379,35 @@ void assemble(HMat& h, Geometry& g, const MaternDev& p, double eps, bool fixed_r
   int* d_rank_tmp = dmalloc<int>(L);
   int* d_err = dmalloc<int>(1);
   HMGP_CUDA(cudaMemsetAsync(d_err, 0, 4, st));
-  // staging of ACA results: per chunk
-  struct Staged {
-    int leaf;
-    size_t offU, offV;
-  };
-  std::vector<std::vector<double>> keepU(L), keepV(L);  // not used (kept device-side)
-  (void)keepU;
-  (void)keepV;
   // Device staging buffers per chunk; results copied into the final pool after
   // the ranks are known.  We keep all chunk buffers alive until the pool copy.
+  // Pass 1 gives every block a 64-column ACA capacity; a block that reaches it
+  // without meeting the stopping rule is recomputed from scratch in pass 2 with
+  // the full max_terms (ACA is deterministic, so the result is the same as a
+  // single run with full capacity).
   struct Chunk {
     std::vector<int> leaves;
+    std::vector<char> valid;
     double* buf = nullptr;
     std::vector<size_t> offU, offV;
     std::vector<int> cap;
     double* ws = nullptr;
   };
   std::vector<Chunk> chunks;
-  const size_t kChunkDoubles = (size_t)1 << 28;  // 2 GiB of U/V staging per chunk
-  {
+  const size_t kChunkDoubles = (size_t)1 << 30;  // 8 GiB of U/V staging per chunk
+  auto max_terms_of = [&](int k) {
+    int mt = std::min({mm[k], nn[k], max_rank});
+    if (fixed_rank) mt = std::min(mt, rank_k);
+    return mt;
+  };
+  auto run_pass = [&](const std::vector<int>& list, int capmax) {
     size_t i = 0;
-    while (i < adm.size()) {
+    while (i < list.size()) {
       Chunk c;
       size_t tot = 0;
-      while (i < adm.size()) {
-        const int k = adm[i];
-        int cap = std::min({mm[k], nn[k], max_rank});
-        if (fixed_rank) cap = std::min(cap, rank_k);
+      while (i < list.size()) {
+        const int k = list[i];
+        const int cap = std::min(max_terms_of(k), capmax);
         const size_t need = (size_t)(mm[k] + nn[k]) * cap;
         if (!c.leaves.empty() && tot + need > kChunkDoubles) break;
         c.leaves.push_back(k);
@@ -425,7 +431,7 @@ void assemble(HMat& h, Geometry& g, const MaternDev& p, double eps, bool fixed_r
       for (size_t t = 0; t < c.leaves.size(); ++t) {
         const int k = c.leaves[t];
         items.push_back(AcaItem{c.buf + c.offU[t], c.buf + c.offV[t], r0v[k], c0v[k], mm[k], nn[k],
-                                c.cap[t], d_rank_tmp + k, d_flags + foff[t]});
+                                c.cap[t], max_terms_of(k), d_rank_tmp + k, d_flags + foff[t]});
       }
       AcaItem* d_items = upload(items, st);
       k_aca<<<(int)items.size(), kAcaThreads, 0, st>>>(d_items, p, g.d_xt, g.n, g.dim, eps,
@@ -471,8 +477,24 @@ void assemble(HMat& h, Geometry& g, const MaternDev& p, double eps, bool fixed_r
       HMGP_CUDA(cudaStreamSynchronize(st));
       cudaFree(d_items);
       cudaFree(d_flags);
+      c.valid.assign(c.leaves.size(), 1);
       chunks.push_back(std::move(c));
     }
+  };
+  run_pass(adm, 64);
+  {
+    HMGP_CUDA(cudaMemcpyAsync(rank.data(), d_rank_tmp, (size_t)L * 4, cudaMemcpyDeviceToHost, st));
+    HMGP_CUDA(cudaStreamSynchronize(st));
+    std::vector<int> redo;
+    for (Chunk& c : chunks)
+      for (size_t t = 0; t < c.leaves.size(); ++t)
+        if (rank[c.leaves[t]] < 0) {
+          c.valid[t] = 0;
+          redo.push_back(c.leaves[t]);
+        }
+    if (!redo.empty()) run_pass(redo, 1 << 30);
+  }
+  {
   }
   phase_mark(PH_ACA);
   HMGP_CUDA(cudaMemcpyAsync(rank.data(), d_rank_tmp, (size_t)L * 4, cudaMemcpyDeviceToHost, st));
@@ -555,6 +577,7 @@ void assemble(HMat& h, Geometry& g, const MaternDev& p, double eps, bool fixed_r
     std::vector<CopyItem> cp;
     std::vector<OuterItem> oi;
     for (size_t t = 0; t < c.leaves.size(); ++t) {
+      if (!c.valid[t]) continue;  // superseded by the full-capacity pass
       const int k = c.leaves[t];
       const double* U = c.buf + c.offU[t];
       const double* V = c.buf + c.offV[t];

@@ -160,12 +160,21 @@ struct Engine {
     return m;
   }
 
+  // --- launch statistics (HMGP_STATS=1 prints them after the factorization)
+  enum { S_GEMM, S_COPY, S_TRUNC, S_TRSML, S_TRSMR, S_LEAF, S_N };
+  long long st_launch[S_N] = {}, st_items[S_N] = {};
+  void stat(int k, size_t items) {
+    ++st_launch[k];
+    st_items[k] += (long long)items;
+  }
+
   // --- batched primitive launchers
   void gemm(std::vector<GemmItem>& v) {
     if (v.empty()) return;
     int tiles = 1;
     for (auto& g : v) tiles = std::max(tiles, ((g.M.v + 63) / 64) * ((g.N.v + 63) / 64));
     launch_gemm(sg.put(v), (int)v.size(), tiles, st);
+    stat(S_GEMM, v.size());
     v.clear();
   }
   void copy(std::vector<CopyScaleItem>& v) {
@@ -173,6 +182,7 @@ struct Engine {
     int mx = 1;
     for (auto& c : v) mx = std::max<long long>(mx, std::min<long long>((long long)c.rows * c.cols.v, 1 << 24));
     launch_copy_scale(sg.put(v), (int)v.size(), mx, st);
+    stat(S_COPY, v.size());
     v.clear();
   }
   void lrupd(std::vector<TruncItem>& v) {
@@ -181,7 +191,14 @@ struct Engine {
     for (const TruncItem& t : v)
       if (t.cond != 4) trunc_smem_dims(t.m, t.n, &sw, &smn);
     launch_truncate(sg.put(v), (int)v.size(), eps, d_err, st, sw, smn);
+    stat(S_TRUNC, v.size());
     v.clear();
+  }
+  void print_stats() const {
+    static const char* nm[S_N] = {"gemm", "copy", "lrupd", "trsm_left", "trsm_right", "leaf"};
+    for (int k = 0; k < S_N; ++k)
+      fprintf(stderr, "[hmgp] %-10s launches %9lld items %10lld (%.1f/launch)\n", nm[k], st_launch[k],
+              st_items[k], st_launch[k] ? (double)st_items[k] / st_launch[k] : 0.0);
   }
   CopyScaleItem cpy(const double* src, int lds, MV dst, Dim cols, int trans, double alpha,
                     const double* d, int mode) {
@@ -398,6 +415,7 @@ struct Engine {
         mc = std::max(mc, m.cols.v);
       }
       launch_trsm_left(sg.put(v), (int)v.size(), mc, st);
+      stat(S_TRSML, v.size());
       return;
     }
     const int l00 = kid(l, 0, 0), l10 = kid(l, 1, 0), l11 = kid(l, 1, 1);
@@ -426,7 +444,8 @@ struct Engine {
         v.push_back(TrsmRItem{L.a, L.m, L.m, x.p, x.ld, x.rows});
         mr = std::max(mr, x.rows);
       }
-      launch_trsm_right(sg.put(v), (int)v.size(), mr, st);
+      launch_trsm_right(sg.put(v), (int)v.size(), mr, st, L.m);
+      stat(S_TRSMR, v.size());
       if (ldl) {
         std::vector<CopyScaleItem> c;
         for (const MV& x : xs) c.push_back(cpy(x.p, x.ld, x, dimv(L.m), 0, 1.0, dseg(rb(l)), 4));
@@ -484,6 +503,7 @@ struct Engine {
           if (ldl) c.push_back(cpy(V.p, V.ld, V, V.cols, 0, 1.0, dseg(rb(l)), 2));
         }
         launch_trsm_left(sg.put(v), (int)v.size(), mc, st);
+      stat(S_TRSML, v.size());
         copy(c);
       }
       if (!dn.empty()) {
@@ -987,6 +1007,7 @@ struct Engine {
     if (kind(a) == DENSE) {
       const LeafDev& l = LF(a);
       launch_leaf_factor(l.a, l.m, rb(a), ldl ? 1 : 0, F.d_d, F.clamp_tol, F.d_status, st);
+      stat(S_LEAF, 1);
       return;
     }
     factor_diag(kid(a, 0, 0));
@@ -997,6 +1018,40 @@ struct Engine {
 };
 
 // ------------------------------------------------------ solve schedules ---
+// Diagonal-leaf triangular solve: the CTA stages L (b x b) and x in shared
+// memory with coalesced loads, then one warp runs the substitution on-chip.
+__global__ void k_trsv_leaf_smem(const double* __restrict__ Lg, int b, double* __restrict__ xg,
+                                 int trans) {
+  extern __shared__ double sm[];
+  double* L = sm;
+  double* x = sm + (size_t)b * b;
+  for (int e = threadIdx.x; e < b * b; e += blockDim.x) L[e] = Lg[e];
+  for (int e = threadIdx.x; e < b; e += blockDim.x) x[e] = xg[e];
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    if (!trans) {
+      for (int j = 0; j < b; ++j) {
+        const double xj = x[j] / L[(size_t)j * b + j];
+        __syncwarp();
+        if (lane == 0) x[j] = xj;
+        for (int i = j + 1 + lane; i < b; i += 32) x[i] -= L[(size_t)j * b + i] * xj;
+        __syncwarp();
+      }
+    } else {
+      for (int j = b - 1; j >= 0; --j) {
+        double s = 0.0;
+        for (int i = j + 1 + lane; i < b; i += 32) s += L[(size_t)j * b + i] * x[i];
+        s = warp_sum(s);
+        if (lane == 0) x[j] = (x[j] - s) / L[(size_t)j * b + j];
+        __syncwarp();
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < b; e += blockDim.x) xg[e] = x[e];
+}
+
 __global__ void k_trsv_leaf(const double* __restrict__ L, int b, double* __restrict__ x, int trans) {
   // one warp; x has b entries (tree-order segment)
   const int lane = threadIdx.x;
@@ -1017,6 +1072,22 @@ __global__ void k_trsv_leaf(const double* __restrict__ L, int b, double* __restr
       __syncwarp();
     }
   }
+}
+
+static void launch_trsv(const double* L, int b, double* x, int trans, cudaStream_t st) {
+  const size_t bytes = ((size_t)b * b + b) * 8;
+  if (bytes <= 200 * 1024) {
+    static bool configured = false;
+    if (!configured) {
+      HMGP_CUDA(cudaFuncSetAttribute(k_trsv_leaf_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     200 * 1024));
+      configured = true;
+    }
+    k_trsv_leaf_smem<<<1, 256, bytes, st>>>(L, b, x, trans);
+  } else {
+    k_trsv_leaf<<<1, 32, 0, st>>>(L, b, x, trans);
+  }
+  HMGP_LAUNCH_CHECK();
 }
 
 struct SolveBlk {
@@ -1174,6 +1245,7 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
       for (int k = 0; k < L; ++k)
         if (F.leaf[k].kind == LOWRANK) lr.push_back(F.leaf_node[k]);
       E.compress(lr);
+      if (getenv("HMGP_STATS")) E.print_stats();
       phase_mark(PH_FACTOR);
       HMGP_CUDA(cudaMemcpyAsync(&err, E.d_err, 4, cudaMemcpyDeviceToHost, st));
       HMGP_CUDA(cudaStreamSynchronize(st));
@@ -1263,7 +1335,7 @@ void forward_solve(const Factor& F, double* v, cudaStream_t st) {
   const int nd = (int)F.diag_leaf.size();
   for (int t = 0; t < nd; ++t) {
     const LeafDev& l = F.leaf[F.diag_leaf[t]];
-    k_trsv_leaf<<<1, 32, 0, st>>>(l.a, l.m, v + F.diag_base[t], 0);
+    launch_trsv(l.a, l.m, v + F.diag_base[t], 0, st);
     HMGP_LAUNCH_CHECK();
     const int cnt = F.fwd_off[t + 1] - F.fwd_off[t];
     if (cnt > 0) {
@@ -1278,7 +1350,7 @@ void backward_solve(const Factor& F, double* v, cudaStream_t st) {
   const int nd = (int)F.diag_leaf.size();
   for (int t = nd - 1; t >= 0; --t) {
     const LeafDev& l = F.leaf[F.diag_leaf[t]];
-    k_trsv_leaf<<<1, 32, 0, st>>>(l.a, l.m, v + F.diag_base[t], 1);
+    launch_trsv(l.a, l.m, v + F.diag_base[t], 1, st);
     HMGP_LAUNCH_CHECK();
     const int cnt = F.bwd_off[t + 1] - F.bwd_off[t];
     if (cnt > 0) {

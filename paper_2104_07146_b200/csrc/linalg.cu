@@ -168,10 +168,59 @@ __global__ void k_trsm_right(const TrsmRItem* __restrict__ items) {
   }
 }
 
-void launch_trsm_right(const TrsmRItem* d_items, int count, int max_rows, cudaStream_t st) {
+// Shared-memory variant: L (t x t) and a 64-row tile of X staged on chip; the
+// substitution runs column by column with all threads on the tile.
+constexpr int kTrsmRTile = 64;
+__global__ void __launch_bounds__(256) k_trsm_right_smem(const TrsmRItem* __restrict__ items) {
+  const TrsmRItem it = items[blockIdx.x];
+  extern __shared__ double sm[];
+  const int t = it.t;
+  double* L = sm;
+  double* X = sm + (size_t)t * t;  // kTrsmRTile x t, ld kTrsmRTile
+  for (int e = threadIdx.x; e < t * t; e += blockDim.x) L[e] = it.L[(size_t)(e / t) * it.ldl + e % t];
+  for (int r0 = blockIdx.y * kTrsmRTile; r0 < it.s; r0 += gridDim.y * kTrsmRTile) {
+    const int rows = min(kTrsmRTile, it.s - r0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kTrsmRTile * t; e += blockDim.x) {
+      const int r = e % kTrsmRTile, c = e / kTrsmRTile;
+      X[e] = r < rows ? it.X[(size_t)c * it.ldx + r0 + r] : 0.0;
+    }
+    __syncthreads();
+    for (int j = 0; j < t; ++j) {
+      if (threadIdx.x < kTrsmRTile) X[(size_t)j * kTrsmRTile + threadIdx.x] /= L[(size_t)j * t + j];
+      __syncthreads();
+      const int w = t - j - 1;
+      for (int e = threadIdx.x; e < kTrsmRTile * w; e += blockDim.x) {
+        const int r = e % kTrsmRTile, c = j + 1 + e / kTrsmRTile;
+        X[(size_t)c * kTrsmRTile + r] -= X[(size_t)j * kTrsmRTile + r] * L[(size_t)j * t + c];
+      }
+      __syncthreads();
+    }
+    for (int e = threadIdx.x; e < kTrsmRTile * t; e += blockDim.x) {
+      const int r = e % kTrsmRTile, c = e / kTrsmRTile;
+      if (r < rows) it.X[(size_t)c * it.ldx + r0 + r] = X[e];
+    }
+  }
+  if (blockIdx.y == 0 && threadIdx.x == 0) atomicAdd(&d_cnt_trsm, (double)t * t * it.s);
+}
+
+void launch_trsm_right(const TrsmRItem* d_items, int count, int max_rows, cudaStream_t st,
+                       int max_t) {
   if (count <= 0) return;
-  const int gy = max(1, min((max_rows + 127) / 128, 64));
-  k_trsm_right<<<dim3(count, gy), 128, 0, st>>>(d_items);
+  const size_t bytes = ((size_t)max_t * max_t + (size_t)kTrsmRTile * max_t) * 8;
+  if (bytes <= 200 * 1024) {
+    static bool configured = false;
+    if (!configured) {
+      HMGP_CUDA(cudaFuncSetAttribute(k_trsm_right_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     200 * 1024));
+      configured = true;
+    }
+    const int gy = max(1, min((max_rows + kTrsmRTile - 1) / kTrsmRTile, 32));
+    k_trsm_right_smem<<<dim3(count, gy), 256, bytes, st>>>(d_items);
+  } else {
+    const int gy = max(1, min((max_rows + 127) / 128, 64));
+    k_trsm_right<<<dim3(count, gy), 128, 0, st>>>(d_items);
+  }
   HMGP_LAUNCH_CHECK();
 }
 
@@ -289,15 +338,13 @@ __global__ void k_leaf_factor(double* __restrict__ Dg, int b, int base, int ldl,
   if (use_smem)
     for (int e = threadIdx.x; e < b * b; e += blockDim.x) A[e] = Dg[e];
   __syncthreads();
+  // Right-looking: the trailing lower triangle already holds every update of
+  // the previous columns, so the pivot is A(j,j) (same value as the reference's
+  // left-looking s = m(j,j) - sum_k m(j,k)^2 d_k, different summation order).
+  (void)red;
   for (int j = 0; j < b; ++j) {
-    double part = 0.0;
-    for (int k = threadIdx.x; k < j; k += blockDim.x) {
-      const double l = A[(size_t)k * b + j];
-      part += ldl ? l * l * d[base + k] : l * l;
-    }
-    const double sum = block_sum(part, red);
     if (threadIdx.x == 0) {
-      double s = A[(size_t)j * b + j] - sum;
+      double s = A[(size_t)j * b + j];
       atomic_min_double(&st->min_pivot, s);
       bool failed;
       if (ldl) {
@@ -326,13 +373,13 @@ __global__ void k_leaf_factor(double* __restrict__ Dg, int b, int base, int ldl,
       if (ldl) d[base + j] = s;
       A[(size_t)j * b + j] = ldl ? 1.0 : piv;
     }
-    for (int i = j + 1 + threadIdx.x; i < b; i += blockDim.x) {
-      double v = A[(size_t)j * b + i];
-      for (int k = 0; k < j; ++k) {
-        const double t = A[(size_t)k * b + i] * A[(size_t)k * b + j];
-        v -= ldl ? t * d[base + k] : t;
-      }
-      A[(size_t)j * b + i] = v / piv;
+    for (int i = j + 1 + threadIdx.x; i < b; i += blockDim.x) A[(size_t)j * b + i] /= piv;
+    __syncthreads();
+    const int t = b - j - 1;
+    const double w = ldl ? s : 1.0;
+    for (int e = threadIdx.x; e < t * t; e += blockDim.x) {
+      const int i = j + 1 + e % t, k = j + 1 + e / t;
+      if (i >= k) A[(size_t)k * b + i] -= A[(size_t)j * b + i] * A[(size_t)j * b + k] * w;
     }
     __syncthreads();
   }

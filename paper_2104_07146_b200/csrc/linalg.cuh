@@ -91,7 +91,8 @@ struct LeafFactorStatus {
 
 void launch_gemm(const GemmItem* d_items, int count, int max_tiles, cudaStream_t st);
 void launch_trsm_left(const TrsmLItem* d_items, int count, int max_cols, cudaStream_t st);
-void launch_trsm_right(const TrsmRItem* d_items, int count, int max_rows, cudaStream_t st);
+void launch_trsm_right(const TrsmRItem* d_items, int count, int max_rows, cudaStream_t st,
+                       int max_t);
 void launch_copy_scale(const CopyScaleItem* d_items, int count, int max_elems, cudaStream_t st);
 void launch_append(const AppendItem* d_items, int count, int max_elems, int* d_err, cudaStream_t st);
 // one diagonal leaf (b x b at D, ld b), tree rows [base, base+b); LDL writes d[base..]

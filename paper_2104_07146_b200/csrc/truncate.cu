@@ -18,7 +18,7 @@
 
 namespace hmgp_gpu {
 
-constexpr int kTruncThreads = 256;
+constexpr int kTruncThreads = 512;
 constexpr int kMaxTruncCols = 1024;
 constexpr int kChunk = 8;              // factor columns staged per pass when forming W
 constexpr int kMaxSmemW = 16384;       // W = [U|aP][V|Q]^T in shared memory (128 KB)
@@ -246,6 +246,7 @@ __device__ RS cta_rrqr_svd(double* W, int p, int q, double eps, double* tau, int
   }
   const int kmax = min(p, q);
   int k = 0;
+  __shared__ double s_part[32];
   for (; k < kmax; ++k) {
     double part = 0.0, a = -1.0;
     int ia = -1;
@@ -256,10 +257,16 @@ __device__ RS cta_rrqr_svd(double* W, int p, int q, double eps, double* tau, int
         ia = j;
       }
     }
-    const double resid = block_sum(part, red);
+    // one fused reduction: trailing Frobenius norm^2 and the pivot column
+    part = warp_sum(part);
+    if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = part;
     double best;
-    const int jm = block_argmax(a, ia, redv, redi, &best);
-    if (threadIdx.x == 0) s_stop = !(sqrt(resid) > s_thresh) || jm < 0;
+    const int jm = block_argmax(a, ia, redv, redi, &best);  // contains the barrier
+    if (threadIdx.x == 0) {
+      double resid = 0.0;
+      for (int q2 = 0; q2 < nw; ++q2) resid += s_part[q2];
+      s_stop = !(sqrt(resid) > s_thresh) || jm < 0;
+    }
     __syncthreads();
     if (s_stop) break;
     if (jm != k) {  // swap columns k <-> jm
@@ -309,19 +316,23 @@ __device__ RS cta_rrqr_svd(double* W, int p, int q, double eps, double* tau, int
     __syncthreads();
     for (int j = k + 1 + w; j < q; j += nw) {  // apply H_k, refresh the trailing norms
       double* cj = W + (size_t)j * p;
+      double s = 0.0;
       if (t != 0.0) {
-        double s = 0.0;
         for (int i = k + 1 + lane; i < p; i += 32) s += col[i] * cj[i];
         s = warp_sum(s);
         s = (s + cj[k]) * t;
-        for (int i = k + 1 + lane; i < p; i += 32) cj[i] -= s * col[i];
-        __syncwarp();
-        if (lane == 0) cj[k] -= s;
       }
       double s2 = 0.0;
-      for (int i = k + 1 + lane; i < p; i += 32) s2 += cj[i] * cj[i];
+      for (int i = k + 1 + lane; i < p; i += 32) {
+        const double v = cj[i] - s * col[i];
+        cj[i] = v;
+        s2 += v * v;
+      }
       s2 = warp_sum(s2);
-      if (lane == 0) cn[j] = s2;
+      if (lane == 0) {
+        cj[k] -= s;
+        cn[j] = s2;
+      }
     }
     __syncthreads();
     flops += 6.0 * (p - k) * (q - k);
