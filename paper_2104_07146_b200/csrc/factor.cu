@@ -163,9 +163,26 @@ struct Engine {
   // --- launch statistics (HMGP_STATS=1 prints them after the factorization)
   enum { S_GEMM, S_COPY, S_TRUNC, S_TRSML, S_TRSMR, S_LEAF, S_N };
   long long st_launch[S_N] = {}, st_items[S_N] = {};
+  // (stats mode) device time per primitive: an event after every launch, the
+  // gap to the previous event is charged to the primitive just launched.
+  bool stats_on = getenv("HMGP_STATS") != nullptr;
+  std::vector<std::pair<int, cudaEvent_t>> st_ev;
+  cudaEvent_t st_prev = nullptr;
   void stat(int k, size_t items) {
     ++st_launch[k];
     st_items[k] += (long long)items;
+    if (stats_on) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      cudaEventRecord(e, st);
+      st_ev.push_back({k, e});
+    }
+  }
+  void stats_begin() {
+    if (stats_on) {
+      cudaEventCreate(&st_prev);
+      cudaEventRecord(st_prev, st);
+    }
   }
 
   // --- batched primitive launchers
@@ -196,9 +213,19 @@ struct Engine {
   }
   void print_stats() const {
     static const char* nm[S_N] = {"gemm", "copy", "lrupd", "trsm_left", "trsm_right", "leaf"};
+    double ms[S_N] = {};
+    cudaStreamSynchronize(st);
+    cudaEvent_t prev = st_prev;
+    for (const auto& pe : st_ev) {
+      float t = 0.f;
+      if (prev) cudaEventElapsedTime(&t, prev, pe.second);
+      ms[pe.first] += t;
+      prev = pe.second;
+    }
     for (int k = 0; k < S_N; ++k)
-      fprintf(stderr, "[hmgp] %-10s launches %9lld items %10lld (%.1f/launch)\n", nm[k], st_launch[k],
-              st_items[k], st_launch[k] ? (double)st_items[k] / st_launch[k] : 0.0);
+      fprintf(stderr, "[hmgp] %-10s launches %9lld items %10lld (%.1f/launch) %10.1f ms\n", nm[k],
+              st_launch[k], st_items[k], st_launch[k] ? (double)st_items[k] / st_launch[k] : 0.0,
+              ms[k]);
   }
   CopyScaleItem cpy(const double* src, int lds, MV dst, Dim cols, int trans, double alpha,
                     const double* d, int mode) {
@@ -596,14 +623,60 @@ struct Engine {
       }
       seq[s].push_back(i);
     }
-    size_t rounds = 0;
-    for (const auto& v : seq) rounds = std::max(rounds, v.size());
-    for (size_t r = 0; r < rounds; ++r) {
-      std::vector<Add> batch;
-      for (const auto& v : seq)
-        if (r < v.size()) batch.push_back(flat[v[r]]);
-      add_leaves(batch);
+    // two launches in total: one CTA per dense target runs its GEMM updates in
+    // order, one CTA per low-rank target runs its append / watermark
+    // recompressions in order (same decisions as the reference, hblock.cpp:200)
+    const size_t mk = ar.mark();
+    std::vector<GemmItem> g;
+    std::vector<int> goff{0};
+    std::vector<TruncItem> t;
+    std::vector<int> toff{0};
+    int sw = 0, smn = 0;
+    for (const auto& v : seq) {
+      const int c = flat[v[0]].c;
+      const LeafDev& l = LF(c);
+      if (kind(c) == DENSE) {  // hblock.cpp:181-184
+        for (int i : v) {
+          const Add& a = flat[i];
+          GemmItem gi{};
+          gi.A = a.p.p;
+          gi.lda = a.p.ld;
+          gi.B = a.q.p;
+          gi.ldb = a.q.ld;
+          gi.tb = 1;
+          gi.C = l.a + (size_t)(a.col0 - cb(c)) * l.m + (a.row0 - rb(c));
+          gi.ldc = l.m;
+          gi.M = dimv(a.p.rows);
+          gi.N = dimv(a.q.rows);
+          gi.K = a.p.cols;
+          gi.alpha = a.alpha;
+          g.push_back(gi);
+        }
+        goff.push_back((int)g.size());
+      } else {  // hblock.cpp:185-203
+        int rcap = 0;
+        for (int i : v) rcap = std::max(rcap, l.cap + flat[i].p.cols.v);
+        double* ws = ar.dbl(trunc_ws_doubles(l.m, l.n, rcap));
+        for (int i : v) {
+          const Add& a = flat[i];
+          TruncItem ti = lritem(l.a, l.b, l.m, l.n, rankp(c), compp(c), 2, l.cap, &a.p, &a.q,
+                                a.row0 - rb(c), a.col0 - cb(c), a.alpha, l.cap + a.p.cols.v);
+          ti.ws = ws;
+          t.push_back(ti);
+        }
+        toff.push_back((int)t.size());
+        trunc_smem_dims(l.m, l.n, &sw, &smn);
+      }
     }
+    if (!g.empty()) {
+      launch_gemm_seq(sg.put(g), sg.put(goff), (int)goff.size() - 1, st);
+      stat(S_GEMM, g.size());
+    }
+    if (!t.empty()) {
+      launch_truncate_seq(sg.put(t), sg.put(toff), (int)toff.size() - 1, eps, d_err, st, sw, smn);
+      stat(S_TRUNC, t.size());
+    }
+    ar.release(mk);
   }
 
   // distinct leaf targets, one add each
@@ -1239,6 +1312,7 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
     int err = 0;
     {
       Engine E(F, st, arena_bytes, tcap);
+      E.stats_begin();
       E.factor_diag(0);
       // compress_all (hfactor.cpp:321-328): every LR leaf, independent
       std::vector<int> lr;

@@ -27,16 +27,36 @@ void linalg_counters_read_reset(double* g, double* t, double* l) {
 // 256 threads x (4 x 4) register micro-tile.  Dimensions may live on device.
 constexpr int GT = 64, GK = 16;
 
+__device__ void gemm_item(const GemmItem& it, int tile0, int tstride, bool count);
+
 __global__ void __launch_bounds__(256) k_gemm(const GemmItem* __restrict__ items) {
-  const GemmItem it = items[blockIdx.x];
+  gemm_item(items[blockIdx.x], blockIdx.y, gridDim.y, blockIdx.y == 0);
+}
+
+// One CTA per target: its GEMM updates items[off[b] .. off[b+1]) in order.
+__global__ void __launch_bounds__(256) k_gemm_seq(const GemmItem* __restrict__ items,
+                                                  const int* __restrict__ off) {
+  for (int i = off[blockIdx.x]; i < off[blockIdx.x + 1]; ++i) {
+    gemm_item(items[i], 0, 1, true);
+    __syncthreads();
+  }
+}
+
+void launch_gemm_seq(const GemmItem* d_items, const int* d_off, int targets, cudaStream_t st) {
+  if (targets <= 0) return;
+  k_gemm_seq<<<targets, 256, 0, st>>>(d_items, d_off);
+  HMGP_LAUNCH_CHECK();
+}
+
+__device__ void gemm_item(const GemmItem& it, int tile0, int tstride, bool count) {
   const int M = it.M.get(), N = it.N.get(), K = it.K.get();
   if (M <= 0 || N <= 0) return;
-  if (blockIdx.y == 0 && threadIdx.x == 0) atomicAdd(&d_cnt_gemm, 2.0 * M * N * K);
+  if (count && threadIdx.x == 0) atomicAdd(&d_cnt_gemm, 2.0 * M * N * K);
   const int tm = (M + GT - 1) / GT, tn = (N + GT - 1) / GT;
   __shared__ double sA[GK][GT + 1];
   __shared__ double sB[GK][GT + 1];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  for (int tile = blockIdx.y; tile < tm * tn; tile += gridDim.y) {
+  for (int tile = tile0; tile < tm * tn; tile += tstride) {
     const int i0 = (tile % tm) * GT, j0 = (tile / tm) * GT;
     double acc[4][4];
 #pragma unroll

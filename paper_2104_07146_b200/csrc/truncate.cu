@@ -370,10 +370,27 @@ __device__ RS cta_rrqr_svd(double* W, int p, int q, double eps, double* tau, int
   return RS{kq, s_keep, flops};
 }
 
+__device__ void lr_update(const TruncItem& it, double eps, int* err, int smem_w, int smem_mn);
+
 __global__ void __launch_bounds__(kTruncThreads) k_truncate(const TruncItem* __restrict__ items,
                                                             double eps, int* err, int smem_w,
                                                             int smem_mn) {
-  const TruncItem it = items[blockIdx.x];
+  lr_update(items[blockIdx.x], eps, err, smem_w, smem_mn);
+}
+
+// One CTA per target: its updates items[off[b] .. off[b+1]) run in order (the
+// reference's per-target sequence and watermark decisions), all targets at once.
+__global__ void __launch_bounds__(kTruncThreads) k_truncate_seq(const TruncItem* __restrict__ items,
+                                                                const int* __restrict__ off,
+                                                                double eps, int* err, int smem_w,
+                                                                int smem_mn) {
+  for (int i = off[blockIdx.x]; i < off[blockIdx.x + 1]; ++i) {
+    lr_update(items[i], eps, err, smem_w, smem_mn);
+    __syncthreads();
+  }
+}
+
+__device__ void lr_update(const TruncItem& it, double eps, int* err, int smem_w, int smem_mn) {
   __shared__ double red[32];
   __shared__ double s_sig[kMaxTruncCols];
   __shared__ int s_ord[kMaxTruncCols];
@@ -579,13 +596,33 @@ void launch_truncate(const TruncItem* d_items, int count, double eps, int* d_err
     smem_mn = 0;
   }
   const size_t bytes = ((size_t)smem_w + (size_t)kChunk * smem_mn) * 8;
-  static size_t configured = 0;
-  if (bytes > 48 * 1024 && bytes > configured) {
-    HMGP_CUDA(cudaFuncSetAttribute(k_truncate, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)((kMaxSmemW + (size_t)kChunk * kMaxSmemMN) * 8)));
-    configured = (kMaxSmemW + (size_t)kChunk * kMaxSmemMN) * 8;
+  static bool configured = false;
+  if (!configured) {
+    const int mx = (int)((kMaxSmemW + (size_t)kChunk * kMaxSmemMN) * 8);
+    HMGP_CUDA(cudaFuncSetAttribute(k_truncate, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    HMGP_CUDA(cudaFuncSetAttribute(k_truncate_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    configured = true;
   }
   k_truncate<<<count, kTruncThreads, bytes, st>>>(d_items, eps, d_err, smem_w, smem_mn);
+  HMGP_LAUNCH_CHECK();
+}
+
+void launch_truncate_seq(const TruncItem* d_items, const int* d_off, int targets, double eps,
+                         int* d_err, cudaStream_t st, int smem_w, int smem_mn) {
+  if (targets <= 0) return;
+  if (smem_w > kMaxSmemW || smem_mn > kMaxSmemMN) {
+    smem_w = 0;
+    smem_mn = 0;
+  }
+  const size_t bytes = ((size_t)smem_w + (size_t)kChunk * smem_mn) * 8;
+  static bool configured = false;
+  if (!configured) {
+    const int mx = (int)((kMaxSmemW + (size_t)kChunk * kMaxSmemMN) * 8);
+    HMGP_CUDA(cudaFuncSetAttribute(k_truncate, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    HMGP_CUDA(cudaFuncSetAttribute(k_truncate_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    configured = true;
+  }
+  k_truncate_seq<<<targets, kTruncThreads, bytes, st>>>(d_items, d_off, eps, d_err, smem_w, smem_mn);
   HMGP_LAUNCH_CHECK();
 }
 
