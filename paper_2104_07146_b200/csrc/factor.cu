@@ -17,6 +17,8 @@
 #include <climits>
 #include <cmath>
 #include <cstring>
+#include <array>
+#include <map>
 #include <vector>
 
 #include "common.cuh"
@@ -168,6 +170,8 @@ struct Engine {
   bool stats_on = getenv("HMGP_STATS") != nullptr;
   std::vector<std::pair<int, cudaEvent_t>> st_ev;
   cudaEvent_t st_prev = nullptr;
+  std::vector<std::array<int, 4>> st_meta;  // per event: max m, max n, items, max seq length
+  std::array<int, 4> st_next{};
   void stat(int k, size_t items) {
     ++st_launch[k];
     st_items[k] += (long long)items;
@@ -176,6 +180,8 @@ struct Engine {
       cudaEventCreate(&e);
       cudaEventRecord(e, st);
       st_ev.push_back({k, e});
+      st_meta.push_back(st_next);
+      st_next = {};
     }
   }
   void stats_begin() {
@@ -202,11 +208,19 @@ struct Engine {
     stat(S_COPY, v.size());
     v.clear();
   }
+  void note_dims(int m, int n, int items, int seq) {
+    st_next[0] = std::max(st_next[0], m);
+    st_next[1] = std::max(st_next[1], n);
+    st_next[2] = items;
+    st_next[3] = std::max(st_next[3], seq);
+  }
   void lrupd(std::vector<TruncItem>& v) {
     if (v.empty()) return;
     int sw = 0, smn = 0;
-    for (const TruncItem& t : v)
+    for (const TruncItem& t : v) {
       if (t.cond != 4) trunc_smem_dims(t.m, t.n, &sw, &smn);
+      if (stats_on) note_dims(t.m, t.n, (int)v.size(), 1);
+    }
     launch_truncate(sg.put(v), (int)v.size(), eps, d_err, st, sw, smn);
     stat(S_TRUNC, v.size());
     v.clear();
@@ -216,12 +230,33 @@ struct Engine {
     double ms[S_N] = {};
     cudaStreamSynchronize(st);
     cudaEvent_t prev = st_prev;
-    for (const auto& pe : st_ev) {
+    std::vector<std::pair<float, size_t>> tr;
+    for (size_t i = 0; i < st_ev.size(); ++i) {
+      const auto& pe = st_ev[i];
       float t = 0.f;
       if (prev) cudaEventElapsedTime(&t, prev, pe.second);
       ms[pe.first] += t;
+      if (pe.first == S_TRUNC) tr.push_back({t, i});
       prev = pe.second;
     }
+    std::sort(tr.begin(), tr.end(), [](auto& a, auto& b) { return a.first > b.first; });
+    for (size_t q = 0; q < tr.size() && q < 12; ++q) {
+      const auto& m = st_meta[tr[q].second];
+      fprintf(stderr, "[hmgp]   lrupd launch %8.2f ms: max m %d, max n %d, items %d, longest seq %d\n",
+              tr[q].first, m[0], m[1], m[2], m[3]);
+    }
+    // histogram of lrupd time by max(m, n)
+    std::map<int, std::pair<double, int>> hist;
+    for (const auto& x : tr) {
+      const auto& m = st_meta[x.second];
+      int b = 1;
+      while (b < std::max(m[0], m[1])) b <<= 1;
+      hist[b].first += x.first;
+      hist[b].second += 1;
+    }
+    for (const auto& h : hist)
+      fprintf(stderr, "[hmgp]   lrupd max-dim <= %6d: %6d launches %9.1f ms\n", h.first, h.second.second,
+              h.second.first);
     for (int k = 0; k < S_N; ++k)
       fprintf(stderr, "[hmgp] %-10s launches %9lld items %10lld (%.1f/launch) %10.1f ms\n", nm[k],
               st_launch[k], st_items[k], st_launch[k] ? (double)st_items[k] / st_launch[k] : 0.0,
@@ -441,7 +476,7 @@ struct Engine {
         v.push_back(TrsmLItem{L.a, L.m, L.m, m.p, m.ld, m.cols, 0});
         mc = std::max(mc, m.cols.v);
       }
-      launch_trsm_left(sg.put(v), (int)v.size(), mc, st);
+      launch_trsm_left(sg.put(v), (int)v.size(), mc, st, L.m);
       stat(S_TRSML, v.size());
       return;
     }
@@ -529,7 +564,7 @@ struct Engine {
           mc = std::max(mc, V.cols.v);
           if (ldl) c.push_back(cpy(V.p, V.ld, V, V.cols, 0, 1.0, dseg(rb(l)), 2));
         }
-        launch_trsm_left(sg.put(v), (int)v.size(), mc, st);
+        launch_trsm_left(sg.put(v), (int)v.size(), mc, st, L.m);
       stat(S_TRSML, v.size());
         copy(c);
       }
@@ -665,6 +700,7 @@ struct Engine {
           t.push_back(ti);
         }
         toff.push_back((int)t.size());
+        if (stats_on) note_dims(l.m, l.n, (int)seq.size(), (int)v.size());
         trunc_smem_dims(l.m, l.n, &sw, &smn);
       }
     }

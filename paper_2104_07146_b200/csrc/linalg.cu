@@ -167,10 +167,58 @@ __global__ void k_trsm_left(const TrsmLItem* __restrict__ items) {
   }
 }
 
-void launch_trsm_left(const TrsmLItem* d_items, int count, int max_cols, cudaStream_t st) {
+// Shared-memory variant: the CTA stages L (b x b) once; each warp solves one
+// right-hand side column out of shared memory (lanes over rows).
+__global__ void __launch_bounds__(512) k_trsm_left_smem(const TrsmLItem* __restrict__ items) {
+  const TrsmLItem it = items[blockIdx.x];
+  const int cols = it.cols.get();
+  const int b = it.b;
+  if (cols <= 0 || blockIdx.y * (blockDim.x >> 5) >= cols) return;
+  extern __shared__ double sm[];
+  double* L = sm;
+  for (int e = threadIdx.x; e < b * b; e += blockDim.x) L[e] = it.L[(size_t)(e / b) * it.ldl + e % b];
+  if (blockIdx.y == 0 && threadIdx.x == 0) atomicAdd(&d_cnt_trsm, (double)b * b * cols);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int c = blockIdx.y * nw + w; c < cols; c += gridDim.y * nw) {
+    double* x = it.M + (size_t)c * it.ldm;
+    if (!it.trans) {
+      for (int j = 0; j < b; ++j) {
+        const double xj = x[j] / L[(size_t)j * b + j];
+        __syncwarp();
+        if (lane == 0) x[j] = xj;
+        for (int i = j + 1 + lane; i < b; i += 32) x[i] -= L[(size_t)j * b + i] * xj;
+        __syncwarp();
+      }
+    } else {
+      for (int j = b - 1; j >= 0; --j) {
+        double s = 0.0;
+        for (int i = j + 1 + lane; i < b; i += 32) s += L[(size_t)j * b + i] * x[i];
+        s = warp_sum(s);
+        if (lane == 0) x[j] = (x[j] - s) / L[(size_t)j * b + j];
+        __syncwarp();
+      }
+    }
+  }
+}
+
+void launch_trsm_left(const TrsmLItem* d_items, int count, int max_cols, cudaStream_t st,
+                      int max_b) {
   if (count <= 0) return;
-  const int gy = max(1, min((max_cols + 7) / 8, 32));
-  k_trsm_left<<<dim3(count, gy), 256, 0, st>>>(d_items);
+  const size_t bytes = (size_t)max_b * max_b * 8;
+  if (max_b > 0 && bytes <= 200 * 1024) {
+    static bool configured = false;
+    if (!configured) {
+      HMGP_CUDA(cudaFuncSetAttribute(k_trsm_left_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     200 * 1024));
+      configured = true;
+    }
+    const int gy = max(1, min((max_cols + 15) / 16, 32));
+    k_trsm_left_smem<<<dim3(count, gy), 512, bytes, st>>>(d_items);
+  } else {
+    const int gy = max(1, min((max_cols + 7) / 8, 32));
+    k_trsm_left<<<dim3(count, gy), 256, 0, st>>>(d_items);
+  }
   HMGP_LAUNCH_CHECK();
 }
 

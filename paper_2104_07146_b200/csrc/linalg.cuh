@@ -92,7 +92,8 @@ struct LeafFactorStatus {
 void launch_gemm(const GemmItem* d_items, int count, int max_tiles, cudaStream_t st);
 // per-target ordered sequences: CTA b runs items[off[b]..off[b+1]) in order
 void launch_gemm_seq(const GemmItem* d_items, const int* d_off, int targets, cudaStream_t st);
-void launch_trsm_left(const TrsmLItem* d_items, int count, int max_cols, cudaStream_t st);
+void launch_trsm_left(const TrsmLItem* d_items, int count, int max_cols, cudaStream_t st,
+                      int max_b);
 void launch_trsm_right(const TrsmRItem* d_items, int count, int max_rows, cudaStream_t st,
                        int max_t);
 void launch_copy_scale(const CopyScaleItem* d_items, int count, int max_elems, cudaStream_t st);
