@@ -444,7 +444,9 @@ void assemble(HMat& h, Geometry& g, const MaternDev& p, double eps, bool fixed_r
         for (size_t t = 0; t < c.leaves.size(); ++t) {
           const int k = c.leaves[t];
           woff.push_back(wsd);
-          wsd += c.cap[t] > 16 ? trunc_ws_doubles(mm[k], nn[k], c.cap[t]) : 0;
+          wsd += c.cap[t] <= 16 ? 0
+                 : trunc_use_cluster(mm[k], nn[k]) ? trunc_ws_doubles_cluster(mm[k], nn[k], c.cap[t])
+                                                   : trunc_ws_doubles(mm[k], nn[k], c.cap[t]);
         }
         c.ws = dmalloc<double>(wsd);
         std::vector<TruncItem> ti;
@@ -463,11 +465,23 @@ void assemble(HMat& h, Geometry& g, const MaternDev& p, double eps, bool fixed_r
           x.ws = c.ws + woff[t];
           ti.push_back(x);
         }
-        if (!ti.empty()) {
-          TruncItem* d_ti = upload(ti, st);
+        std::vector<TruncItem> tbig, tsmall;
+        for (const TruncItem& x : ti) (trunc_use_cluster(x.m, x.n) ? tbig : tsmall).push_back(x);
+        if (!tbig.empty()) {  // large blocks: one 8-CTA cluster each
+          TruncItem* d_tb = upload(tbig, st);
+          std::vector<int> off(tbig.size() + 1);
+          for (size_t q = 0; q <= tbig.size(); ++q) off[q] = (int)q;
+          int* d_off = upload(off, st);
+          launch_truncate_cluster(d_tb, d_off, (int)tbig.size(), eps, d_err, st);
+          HMGP_CUDA(cudaStreamSynchronize(st));
+          cudaFree(d_tb);
+          cudaFree(d_off);
+        }
+        if (!tsmall.empty()) {
+          TruncItem* d_ti = upload(tsmall, st);
           int sw = 0, smn = 0;
-          for (const TruncItem& x : ti) trunc_smem_dims(x.m, x.n, &sw, &smn);
-          launch_truncate(d_ti, (int)ti.size(), eps, d_err, st, sw, smn);
+          for (const TruncItem& x : tsmall) trunc_smem_dims(x.m, x.n, &sw, &smn);
+          launch_truncate(d_ti, (int)tsmall.size(), eps, d_err, st, sw, smn);
           HMGP_CUDA(cudaStreamSynchronize(st));
           cudaFree(d_ti);
         }

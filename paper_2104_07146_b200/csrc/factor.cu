@@ -214,7 +214,18 @@ struct Engine {
     st_next[2] = items;
     st_next[3] = std::max(st_next[3], seq);
   }
-  void lrupd(std::vector<TruncItem>& v) {
+  void lrupd(std::vector<TruncItem>& v0) {
+    if (v0.empty()) return;
+    // large blocks -> one 8-CTA cluster each; the rest -> one CTA each
+    std::vector<TruncItem> v, big;
+    for (const TruncItem& t : v0) (t.cond != 4 && trunc_use_cluster(t.m, t.n) ? big : v).push_back(t);
+    v0.clear();
+    if (!big.empty()) {
+      std::vector<int> off(big.size() + 1);
+      for (size_t i = 0; i <= big.size(); ++i) off[i] = (int)i;
+      launch_truncate_cluster(sg.put(big), sg.put(off), (int)big.size(), eps, d_err, st);
+      stat(S_TRUNC, big.size());
+    }
     if (v.empty()) return;
     int sw = 0, smn = 0;
     for (const TruncItem& t : v) {
@@ -311,7 +322,8 @@ struct Engine {
   void lrupd_ws(std::vector<TruncItem>& v) {
     for (auto& t : v) {
       if (t.cond == 4) continue;
-      t.ws = ar.dbl(trunc_ws_doubles(t.m, t.n, t.rcap));
+      t.ws = ar.dbl(trunc_use_cluster(t.m, t.n) ? trunc_ws_doubles_cluster(t.m, t.n, t.rcap)
+                                                : trunc_ws_doubles(t.m, t.n, t.rcap));
     }
     lrupd(v);
   }
@@ -664,8 +676,8 @@ struct Engine {
     const size_t mk = ar.mark();
     std::vector<GemmItem> g;
     std::vector<int> goff{0};
-    std::vector<TruncItem> t;
-    std::vector<int> toff{0};
+    std::vector<TruncItem> t, tb;
+    std::vector<int> toff{0}, tboff{0};
     int sw = 0, smn = 0;
     for (const auto& v : seq) {
       const int c = flat[v[0]].c;
@@ -691,22 +703,33 @@ struct Engine {
       } else {  // hblock.cpp:185-203
         int rcap = 0;
         for (int i : v) rcap = std::max(rcap, l.cap + flat[i].p.cols.v);
-        double* ws = ar.dbl(trunc_ws_doubles(l.m, l.n, rcap));
+        const bool clu = trunc_use_cluster(l.m, l.n);
+        double* ws = ar.dbl(clu ? trunc_ws_doubles_cluster(l.m, l.n, rcap)
+                                : trunc_ws_doubles(l.m, l.n, rcap));
+        std::vector<TruncItem>& dst = clu ? tb : t;
         for (int i : v) {
           const Add& a = flat[i];
           TruncItem ti = lritem(l.a, l.b, l.m, l.n, rankp(c), compp(c), 2, l.cap, &a.p, &a.q,
                                 a.row0 - rb(c), a.col0 - cb(c), a.alpha, l.cap + a.p.cols.v);
           ti.ws = ws;
-          t.push_back(ti);
+          dst.push_back(ti);
         }
-        toff.push_back((int)t.size());
-        if (stats_on) note_dims(l.m, l.n, (int)seq.size(), (int)v.size());
-        trunc_smem_dims(l.m, l.n, &sw, &smn);
+        if (clu) {
+          tboff.push_back((int)tb.size());
+        } else {
+          toff.push_back((int)t.size());
+          if (stats_on) note_dims(l.m, l.n, (int)seq.size(), (int)v.size());
+          trunc_smem_dims(l.m, l.n, &sw, &smn);
+        }
       }
     }
     if (!g.empty()) {
       launch_gemm_seq(sg.put(g), sg.put(goff), (int)goff.size() - 1, st);
       stat(S_GEMM, g.size());
+    }
+    if (!tb.empty()) {
+      launch_truncate_cluster(sg.put(tb), sg.put(tboff), (int)tboff.size() - 1, eps, d_err, st);
+      stat(S_TRUNC, tb.size());
     }
     if (!t.empty()) {
       launch_truncate_seq(sg.put(t), sg.put(toff), (int)toff.size() - 1, eps, d_err, st, sw, smn);

@@ -126,6 +126,11 @@ size_t trunc_ws_doubles(int m, int n, int rcap);
 void trunc_smem_dims(int m, int n, int* smem_w, int* smem_mn);
 void launch_truncate(const TruncItem* d_items, int count, double eps, int* d_err, cudaStream_t st,
                      int smem_w, int smem_mn);
+// large blocks: one 8-CTA cluster per target sequence (distributed Householder)
+bool trunc_use_cluster(int m, int n);
+size_t trunc_ws_doubles_cluster(int m, int n, int rcap);
+void launch_truncate_cluster(const TruncItem* d_items, const int* d_off, int targets, double eps,
+                             int* d_err, cudaStream_t st);
 // per-target ordered sequences: CTA b runs items[off[b]..off[b+1]) in order
 void launch_truncate_seq(const TruncItem* d_items, const int* d_off, int targets, double eps,
                          int* d_err, cudaStream_t st, int smem_w, int smem_mn);

@@ -11,6 +11,8 @@
 // Jacobi; the reference uses Eigen's two-sided JacobiSVD / dgesdd — the same
 // singular triplets up to rounding, so the kept rank only differs when a
 // singular value sits within rounding of the cut.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 
 #include "common.cuh"
@@ -586,6 +588,300 @@ __device__ void lr_update(const TruncItem& it, double eps, int* err, int smem_w,
     atomicAdd(&d_cnt_trunc, fl);
     atomicAdd(&d_cnt_titems, 1.0);
   }
+}
+
+// ===================================================================== //
+// Large blocks: one thread-block CLUSTER of kClu CTAs per target.  CTA c owns
+// the row slice [c*ms, (c+1)*ms) of the stacked factors; Householder QR and
+// the Q application run column by column with the per-column reductions
+// exchanged through distributed shared memory (2 cluster barriers per column,
+// double-buffered partials).  The small core R_u R_v^T goes through the same
+// rank-revealing SVD as the single-CTA path, on CTA 0.
+// ===================================================================== //
+constexpr int kClu = 8;
+constexpr int kCluMaxR = 1024;
+
+namespace cg = cooperative_groups;
+
+struct CluShared {
+  double part[2][kCluMaxR + 2];  // per column step: [0] tail norm^2, [1] row-k value, [2..] dots
+};
+
+// Distributed Householder QR of A (m x r, ld m) over the cluster's row slices.
+__device__ void clu_qr(cg::cluster_group& cl, CluShared& sh, double* A, int m, int r, double* tau) {
+  const int rank = cl.block_rank();
+  const int ms = (m + kClu - 1) / kClu, lo = rank * ms, hi = min(m, lo + ms);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __shared__ double red[32];
+  const int kmax = min(m, r);
+  for (int k = 0; k < kmax; ++k) {
+    double* P = sh.part[k & 1];
+    double* col = A + (size_t)k * m;
+    // (a) partial tail norm^2 over own rows > k; owner of row k publishes A(k,k)
+    double part = 0.0;
+    for (int i = max(lo, k + 1) + threadIdx.x; i < hi; i += blockDim.x) part += col[i] * col[i];
+    part = block_sum(part, red);
+    if (threadIdx.x == 0) {
+      P[0] = part;
+      P[1] = (k >= lo && k < hi) ? col[k] : 0.0;
+    }
+    cl.sync();
+    // (b) every CTA forms the same reflector from the cluster-wide sums
+    double tail2 = 0.0, c0 = 0.0;
+    for (int c = 0; c < kClu; ++c) {
+      const double* Q = cl.map_shared_rank(P, c);
+      tail2 += Q[0];
+      c0 += Q[1];
+    }
+    double t, beta, inv;
+    if (tail2 <= 2.2250738585072014e-308) {
+      t = 0.0;
+      beta = c0;
+      inv = 0.0;
+    } else {
+      beta = sqrt(c0 * c0 + tail2);
+      if (c0 >= 0.0) beta = -beta;
+      inv = 1.0 / (c0 - beta);
+      t = (beta - c0) / beta;
+    }
+    for (int i = max(lo, k + 1) + threadIdx.x; i < hi; i += blockDim.x) col[i] = (t == 0.0) ? 0.0 : col[i] * inv;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (k >= lo && k < hi) col[k] = beta;
+      if (rank == 0) tau[k] = t;
+    }
+    if (t == 0.0) {
+      cl.sync();
+      continue;
+    }
+    // (c) partial dots v^T A(:, j) over own rows for the trailing columns
+    for (int j = k + 1 + w; j < r; j += nw) {
+      const double* cj = A + (size_t)j * m;
+      double s = 0.0;
+      for (int i = max(lo, k + 1) + lane; i < hi; i += 32) s += col[i] * cj[i];
+      s = warp_sum(s);
+      if (lane == 0) P[2 + j] = s + ((k >= lo && k < hi) ? cj[k] : 0.0);
+    }
+    cl.sync();
+    // (d) full dots from every CTA, update own rows
+    for (int j = k + 1 + w; j < r; j += nw) {
+      double s = 0.0;
+      for (int c = 0; c < kClu; ++c) s += cl.map_shared_rank(P, c)[2 + j];
+      s *= t;
+      double* cj = A + (size_t)j * m;
+      for (int i = max(lo, k + 1) + lane; i < hi; i += 32) cj[i] -= s * col[i];
+      if (lane == 0 && k >= lo && k < hi) cj[k] -= s;
+    }
+    __syncthreads();
+  }
+  cl.sync();
+}
+
+// E <- Q E over the cluster's row slices (Q from clu_qr), E m x c (ld m).
+__device__ void clu_apply_q(cg::cluster_group& cl, CluShared& sh, const double* A, int m, int kq,
+                            const double* tau, double* E, int c) {
+  const int rank = cl.block_rank();
+  const int ms = (m + kClu - 1) / kClu, lo = rank * ms, hi = min(m, lo + ms);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int step = 0;  // buffer parity per EXECUTED step (skipped reflectors do not sync)
+  for (int k = kq - 1; k >= 0; --k) {
+    const double t = tau[k];
+    if (t == 0.0) continue;
+    double* P = sh.part[(step++) & 1];
+    const double* v = A + (size_t)k * m;
+    for (int j = w; j < c; j += nw) {
+      const double* e = E + (size_t)j * m;
+      double s = 0.0;
+      for (int i = max(lo, k + 1) + lane; i < hi; i += 32) s += v[i] * e[i];
+      s = warp_sum(s);
+      if (lane == 0) P[2 + j] = s + ((k >= lo && k < hi) ? e[k] : 0.0);
+    }
+    cl.sync();
+    for (int j = w; j < c; j += nw) {
+      double s = 0.0;
+      for (int q = 0; q < kClu; ++q) s += cl.map_shared_rank(P, q)[2 + j];
+      s *= t;
+      double* e = E + (size_t)j * m;
+      for (int i = max(lo, k + 1) + lane; i < hi; i += 32) e[i] -= s * v[i];
+      if (lane == 0 && k >= lo && k < hi) e[k] -= s;
+    }
+    __syncthreads();
+  }
+  cl.sync();
+}
+
+__device__ void lr_update_cluster(cg::cluster_group& cl, CluShared& sh, const TruncItem& it,
+                                  double eps, int* err) {
+  const int rank = cl.block_rank();
+  __shared__ double red[32];
+  __shared__ double s_sig[kMaxTruncCols];
+  __shared__ int s_ord[kMaxTruncCols];
+  __shared__ int s_keep, s_kq;
+  const int r0 = *it.rank;
+  const int add = it.P ? (it.addp ? *it.addp : it.addv) : 0;
+  const int r = r0 + add;
+  bool go;
+  switch (it.cond) {
+    case 1: go = r > 16; break;
+    case 2: go = r > *it.compact + 16; break;
+    case 3: go = r > 48; break;
+    case 4: go = false; break;
+    default: go = r > 0; break;
+  }
+  const int m = it.m, n = it.n;
+  const int msu = (m + kClu - 1) / kClu, mlo = rank * msu, mhi = min(m, mlo + msu);
+  const int msv = (n + kClu - 1) / kClu, nlo = rank * msv, nhi = min(n, nlo + msv);
+  if (!go) {
+    if (add > 0 && r > it.cap) {
+      if (rank == 0 && threadIdx.x == 0) atomicOr(err, 2);
+      cl.sync();
+      return;
+    }
+    for (int k = 0; k < add; ++k) {
+      for (int i = mlo + threadIdx.x; i < mhi; i += blockDim.x) {
+        const int pi = i - it.pro;
+        it.U[(size_t)(r0 + k) * m + i] = (pi >= 0 && pi < it.pr) ? it.alpha * it.P[(size_t)k * it.ldp + pi] : 0.0;
+      }
+      for (int i = nlo + threadIdx.x; i < nhi; i += blockDim.x) {
+        const int qi = i - it.qro;
+        it.V[(size_t)(r0 + k) * n + i] = (qi >= 0 && qi < it.qr) ? it.Q[(size_t)k * it.ldq + qi] : 0.0;
+      }
+    }
+    cl.sync();
+    if (rank == 0 && threadIdx.x == 0) {
+      *it.rank = r;
+      if (it.cond == 0 && it.compact) *it.compact = r;
+    }
+    cl.sync();
+    return;
+  }
+  if (r > it.rcap || r > kCluMaxR) {
+    if (rank == 0 && threadIdx.x == 0) atomicOr(err, 1);
+    cl.sync();
+    return;
+  }
+  double* WU = it.ws;
+  double* WV = WU + (size_t)m * it.rcap;
+  double* tu = WV + (size_t)n * it.rcap;
+  double* tv = tu + it.rcap;
+  double* C = tv + it.rcap;
+  // stage [U | aP] and [V | Q] (own row slices)
+  for (int l = 0; l < r; ++l) {
+    for (int i = mlo + threadIdx.x; i < mhi; i += blockDim.x) {
+      double v;
+      if (l < r0) {
+        v = it.U[(size_t)l * m + i];
+      } else {
+        const int pi = i - it.pro;
+        v = (pi >= 0 && pi < it.pr) ? it.alpha * it.P[(size_t)(l - r0) * it.ldp + pi] : 0.0;
+      }
+      WU[(size_t)l * m + i] = v;
+    }
+    for (int i = nlo + threadIdx.x; i < nhi; i += blockDim.x) {
+      double v;
+      if (l < r0) {
+        v = it.V[(size_t)l * n + i];
+      } else {
+        const int qi = i - it.qro;
+        v = (qi >= 0 && qi < it.qr) ? it.Q[(size_t)(l - r0) * it.ldq + qi] : 0.0;
+      }
+      WV[(size_t)l * n + i] = v;
+    }
+  }
+  cl.sync();
+  clu_qr(cl, sh, WU, m, r, tu);
+  clu_qr(cl, sh, WV, n, r, tv);
+  const int ku = min(m, r), kv = min(n, r);
+  const int kqmax = min(ku, kv);
+  double* tau = C + (size_t)ku * kv;
+  double* cn = tau + kv;
+  int* piv = reinterpret_cast<int*>(cn + kv);
+  double* G = cn + 2 * kv;
+  double* J = G + (size_t)kv * kqmax;
+  double* Uc = J + (size_t)kqmax * kqmax;
+  double* gsig = Uc + (size_t)ku * kqmax;  // exported sigma / order for the other CTAs
+  int* gord = reinterpret_cast<int*>(gsig + kqmax);
+  RS rs{0, 0, 0.0};
+  if (rank == 0) {
+    for (int idx = threadIdx.x; idx < ku * kv; idx += blockDim.x) {
+      const int i = idx % ku, j = idx / ku;
+      double s = 0.0;
+      for (int l = max(i, j); l < r; ++l) s += WU[(size_t)l * m + i] * WV[(size_t)l * n + j];
+      C[(size_t)j * ku + i] = s;
+    }
+    __syncthreads();
+    rs = cta_rrqr_svd(C, ku, kv, eps, tau, piv, cn, G, J, s_sig, s_ord, red);
+    for (int idx = threadIdx.x; idx < ku * rs.keep; idx += blockDim.x) {
+      const int i = idx % ku, c = idx / ku, src = s_ord[c];
+      Uc[idx] = i < rs.kq ? J[(size_t)src * rs.kq + i] * s_sig[src] : 0.0;
+    }
+    __syncthreads();
+    cta_apply_q(C, ku, rs.kq, tau, Uc, rs.keep);
+    for (int c = threadIdx.x; c < rs.keep; c += blockDim.x) {
+      gsig[c] = s_sig[s_ord[c]];
+      gord[c] = s_ord[c];
+    }
+    if (threadIdx.x == 0) {
+      s_keep = rs.keep;
+      s_kq = rs.kq;
+      gord[kqmax] = rs.keep;  // published to the cluster through global memory
+    }
+    __syncthreads();
+  }
+  cl.sync();
+  const int keep = gord[kqmax];
+  if (keep > it.cap) {
+    if (rank == 0 && threadIdx.x == 0) atomicOr(err, 4);
+    cl.sync();
+    return;
+  }
+  // E_u = [U_core; 0] -> it.U, E_v = [Y; 0] -> it.V (own row slices)
+  for (int c = 0; c < keep; ++c) {
+    for (int i = mlo + threadIdx.x; i < mhi; i += blockDim.x)
+      it.U[(size_t)c * m + i] = i < ku ? Uc[(size_t)c * ku + i] : 0.0;
+    const int src = gord[c];
+    const double sg = gsig[c];
+    for (int i = nlo + threadIdx.x; i < nhi; i += blockDim.x)
+      it.V[(size_t)c * n + i] = i < kv ? G[(size_t)src * kv + i] / sg : 0.0;
+  }
+  cl.sync();
+  clu_apply_q(cl, sh, WU, m, ku, tu, it.U, keep);
+  clu_apply_q(cl, sh, WV, n, kv, tv, it.V, keep);
+  if (rank == 0 && threadIdx.x == 0) {
+    *it.rank = keep;
+    if (it.compact) *it.compact = keep;
+    const double fl = qr_flops(m, r) + qr_flops(n, r) + (double)ku * kv * r + rs.flops +
+                      4.0 * keep * ((double)m * ku + (double)n * kv + (double)ku * s_kq);
+    atomicAdd(&d_cnt_trunc, fl);
+    atomicAdd(&d_cnt_titems, 1.0);
+  }
+  cl.sync();
+}
+
+// cluster b (CTAs b*kClu .. b*kClu+kClu-1) runs target b's sequence in order
+__global__ void __cluster_dims__(kClu, 1, 1) __launch_bounds__(kTruncThreads)
+    k_truncate_cluster(const TruncItem* __restrict__ items, const int* __restrict__ off, double eps,
+                       int* err) {
+  cg::cluster_group cl = cg::this_cluster();
+  __shared__ CluShared sh;
+  const int b = blockIdx.x / kClu;
+  for (int i = off[b]; i < off[b + 1]; ++i) lr_update_cluster(cl, sh, items[i], eps, err);
+}
+
+size_t trunc_ws_doubles_cluster(int m, int n, int rcap) {
+  const size_t rc = (size_t)rcap, kq = std::min((size_t)std::min(m, n), rc);
+  return (size_t)(m + n) * rc + 5 * rc + rc * rc + 3 * rc * kq + kq * kq + 2 * kq + 2;
+}
+
+bool trunc_use_cluster(int m, int n) {
+  return !((size_t)m * n <= (size_t)kMaxSmemW && m + n <= kMaxSmemMN) && std::max(m, n) >= 512;
+}
+
+void launch_truncate_cluster(const TruncItem* d_items, const int* d_off, int targets, double eps,
+                             int* d_err, cudaStream_t st) {
+  if (targets <= 0) return;
+  k_truncate_cluster<<<targets * kClu, kTruncThreads, 0, st>>>(d_items, d_off, eps, d_err);
+  HMGP_LAUNCH_CHECK();
 }
 
 void launch_truncate(const TruncItem* d_items, int count, double eps, int* d_err, cudaStream_t st,
