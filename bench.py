@@ -247,12 +247,64 @@ def run_ours(args):
             "roofline": roofline,
             "hbm_peak_gbs": peaks.get("hbm_gbs"),
         }
+        if not args.no_extras and not args.small:
+            line["extras"] = extras(hm, _lib, ctx, stream)
         if not args.no_cpu_baseline and ws == 1:
             line["cpu_baseline"] = cpu_baseline(budget_s=args.cpu_budget)
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def extras(hm, _lib, ctx, stream):
+    """Other BASELINE configs, measured once each (device events on the library
+    stream): C2 assembly entries/s and C4-shaped kriging predictions/s."""
+    import torch
+    out = {}
+
+    def dev_ms(fn):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        r = fn()
+        e1.record(stream)
+        e1.synchronize()
+        return e0.elapsed_time(e1), r
+
+    # C2: assembly only, n = 65536 jittered 256x256, leaf 64, eta 2, eps 1e-7
+    x = hm.jittered_grid(256, SEED)
+    g = hm.Geometry(x, 64, 2.0, ctx=ctx)
+    cnt, na, nd = g.block_counts()
+    c2 = {"n": 65536, "leaf": 64, "eps": 1e-7, "blocks": int(cnt), "admissible": int(na), "dense": int(nd)}
+    w = (C.c_double * 10)()
+    for nu in (0.5, 1.5, 0.325):
+        th = [1.0, 0.1, nu, 0.01]
+        hm.assemble(g, th, hm.RankControl.fixed_accuracy(1e-7))  # warm-up
+        _lib.hmgp_work_counters(w, 10, 1)
+        ms, h = dev_ms(lambda: hm.assemble(g, th, hm.RankControl.fixed_accuracy(1e-7)))
+        _lib.hmgp_work_counters(w, 10, 1)
+        entries = w[0] + w[1]
+        c2[f"nu={nu}"] = {"ms": ms, "entries": entries, "entries_per_s": entries / (ms / 1e3),
+                          "dense_entries": w[0], "aca_entries": w[1], "max_rank": h.stats()["max_rank"]}
+        del h
+    out["C2_assembly"] = c2
+    # C4-shaped kriging: n = 65536 training (jittered), m = 10000 uniform test points,
+    # θ = (1, 0.1, 0.5, 0.01); Z iid normals (exact-sample Z needs a 34 GB dense
+    # Cholesky — a data utility outside the timed path, not built yet)
+    z = hm.normals(65536, Z_SEED)
+    te = hm.random_locations(10000, SEED + 1)
+    cfg = hm.HConfig(leaf_size=64, rank=hm.RankControl.fixed_accuracy(1e-7))
+    hm.predict(x, z, te[:100], [1.0, 0.1, 0.5, 0.01], cfg, ctx=ctx)  # warm-up
+    ms, pr = dev_ms(lambda: hm.predict(x, z, te, [1.0, 0.1, 0.5, 0.01], cfg, ctx=ctx))
+    ph = (C.c_double * 10)()
+    _lib.hmgp_last_phases(ctx.h, ph, 10)
+    out["C4_kriging"] = {"n": 65536, "m": 10000, "theta": [1.0, 0.1, 0.5, 0.01], "ms": ms,
+                         "predictions_per_s": 10000 / (ms / 1e3),
+                         "cross_covariance_ms": ph[9], "cross_entries_per_s": 10000 * 65536 / (ph[9] / 1e3)
+                         if ph[9] > 0 else None, "factor_ms": ph[5]}
+    return out
 
 
 # --------------------------------------------------------------------------
@@ -316,6 +368,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--small", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=30.0)
     args = ap.parse_args()
     if args.impl == "reference":
