@@ -18,6 +18,7 @@
 #include <cmath>
 #include <cstring>
 #include <array>
+#include <chrono>
 #include <map>
 #include <vector>
 
@@ -1206,6 +1207,16 @@ __global__ void k_trsv_leaf(const double* __restrict__ L, int b, double* __restr
   }
 }
 
+struct CloneItem {
+  const double* src;
+  double* dst;
+  size_t count;
+};
+__global__ void k_clone(const CloneItem* __restrict__ items) {
+  const CloneItem it = items[blockIdx.x];
+  for (size_t i = threadIdx.x; i < it.count; i += blockDim.x) it.dst[i] = it.src[i];
+}
+
 static void launch_trsv(const double* L, int b, double* x, int trans, cudaStream_t st) {
   const size_t bytes = ((size_t)b * b + b) * 8;
   if (bytes <= 200 * 1024) {
@@ -1343,14 +1354,7 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
   F.leaf_node = H.leaf_node;
   const int L = (int)H.leaf.size();
   // clone payload (hblock.cpp:17-28): same layout, new pool; compact_cols = 0
-  HMGP_CUDA(cudaMalloc(&F.pool, std::max<size_t>(1, H.pool_doubles) * 8));
-  F.leaf = H.leaf;
-  for (auto& l : F.leaf) {
-    l.a = F.pool + (l.a - H.pool);
-    if (l.b) l.b = F.pool + (l.b - H.pool);
-  }
   HMGP_CUDA(cudaMalloc(&F.d_leaf, sizeof(LeafDev) * std::max(L, 1)));
-  HMGP_CUDA(cudaMemcpyAsync(F.d_leaf, F.leaf.data(), sizeof(LeafDev) * L, cudaMemcpyHostToDevice, st));
   HMGP_CUDA(cudaMalloc(&F.d_rank, 4 * std::max(L, 1)));
   HMGP_CUDA(cudaMalloc(&F.d_compact, 4 * std::max(L, 1)));
   HMGP_CUDA(cudaMalloc(&F.d_d, 8ull * G.n));
@@ -1360,9 +1364,55 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
   // Temporaries are sized with a width capacity TCAP; a product wider than that
   // is detected on device (error flag) and the factorization is redone with a
   // doubled capacity — results never depend on the capacity that succeeded.
-  for (int tcap = 256;; tcap *= 2) {
-    // clone payload (hblock.cpp:17-28): same layout; compact_cols = 0
-    HMGP_CUDA(cudaMemcpyAsync(F.pool, H.pool, H.pool_doubles * 8, cudaMemcpyDeviceToDevice, st));
+  // A low-rank block whose rank outgrows its column capacity, or a product wider
+  // than TCAP, is detected on device; the factorization is then redone with
+  // doubled capacities (results do not depend on the capacities that succeed).
+  int grow = 1;
+  size_t pool_doubles = 0;
+  for (int tcap = 256;;) {
+    // clone payload (hblock.cpp:17-28) into the factor's own layout; compact_cols = 0
+    F.leaf = H.leaf;
+    size_t total = 0;
+    std::vector<size_t> off(L);
+    for (int k = 0; k < L; ++k) {
+      LeafDev& l = F.leaf[k];
+      off[k] = total;
+      if (l.kind == DENSE) {
+        total += (size_t)l.m * l.n;
+      } else {
+        l.cap = std::min(std::min(l.m, l.n) + 16, H.leaf[k].cap * grow);
+        total += (size_t)(l.m + l.n) * l.cap;
+      }
+    }
+    if (total != pool_doubles) {
+      cudaFree(F.pool);
+      F.pool = nullptr;
+      HMGP_CUDA(cudaMalloc(&F.pool, std::max<size_t>(1, total) * 8));
+      pool_doubles = total;
+    }
+    std::vector<CloneItem> ci;
+    for (int k = 0; k < L; ++k) {
+      LeafDev& l = F.leaf[k];
+      l.a = F.pool + off[k];
+      l.b = l.kind == DENSE ? nullptr : l.a + (size_t)l.m * l.cap;
+      const LeafDev& s = H.leaf[k];
+      if (l.kind == DENSE) {
+        ci.push_back(CloneItem{s.a, l.a, (size_t)l.m * l.n});
+      } else if (H.rank_host[k] > 0) {  // U and V prefixes are contiguous (ld = m, n)
+        ci.push_back(CloneItem{s.a, l.a, (size_t)l.m * H.rank_host[k]});
+        ci.push_back(CloneItem{s.b, l.b, (size_t)l.n * H.rank_host[k]});
+      }
+    }
+    HMGP_CUDA(cudaMemcpyAsync(F.d_leaf, F.leaf.data(), sizeof(LeafDev) * L, cudaMemcpyHostToDevice, st));
+    if (!ci.empty()) {
+      CloneItem* d_ci = nullptr;
+      HMGP_CUDA(cudaMalloc(&d_ci, sizeof(CloneItem) * ci.size()));
+      HMGP_CUDA(cudaMemcpyAsync(d_ci, ci.data(), sizeof(CloneItem) * ci.size(), cudaMemcpyHostToDevice, st));
+      k_clone<<<(int)ci.size(), 256, 0, st>>>(d_ci);
+      HMGP_LAUNCH_CHECK();
+      HMGP_CUDA(cudaStreamSynchronize(st));
+      cudaFree(d_ci);
+    }
     HMGP_CUDA(cudaMemcpyAsync(F.d_rank, H.d_rank, 4ull * L, cudaMemcpyDeviceToDevice, st));
     HMGP_CUDA(cudaMemsetAsync(F.d_compact, 0, 4ull * L, st));
     HMGP_CUDA(cudaMemsetAsync(F.d_d, 0, 8ull * G.n, st));
@@ -1372,13 +1422,22 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
     {
       Engine E(F, st, arena_bytes, tcap);
       E.stats_begin();
+      const auto h0 = std::chrono::steady_clock::now();
       E.factor_diag(0);
       // compress_all (hfactor.cpp:321-328): every LR leaf, independent
       std::vector<int> lr;
       for (int k = 0; k < L; ++k)
         if (F.leaf[k].kind == LOWRANK) lr.push_back(F.leaf_node[k]);
       E.compress(lr);
-      if (getenv("HMGP_STATS")) E.print_stats();
+      if (getenv("HMGP_STATS")) {
+        const auto h1 = std::chrono::steady_clock::now();
+        cudaStreamSynchronize(st);
+        const auto h2 = std::chrono::steady_clock::now();
+        fprintf(stderr, "[hmgp] host enqueue %.1f ms, then GPU drain %.1f ms\n",
+                std::chrono::duration<double, std::milli>(h1 - h0).count(),
+                std::chrono::duration<double, std::milli>(h2 - h1).count());
+        E.print_stats();
+      }
       phase_mark(PH_FACTOR);
       HMGP_CUDA(cudaMemcpyAsync(&err, E.d_err, 4, cudaMemcpyDeviceToHost, st));
       HMGP_CUDA(cudaStreamSynchronize(st));
@@ -1387,8 +1446,10 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
       g_work.factor_attempts += 1;
     }
     if (!err) break;
-    if (tcap >= 1024)
+    if (tcap >= 1024 && grow >= 16)
       throw Error(6, "factorize: low-rank capacity exceeded (code " + std::to_string(err) + ")");
+    tcap = std::min(1024, tcap * 2);
+    grow *= 2;
   }
   LeafFactorStatus s{};
   HMGP_CUDA(cudaMemcpyAsync(&s, F.d_status, sizeof(s), cudaMemcpyDeviceToHost, st));
