@@ -300,6 +300,19 @@ def extras(hm, _lib, ctx, stream):
     ms, pr = dev_ms(lambda: hm.predict(x, z, te, [1.0, 0.1, 0.5, 0.01], cfg, ctx=ctx))
     ph = (C.c_double * 10)()
     _lib.hmgp_last_phases(ctx.h, ph, 10)
+    # C4 θ-sweep throughput on one GPU: an 8-θ subset of the 512-point grid
+    # (every ν and τ², σ² and ℓ at grid values), one geometry, hmgp_loglik_batch
+    from paper_2104_07146_b200 import sweep as sw
+    grid = sw.c4_theta_grid()
+    sub = [i for i in range(len(grid)) if grid[i, 0] == sw.C4_SIGMA2[3] and grid[i, 1] == sw.C4_ELL[3]]
+    g64 = hm.Geometry(x, 64, 2.0, ctx=ctx)
+    dz = torch.from_numpy(z).to(torch.device("cuda", ctx.device))
+    torch.cuda.synchronize()
+    ms_sw, vals = dev_ms(lambda: sw.run_sweep(g64, dz.data_ptr(), grid, sub, cfg, ctx))
+    out["C4_sweep_subset"] = {"n": 65536, "thetas": len(sub), "ms": ms_sw,
+                              "evals_per_s": len(sub) / (ms_sw / 1e3),
+                              "theta_idx": sub, "loglik": vals[:, 0].tolist(),
+                              "status": vals[:, 3].tolist()}
     out["C4_kriging"] = {"n": 65536, "m": 10000, "theta": [1.0, 0.1, 0.5, 0.01], "ms": ms,
                          "predictions_per_s": 10000 / (ms / 1e3),
                          "cross_covariance_ms": ph[9], "cross_entries_per_s": 10000 * 65536 / (ph[9] / 1e3)

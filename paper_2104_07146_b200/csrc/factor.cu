@@ -515,17 +515,12 @@ struct Engine {
       const LeafDev& L = LF(l);
       std::vector<TrsmRItem> v;
       int mr = 1;
-      for (const MV& x : xs) {
-        v.push_back(TrsmRItem{L.a, L.m, L.m, x.p, x.ld, x.rows});
+      for (const MV& x : xs) {  // X <- X L^{-T} D^{-1} in one launch
+        v.push_back(TrsmRItem{L.a, L.m, L.m, x.p, x.ld, x.rows, ldl ? dseg(rb(l)) : nullptr});
         mr = std::max(mr, x.rows);
       }
       launch_trsm_right(sg.put(v), (int)v.size(), mr, st, L.m);
       stat(S_TRSMR, v.size());
-      if (ldl) {
-        std::vector<CopyScaleItem> c;
-        for (const MV& x : xs) c.push_back(cpy(x.p, x.ld, x, dimv(L.m), 0, 1.0, dseg(rb(l)), 4));
-        copy(c);
-      }
       return;
     }
     const int l00 = kid(l, 0, 0), l10 = kid(l, 1, 0), l11 = kid(l, 1, 1);
@@ -567,19 +562,20 @@ struct Engine {
     if (kind(l) == DENSE) {
       const LeafDev& L = LF(l);
       if (!lr.empty()) {
-        compress(lr);
-        std::vector<TrsmLItem> v;
-        std::vector<CopyScaleItem> c;
-        int mc = 1;
+        // compress_low_rank + V <- L^{-1} V (+ D^{-1}) fused in one launch
+        const size_t mk = ar.mark();
+        std::vector<TruncItem> v;
         for (int x : lr) {
-          const MV V = Vv(x);
-          v.push_back(TrsmLItem{L.a, L.m, L.m, V.p, V.ld, V.cols, 0});
-          mc = std::max(mc, V.cols.v);
-          if (ldl) c.push_back(cpy(V.p, V.ld, V, V.cols, 0, 1.0, dseg(rb(l)), 2));
+          const LeafDev& lx = LF(x);
+          TruncItem t = lritem(lx.a, lx.b, lx.m, lx.n, rankp(x), compp(x), 0, lx.cap, nullptr,
+                               nullptr, 0, 0, 1.0, lx.cap);
+          t.post_L = L.a;
+          t.post_ldl_ld = L.m;
+          t.post_d = ldl ? dseg(rb(l)) : nullptr;
+          v.push_back(t);
         }
-        launch_trsm_left(sg.put(v), (int)v.size(), mc, st, L.m);
-      stat(S_TRSML, v.size());
-        copy(c);
+        lrupd_ws(v);
+        ar.release(mk);
       }
       if (!dn.empty()) {
         std::vector<MV> d;

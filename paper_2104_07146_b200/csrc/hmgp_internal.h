@@ -120,6 +120,11 @@ struct TruncItem {
   double alpha;
   int rcap;    // workspace column capacity (>= rank + add)
   double* ws;  // trunc_ws_doubles(m, n, rcap)
+  // optional fused post-op (trsm_lower_t with a dense leaf, hfactor.cpp:198-202):
+  // V <- L^{-1} V (L n x n lower, stored diagonal), then V rows /= d (LDL)
+  const double* post_L;
+  int post_ldl_ld;
+  const double* post_d;
 };
 size_t trunc_ws_doubles(int m, int n, int rcap);
 // grow the per-launch shared-memory dims for an item that can take the small-block path

@@ -233,6 +233,8 @@ __global__ void k_trsm_right(const TrsmRItem* __restrict__ items) {
       const double* lc = it.L + (size_t)j * it.ldl;
       for (int c = j + 1; c < it.t; ++c) it.X[(size_t)c * it.ldx + r] -= xj * lc[c];
     }
+    if (it.d)
+      for (int j = 0; j < it.t; ++j) it.X[(size_t)j * it.ldx + r] /= it.d[j];
   }
 }
 
@@ -266,7 +268,7 @@ __global__ void __launch_bounds__(256) k_trsm_right_smem(const TrsmRItem* __rest
     }
     for (int e = threadIdx.x; e < kTrsmRTile * t; e += blockDim.x) {
       const int r = e % kTrsmRTile, c = e / kTrsmRTile;
-      if (r < rows) it.X[(size_t)c * it.ldx + r0 + r] = X[e];
+      if (r < rows) it.X[(size_t)c * it.ldx + r0 + r] = it.d ? X[e] / it.d[c] : X[e];
     }
   }
   if (blockIdx.y == 0 && threadIdx.x == 0) atomicAdd(&d_cnt_trsm, (double)t * t * it.s);

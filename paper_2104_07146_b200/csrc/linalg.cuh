@@ -45,6 +45,7 @@ struct TrsmRItem {
   int ldl, t;
   double* X;
   int ldx, s;
+  const double* d;  // optional: then column j /= d[j] (LDL, hfactor.cpp:205-207)
 };
 
 // dst (rows x cols) = alpha * op(src) [.* scale], scale by d on rows (mode 1 mul,

@@ -374,10 +374,36 @@ __device__ RS cta_rrqr_svd(double* W, int p, int q, double eps, double* tau, int
 
 __device__ void lr_update(const TruncItem& it, double eps, int* err, int smem_w, int smem_mn);
 
+// Fused trsm_lower_t post-op (hfactor.cpp:198-202): V <- L^{-1} V, V /= d.
+// One warp per column, lanes over rows; L read through L1/L2.
+__device__ void lr_post_solve(const TruncItem& it) {
+  const int cols = *it.rank, n = it.n, ld = it.post_ldl_ld;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const double* L = it.post_L;
+  for (int c = w; c < cols; c += nw) {
+    double* x = it.V + (size_t)c * n;
+    for (int j = 0; j < n; ++j) {
+      const double xj = x[j] / L[(size_t)j * ld + j];
+      __syncwarp();
+      if (lane == 0) x[j] = xj;
+      const double* lc = L + (size_t)j * ld;
+      for (int i = j + 1 + lane; i < n; i += 32) x[i] -= lc[i] * xj;
+      __syncwarp();
+    }
+    if (it.post_d)
+      for (int i = lane; i < n; i += 32) x[i] /= it.post_d[i];
+  }
+}
+
 __global__ void __launch_bounds__(kTruncThreads) k_truncate(const TruncItem* __restrict__ items,
                                                             double eps, int* err, int smem_w,
                                                             int smem_mn) {
-  lr_update(items[blockIdx.x], eps, err, smem_w, smem_mn);
+  const TruncItem& it = items[blockIdx.x];
+  lr_update(it, eps, err, smem_w, smem_mn);
+  if (it.post_L) {
+    __syncthreads();
+    lr_post_solve(it);
+  }
 }
 
 // One CTA per target: its updates items[off[b] .. off[b+1]) run in order (the
@@ -865,7 +891,13 @@ __global__ void __cluster_dims__(kClu, 1, 1) __launch_bounds__(kTruncThreads)
   cg::cluster_group cl = cg::this_cluster();
   __shared__ CluShared sh;
   const int b = blockIdx.x / kClu;
-  for (int i = off[b]; i < off[b + 1]; ++i) lr_update_cluster(cl, sh, items[i], eps, err);
+  for (int i = off[b]; i < off[b + 1]; ++i) {
+    lr_update_cluster(cl, sh, items[i], eps, err);
+    if (items[i].post_L) {
+      if (cl.block_rank() == 0) lr_post_solve(items[i]);
+      cl.sync();
+    }
+  }
 }
 
 size_t trunc_ws_doubles_cluster(int m, int n, int rcap) {
