@@ -461,8 +461,97 @@ __global__ void k_leaf_factor(double* __restrict__ Dg, int b, int base, int ldl,
   }
 }
 
+// Register-resident right-looking variant for b <= 128: thread t owns row
+// i = t % b and the columns k = t / b + q*G (G = 1024 / b groups), held in
+// registers.  Column j is exchanged through shared memory once per step; the
+// update A(i,k) -= c_i c_k / s is the same for LDL (l = c/s, d = s) and
+// Cholesky (l = c/sqrt(s)).  Two barriers per column.
+constexpr int kLeafRegThreads = 1024;
+constexpr int kLeafRegMaxK = 16;  // columns per thread for b = 128
+__global__ void __launch_bounds__(kLeafRegThreads) k_leaf_factor_reg(double* __restrict__ Dg, int b,
+                                                                     int base, int ldl,
+                                                                     double* __restrict__ d,
+                                                                     double clamp_tol,
+                                                                     LeafFactorStatus* st) {
+  __shared__ double col[128];
+  __shared__ double s_piv;
+  const int G = kLeafRegThreads / b;
+  const int t = threadIdx.x;
+  const bool active = t < G * b;
+  const int i = t % b, g = t / b;
+  const int nk = (b + G - 1) / G;
+  double a[kLeafRegMaxK];
+#pragma unroll
+  for (int q = 0; q < kLeafRegMaxK; ++q) {
+    const int k = g + q * G;
+    a[q] = (active && q < nk && k < b) ? Dg[(size_t)k * b + i] : 0.0;
+  }
+  if (t == 0) atomicAdd(&d_cnt_leaf, (double)b * b * b / 3.0);
+  for (int j = 0; j < b; ++j) {
+    // owners of column j publish it (q = j / G for group g = j % G)
+    if (active && g == j % G) {
+#pragma unroll
+      for (int q = 0; q < kLeafRegMaxK; ++q)
+        if (q == j / G) col[i] = a[q];
+    }
+    __syncthreads();
+    if (t == 0) {
+      double s = col[j];
+      atomic_min_double(&st->min_pivot, s);
+      bool failed;
+      if (ldl) {
+        failed = (s == 0.0);
+        if (s < 0.0) {
+          if (-s <= clamp_tol) {
+            s = clamp_tol;
+            atomicAdd(&st->clamped, 1);
+          } else {
+            atomicAdd(&st->negative, 1);
+          }
+        }
+        d[base + j] = s;
+      } else {
+        failed = !(s > 0.0);
+      }
+      if (failed) {
+        const int pos = base + j;
+        if (atomicMin(&st->fail_pos, pos) > pos) st->fail_val = s;
+      }
+      s_piv = s;
+    }
+    __syncthreads();
+    const double s = s_piv;
+    if (active && i > j) {
+      const double ci = col[i] / s;
+#pragma unroll
+      for (int q = 0; q < kLeafRegMaxK; ++q) {
+        const int k = g + q * G;
+        if (q < nk && k > j && k <= i) a[q] -= ci * col[k];
+      }
+    }
+    // finalize column j in its owners' registers
+    if (active && g == j % G) {
+      const double piv = ldl ? s : sqrt(s);
+#pragma unroll
+      for (int q = 0; q < kLeafRegMaxK; ++q)
+        if (q == j / G) a[q] = (i == j) ? (ldl ? 1.0 : piv) : (i > j ? a[q] / piv : 0.0);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < kLeafRegMaxK; ++q) {
+    const int k = g + q * G;
+    if (active && q < nk && k < b) Dg[(size_t)k * b + i] = (i < k) ? 0.0 : a[q];
+  }
+}
+
 void launch_leaf_factor(double* D, int b, int base, int ldl, double* d, double clamp_tol,
                         LeafFactorStatus* status, cudaStream_t st) {
+  if (b <= 128 && (b + (kLeafRegThreads / b) - 1) / (kLeafRegThreads / b) <= kLeafRegMaxK) {
+    k_leaf_factor_reg<<<1, kLeafRegThreads, 0, st>>>(D, b, base, ldl, d, clamp_tol, status);
+    HMGP_LAUNCH_CHECK();
+    return;
+  }
   const size_t bytes = (size_t)b * b * 8;
   const int use_smem = bytes <= 200 * 1024;
   if (use_smem && bytes > 48 * 1024)

@@ -56,6 +56,38 @@ void trunc_smem_dims(int m, int n, int* smem_w, int* smem_mn) {
   }
 }
 
+// Apply H = I - t v v^T (v = [1; col[k+1:m]]) to columns [j0, j1) of A (ld m):
+// one warp per column group of 4, four independent dot products in flight per
+// warp so the L1/L2 load latency of one column overlaps the others.
+__device__ __forceinline__ void reflect_cols(double* A, int m, int k, const double* col, double t,
+                                             int j0, int j1, int lane, int w, int nw) {
+  for (int jb = j0 + 4 * w; jb < j1; jb += 4 * nw) {
+    double* c[4];
+    double s[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      c[u] = A + (size_t)min(jb + u, j1 - 1) * m;
+      s[u] = 0.0;
+    }
+    for (int i = k + 1 + lane; i < m; i += 32) {
+      const double v = col[i];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) s[u] += v * c[u][i];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) s[u] = warp_sum(s[u]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) s[u] = (s[u] + c[u][k]) * t;
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (jb + u >= j1) continue;
+      for (int i = k + 1 + lane; i < m; i += 32) c[u][i] -= s[u] * col[i];
+      if (lane == 0) c[u][k] -= s[u];
+    }
+  }
+}
+
 // In-place Householder QR of A (m x r, ld m) inside one CTA; tau[min(m,r)].
 __device__ void cta_householder(double* A, int m, int r, double* tau, double* red) {
   const int kmax = min(m, r);
@@ -89,17 +121,7 @@ __device__ void cta_householder(double* A, int m, int r, double* tau, double* re
       tau[k] = t;
     }
     __syncthreads();
-    if (t != 0.0) {
-      for (int j = k + 1 + w; j < r; j += nw) {
-        double* cj = A + (size_t)j * m;
-        double s = 0.0;
-        for (int i = k + 1 + lane; i < m; i += 32) s += col[i] * cj[i];
-        s = warp_sum(s);
-        s = (s + cj[k]) * t;
-        for (int i = k + 1 + lane; i < m; i += 32) cj[i] -= s * col[i];
-        if (lane == 0) cj[k] -= s;
-      }
-    }
+    if (t != 0.0) reflect_cols(A, m, k, col, t, k + 1, r, lane, w, nw);
     __syncthreads();
   }
 }
@@ -109,18 +131,7 @@ __device__ void cta_apply_q(const double* QR, int m, int kq, const double* tau, 
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int k = kq - 1; k >= 0; --k) {
     const double t = tau[k];
-    if (t != 0.0) {
-      const double* v = QR + (size_t)k * m;
-      for (int j = w; j < c; j += nw) {
-        double* e = E + (size_t)j * m;
-        double s = 0.0;
-        for (int i = k + 1 + lane; i < m; i += 32) s += v[i] * e[i];
-        s = warp_sum(s);
-        s = (s + e[k]) * t;
-        for (int i = k + 1 + lane; i < m; i += 32) e[i] -= s * v[i];
-        if (lane == 0) e[k] -= s;
-      }
-    }
+    if (t != 0.0) reflect_cols(E, m, k, QR + (size_t)k * m, t, 0, c, lane, w, nw);
     __syncthreads();
   }
 }
@@ -316,25 +327,45 @@ __device__ RS cta_rrqr_svd(double* W, int p, int q, double eps, double* tau, int
       tau[k] = t;
     }
     __syncthreads();
-    for (int j = k + 1 + w; j < q; j += nw) {  // apply H_k, refresh the trailing norms
-      double* cj = W + (size_t)j * p;
-      double s = 0.0;
+    // apply H_k and refresh the trailing norms, 4 columns per warp in flight
+    for (int jb = k + 1 + 4 * w; jb < q; jb += 4 * nw) {
+      double* c4[4];
+      double s[4], s2[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        c4[u] = W + (size_t)min(jb + u, q - 1) * p;
+        s[u] = 0.0;
+        s2[u] = 0.0;
+      }
       if (t != 0.0) {
-        for (int i = k + 1 + lane; i < p; i += 32) s += col[i] * cj[i];
-        s = warp_sum(s);
-        s = (s + cj[k]) * t;
+        for (int i = k + 1 + lane; i < p; i += 32) {
+          const double v = col[i];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) s[u] += v * c4[u][i];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) s[u] = (warp_sum(s[u]) + c4[u][k]) * t;
       }
-      double s2 = 0.0;
+      __syncwarp();
       for (int i = k + 1 + lane; i < p; i += 32) {
-        const double v = cj[i] - s * col[i];
-        cj[i] = v;
-        s2 += v * v;
+        const double v = col[i];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (jb + u >= q) continue;
+          const double x = c4[u][i] - s[u] * v;
+          c4[u][i] = x;
+          s2[u] += x * x;
+        }
       }
-      s2 = warp_sum(s2);
-      if (lane == 0) {
-        cj[k] -= s;
-        cn[j] = s2;
-      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) s2[u] = warp_sum(s2[u]);
+      if (lane == 0)
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (jb + u < q) {
+            c4[u][k] -= s[u];
+            cn[jb + u] = s2[u];
+          }
     }
     __syncthreads();
     flops += 6.0 * (p - k) * (q - k);
