@@ -486,7 +486,9 @@ __global__ void __launch_bounds__(kLeafRegThreads) k_leaf_factor_reg(double* __r
     const int k = g + q * G;
     a[q] = (active && q < nk && k < b) ? Dg[(size_t)k * b + i] : 0.0;
   }
-  if (t == 0) atomicAdd(&d_cnt_leaf, (double)b * b * b / 3.0);
+  // pivot bookkeeping stays in thread 0's registers; one set of atomics at the end
+  double minp = INFINITY, failv = 0.0;
+  int nclamp = 0, nneg = 0, failpos = INT_MAX;
   for (int j = 0; j < b; ++j) {
     // owners of column j publish it (q = j / G for group g = j % G)
     if (active && g == j % G) {
@@ -497,29 +499,29 @@ __global__ void __launch_bounds__(kLeafRegThreads) k_leaf_factor_reg(double* __r
     __syncthreads();
     if (t == 0) {
       double s = col[j];
-      atomic_min_double(&st->min_pivot, s);
+      minp = fmin(minp, s);
       bool failed;
       if (ldl) {
         failed = (s == 0.0);
         if (s < 0.0) {
           if (-s <= clamp_tol) {
             s = clamp_tol;
-            atomicAdd(&st->clamped, 1);
+            ++nclamp;
           } else {
-            atomicAdd(&st->negative, 1);
+            ++nneg;
           }
         }
-        d[base + j] = s;
       } else {
         failed = !(s > 0.0);
       }
-      if (failed) {
-        const int pos = base + j;
-        if (atomicMin(&st->fail_pos, pos) > pos) st->fail_val = s;
+      if (failed && failpos == INT_MAX) {
+        failpos = base + j;
+        failv = s;
       }
       s_piv = s;
     }
     __syncthreads();
+    if (ldl && t == 32) d[base + j] = s_piv;
     const double s = s_piv;
     if (active && i > j) {
       const double ci = col[i] / s;
@@ -542,6 +544,13 @@ __global__ void __launch_bounds__(kLeafRegThreads) k_leaf_factor_reg(double* __r
   for (int q = 0; q < kLeafRegMaxK; ++q) {
     const int k = g + q * G;
     if (active && q < nk && k < b) Dg[(size_t)k * b + i] = (i < k) ? 0.0 : a[q];
+  }
+  if (t == 0) {
+    atomicAdd(&d_cnt_leaf, (double)b * b * b / 3.0);
+    atomic_min_double(&st->min_pivot, minp);
+    if (nclamp) atomicAdd(&st->clamped, nclamp);
+    if (nneg) atomicAdd(&st->negative, nneg);
+    if (failpos != INT_MAX && atomicMin(&st->fail_pos, failpos) > failpos) st->fail_val = failv;
   }
 }
 
