@@ -444,9 +444,7 @@ void assemble(HMat& h, Geometry& g, const MaternDev& p, double eps, bool fixed_r
         for (size_t t = 0; t < c.leaves.size(); ++t) {
           const int k = c.leaves[t];
           woff.push_back(wsd);
-          wsd += c.cap[t] <= 16 ? 0
-                 : trunc_use_cluster(mm[k], nn[k]) ? trunc_ws_doubles_cluster(mm[k], nn[k], c.cap[t])
-                                                   : trunc_ws_doubles(mm[k], nn[k], c.cap[t]);
+          wsd += c.cap[t] <= 16 ? 0 : trunc_ws_for(mm[k], nn[k], c.cap[t]);
         }
         c.ws = dmalloc<double>(wsd);
         std::vector<TruncItem> ti;
@@ -465,8 +463,21 @@ void assemble(HMat& h, Geometry& g, const MaternDev& p, double eps, bool fixed_r
           x.ws = c.ws + woff[t];
           ti.push_back(x);
         }
-        std::vector<TruncItem> tbig, tsmall;
-        for (const TruncItem& x : ti) (trunc_use_cluster(x.m, x.n) ? tbig : tsmall).push_back(x);
+        std::vector<TruncItem> tbig, tsmall, tmid;
+        for (const TruncItem& x : ti) {
+          const int rt = trunc_route(x.m, x.n, x.rcap);
+          (rt == 2 ? tbig : rt == 1 ? tmid : tsmall).push_back(x);
+        }
+        if (!tmid.empty()) {  // medium blocks: one CTA pair each
+          TruncItem* d_tm = upload(tmid, st);
+          std::vector<int> off(tmid.size() + 1);
+          for (size_t q = 0; q <= tmid.size(); ++q) off[q] = (int)q;
+          int* d_off = upload(off, st);
+          launch_truncate_pair(d_tm, d_off, (int)tmid.size(), eps, d_err, st);
+          HMGP_CUDA(cudaStreamSynchronize(st));
+          cudaFree(d_tm);
+          cudaFree(d_off);
+        }
         if (!tbig.empty()) {  // large blocks: one 8-CTA cluster each
           TruncItem* d_tb = upload(tbig, st);
           std::vector<int> off(tbig.size() + 1);

@@ -187,6 +187,7 @@ struct Engine {
   }
   void stats_begin() {
     if (stats_on) {
+      truncate_hist_enable(true);
       cudaEventCreate(&st_prev);
       cudaEventRecord(st_prev, st);
     }
@@ -217,18 +218,35 @@ struct Engine {
   }
   void lrupd(std::vector<TruncItem>& v0) {
     if (v0.empty()) return;
-    // large blocks -> one 8-CTA cluster each; the rest -> one CTA each
-    std::vector<TruncItem> v, big;
-    for (const TruncItem& t : v0) (t.cond != 4 && trunc_use_cluster(t.m, t.n) ? big : v).push_back(t);
+    // large blocks -> one 8-CTA cluster each, medium -> one CTA pair each, the
+    // rest -> one CTA each
+    std::vector<TruncItem> v, big, mid;
+    for (const TruncItem& t : v0) {
+      const int rt = t.cond == 4 ? 0 : trunc_route(t.m, t.n, t.rcap);
+      (rt == 2 ? big : rt == 1 ? mid : v).push_back(t);
+    }
     v0.clear();
-    if (!big.empty()) {
-      std::vector<int> off(big.size() + 1);
-      for (size_t i = 0; i <= big.size(); ++i) off[i] = (int)i;
-      launch_truncate_cluster(sg.put(big), sg.put(off), (int)big.size(), eps, d_err, st);
-      stat(S_TRUNC, big.size());
+    for (int pass = 0; pass < 2; ++pass) {
+      std::vector<TruncItem>& grp = pass ? mid : big;
+      if (grp.empty()) continue;
+      std::vector<int> off(grp.size() + 1);
+      for (size_t i = 0; i <= grp.size(); ++i) off[i] = (int)i;
+      if (pass)
+        launch_truncate_pair(sg.put(grp), sg.put(off), (int)grp.size(), eps, d_err, st);
+      else
+        launch_truncate_cluster(sg.put(grp), sg.put(off), (int)grp.size(), eps, d_err, st);
+      st_next = {};
+      for (const TruncItem& t : grp) {
+        st_next[0] = std::min(st_next[0], -t.m);
+        st_next[1] = std::max(st_next[1], t.n);
+      }
+      st_next[2] = (int)grp.size();
+      st_next[3] = 1;
+      stat(S_TRUNC, grp.size());
     }
     if (v.empty()) return;
     int sw = 0, smn = 0;
+    st_next = {};
     for (const TruncItem& t : v) {
       if (t.cond != 4) trunc_smem_dims(t.m, t.n, &sw, &smn);
       if (stats_on) note_dims(t.m, t.n, (int)v.size(), 1);
@@ -251,6 +269,7 @@ struct Engine {
       if (pe.first == S_TRUNC) tr.push_back({t, i});
       prev = pe.second;
     }
+    truncate_hist_print();
     std::sort(tr.begin(), tr.end(), [](auto& a, auto& b) { return a.first > b.first; });
     for (size_t q = 0; q < tr.size() && q < 12; ++q) {
       const auto& m = st_meta[tr[q].second];
@@ -258,17 +277,27 @@ struct Engine {
               tr[q].first, m[0], m[1], m[2], m[3]);
     }
     // histogram of lrupd time by max(m, n)
-    std::map<int, std::pair<double, int>> hist;
+    // (cluster launches carry a negative m)
+    std::map<int, std::pair<double, int>> hist, shist;
     for (const auto& x : tr) {
       const auto& m = st_meta[x.second];
       int b = 1;
-      while (b < std::max(m[0], m[1])) b <<= 1;
-      hist[b].first += x.first;
-      hist[b].second += 1;
+      while (b < std::max(std::abs(m[0]), m[1])) b <<= 1;
+      auto& h = hist[m[0] < 0 ? -b : b];
+      h.first += x.first;
+      h.second += 1;
+      int s = 1;
+      while (s < m[3]) s <<= 1;
+      auto& hs = shist[m[0] < 0 ? -s : s];
+      hs.first += x.first;
+      hs.second += 1;
     }
     for (const auto& h : hist)
-      fprintf(stderr, "[hmgp]   lrupd max-dim <= %6d: %6d launches %9.1f ms\n", h.first, h.second.second,
-              h.second.first);
+      fprintf(stderr, "[hmgp]   lrupd %s max-dim <= %6d: %6d launches %9.1f ms\n",
+              h.first < 0 ? "cluster" : "cta    ", std::abs(h.first), h.second.second, h.second.first);
+    for (const auto& h : shist)
+      fprintf(stderr, "[hmgp]   lrupd %s longest seq <= %5d: %6d launches %9.1f ms\n",
+              h.first < 0 ? "cluster" : "cta    ", std::abs(h.first), h.second.second, h.second.first);
     for (int k = 0; k < S_N; ++k)
       fprintf(stderr, "[hmgp] %-10s launches %9lld items %10lld (%.1f/launch) %10.1f ms\n", nm[k],
               st_launch[k], st_items[k], st_launch[k] ? (double)st_items[k] / st_launch[k] : 0.0,
@@ -323,8 +352,7 @@ struct Engine {
   void lrupd_ws(std::vector<TruncItem>& v) {
     for (auto& t : v) {
       if (t.cond == 4) continue;
-      t.ws = ar.dbl(trunc_use_cluster(t.m, t.n) ? trunc_ws_doubles_cluster(t.m, t.n, t.rcap)
-                                                : trunc_ws_doubles(t.m, t.n, t.rcap));
+      t.ws = ar.dbl(trunc_ws_for(t.m, t.n, t.rcap));
     }
     lrupd(v);
   }
@@ -673,9 +701,16 @@ struct Engine {
     const size_t mk = ar.mark();
     std::vector<GemmItem> g;
     std::vector<int> goff{0};
-    std::vector<TruncItem> t, tb;
-    std::vector<int> toff{0}, tboff{0};
+    std::vector<TruncItem> t, tb, tp;
+    std::vector<int> toff{0}, tboff{0}, tpoff{0};
     int sw = 0, smn = 0;
+    std::array<int, 4> meta_t{}, meta_b{}, meta_p{};  // stats: max m, max n, targets, longest seq
+    auto meta = [](std::array<int, 4>& mt, int m, int n, int seq) {
+      mt[0] = std::max(mt[0], m);
+      mt[1] = std::max(mt[1], n);
+      ++mt[2];
+      mt[3] = std::max(mt[3], seq);
+    };
     for (const auto& v : seq) {
       const int c = flat[v[0]].c;
       const LeafDev& l = LF(c);
@@ -700,10 +735,9 @@ struct Engine {
       } else {  // hblock.cpp:185-203
         int rcap = 0;
         for (int i : v) rcap = std::max(rcap, l.cap + flat[i].p.cols.v);
-        const bool clu = trunc_use_cluster(l.m, l.n);
-        double* ws = ar.dbl(clu ? trunc_ws_doubles_cluster(l.m, l.n, rcap)
-                                : trunc_ws_doubles(l.m, l.n, rcap));
-        std::vector<TruncItem>& dst = clu ? tb : t;
+        const int rt = trunc_route(l.m, l.n, rcap);
+        double* ws = ar.dbl(trunc_ws_for(l.m, l.n, rcap));
+        std::vector<TruncItem>& dst = rt == 2 ? tb : rt == 1 ? tp : t;
         for (int i : v) {
           const Add& a = flat[i];
           TruncItem ti = lritem(l.a, l.b, l.m, l.n, rankp(c), compp(c), 2, l.cap, &a.p, &a.q,
@@ -711,11 +745,15 @@ struct Engine {
           ti.ws = ws;
           dst.push_back(ti);
         }
-        if (clu) {
+        if (rt == 2) {
           tboff.push_back((int)tb.size());
+          meta(meta_b, l.m, l.n, (int)v.size());
+        } else if (rt == 1) {
+          tpoff.push_back((int)tp.size());
+          meta(meta_p, l.m, l.n, (int)v.size());
         } else {
           toff.push_back((int)t.size());
-          if (stats_on) note_dims(l.m, l.n, (int)seq.size(), (int)v.size());
+          meta(meta_t, l.m, l.n, (int)v.size());
           trunc_smem_dims(l.m, l.n, &sw, &smn);
         }
       }
@@ -726,10 +764,19 @@ struct Engine {
     }
     if (!tb.empty()) {
       launch_truncate_cluster(sg.put(tb), sg.put(tboff), (int)tboff.size() - 1, eps, d_err, st);
+      st_next = meta_b;
+      st_next[0] = -st_next[0];  // negative m marks a cluster launch
       stat(S_TRUNC, tb.size());
+    }
+    if (!tp.empty()) {
+      launch_truncate_pair(sg.put(tp), sg.put(tpoff), (int)tpoff.size() - 1, eps, d_err, st);
+      st_next = meta_p;
+      st_next[0] = -st_next[0];
+      stat(S_TRUNC, tp.size());
     }
     if (!t.empty()) {
       launch_truncate_seq(sg.put(t), sg.put(toff), (int)toff.size() - 1, eps, d_err, st, sw, smn);
+      st_next = meta_t;
       stat(S_TRUNC, t.size());
     }
     ar.release(mk);

@@ -136,6 +136,16 @@ bool trunc_use_cluster(int m, int n);
 size_t trunc_ws_doubles_cluster(int m, int n, int rcap);
 void launch_truncate_cluster(const TruncItem* d_items, const int* d_off, int targets, double eps,
                              int* d_err, cudaStream_t st);
+// medium blocks: one CTA pair (U side, V side) per target sequence, factors in smem
+bool trunc_use_pair(int m, int n, int rcap);
+size_t trunc_ws_doubles_pair(int m, int n, int rcap);
+void launch_truncate_pair(const TruncItem* d_items, const int* d_off, int targets, double eps,
+                          int* d_err, cudaStream_t st);
+// 0 single CTA (small), 1 CTA pair, 2 8-CTA cluster; workspace for that route
+int trunc_route(int m, int n, int rcap);
+size_t trunc_ws_for(int m, int n, int rcap);
+void truncate_hist_enable(bool on);
+void truncate_hist_print();
 // per-target ordered sequences: CTA b runs items[off[b]..off[b+1]) in order
 void launch_truncate_seq(const TruncItem* d_items, const int* d_off, int targets, double eps,
                          int* d_err, cudaStream_t st, int smem_w, int smem_mn);

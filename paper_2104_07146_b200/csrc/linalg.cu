@@ -466,20 +466,23 @@ __global__ void k_leaf_factor(double* __restrict__ Dg, int b, int base, int ldl,
 // registers.  Column j is exchanged through shared memory once per step; the
 // update A(i,k) -= c_i c_k / s is the same for LDL (l = c/s, d = s) and
 // Cholesky (l = c/sqrt(s)).  Two barriers per column.
+// BMAX (32, 64 or 128) is a compile-time bound on b so every register slot and
+// shared-memory offset is static.
 constexpr int kLeafRegThreads = 1024;
-constexpr int kLeafRegMaxK = 16;  // columns per thread for b = 128
+template <int BMAX>
 __global__ void __launch_bounds__(kLeafRegThreads) k_leaf_factor_reg(double* __restrict__ Dg, int b,
                                                                      int base, int ldl,
                                                                      double* __restrict__ d,
                                                                      double clamp_tol,
                                                                      LeafFactorStatus* st) {
-  __shared__ double col[128];
+  constexpr int G = kLeafRegThreads / BMAX;
+  constexpr int kLeafRegMaxK = BMAX / G;  // columns per thread
+  __shared__ double col[BMAX];
   __shared__ double s_piv;
-  const int G = kLeafRegThreads / b;
   const int t = threadIdx.x;
-  const bool active = t < G * b;
-  const int i = t % b, g = t / b;
-  const int nk = (b + G - 1) / G;
+  const int i = t % BMAX, g = t / BMAX;
+  const bool active = i < b;
+  constexpr int nk = kLeafRegMaxK;
   double a[kLeafRegMaxK];
 #pragma unroll
   for (int q = 0; q < kLeafRegMaxK; ++q) {
@@ -490,12 +493,14 @@ __global__ void __launch_bounds__(kLeafRegThreads) k_leaf_factor_reg(double* __r
   double minp = INFINITY, failv = 0.0;
   int nclamp = 0, nneg = 0, failpos = INT_MAX;
   for (int j = 0; j < b; ++j) {
-    // owners of column j publish it (q = j / G for group g = j % G)
-    if (active && g == j % G) {
+    // owners of column j (group g = j % G, slot qj = j / G) publish it
+    const int qj = j / G;
+    const bool own = active && g == j % G;
+    double aj = 0.0;
 #pragma unroll
-      for (int q = 0; q < kLeafRegMaxK; ++q)
-        if (q == j / G) col[i] = a[q];
-    }
+    for (int q = 0; q < kLeafRegMaxK; ++q)
+      if (q == qj) aj = a[q];
+    if (own) col[i] = aj;
     __syncthreads();
     if (t == 0) {
       double s = col[j];
@@ -523,20 +528,22 @@ __global__ void __launch_bounds__(kLeafRegThreads) k_leaf_factor_reg(double* __r
     __syncthreads();
     if (ldl && t == 32) d[base + j] = s_piv;
     const double s = s_piv;
+    // trailing update of the columns k > j this thread owns (rows i > j only are
+    // ever read again, so the strict upper part may hold stale values)
     if (active && i > j) {
       const double ci = col[i] / s;
-#pragma unroll
-      for (int q = 0; q < kLeafRegMaxK; ++q) {
-        const int k = g + q * G;
-        if (q < nk && k > j && k <= i) a[q] -= ci * col[k];
-      }
-    }
-    // finalize column j in its owners' registers
-    if (active && g == j % G) {
-      const double piv = ldl ? s : sqrt(s);
+      const int qmin = j >= g ? (j - g) / G + 1 : 0;  // first q with g + q*G > j
 #pragma unroll
       for (int q = 0; q < kLeafRegMaxK; ++q)
-        if (q == j / G) a[q] = (i == j) ? (ldl ? 1.0 : piv) : (i > j ? a[q] / piv : 0.0);
+        if (q >= qmin) a[q] -= ci * col[g + q * G];
+    }
+    // finalize column j in its owners' registers
+    if (own) {
+      const double piv = ldl ? s : sqrt(s);
+      const double v = (i == j) ? (ldl ? 1.0 : piv) : (i > j ? aj / piv : 0.0);
+#pragma unroll
+      for (int q = 0; q < kLeafRegMaxK; ++q)
+        if (q == qj) a[q] = v;
     }
     __syncthreads();
   }
@@ -556,8 +563,13 @@ __global__ void __launch_bounds__(kLeafRegThreads) k_leaf_factor_reg(double* __r
 
 void launch_leaf_factor(double* D, int b, int base, int ldl, double* d, double clamp_tol,
                         LeafFactorStatus* status, cudaStream_t st) {
-  if (b <= 128 && (b + (kLeafRegThreads / b) - 1) / (kLeafRegThreads / b) <= kLeafRegMaxK) {
-    k_leaf_factor_reg<<<1, kLeafRegThreads, 0, st>>>(D, b, base, ldl, d, clamp_tol, status);
+  if (b <= 128) {
+    if (b <= 32)
+      k_leaf_factor_reg<32><<<1, kLeafRegThreads, 0, st>>>(D, b, base, ldl, d, clamp_tol, status);
+    else if (b <= 64)
+      k_leaf_factor_reg<64><<<1, kLeafRegThreads, 0, st>>>(D, b, base, ldl, d, clamp_tol, status);
+    else
+      k_leaf_factor_reg<128><<<1, kLeafRegThreads, 0, st>>>(D, b, base, ldl, d, clamp_tol, status);
     HMGP_LAUNCH_CHECK();
     return;
   }

@@ -28,6 +28,60 @@ constexpr int kMaxSmemMN = 1024;       // m + n bound of the staged column chunk
 
 __device__ double d_cnt_trunc, d_cnt_titems;
 
+// (stats mode) per-path histogram of recompressions by max(m, n) and column
+// count r: item count and summed SM cycles.  path 0 small (W in smem), 1 large
+// single CTA, 2 cluster.
+constexpr int kHM = 10, kHR = 10;
+__device__ unsigned long long d_hist_n[4][kHM][kHR], d_hist_cyc[4][kHM][kHR];
+__device__ int d_hist_on;
+__device__ __forceinline__ int hbucket(int v) {
+  int b = 0;
+  while (b < kHM - 1 && (16 << b) < v) ++b;
+  return b;
+}
+__device__ __forceinline__ void hist_add(int path, int m, int n, int r, long long t0) {
+  if (!d_hist_on || threadIdx.x != 0) return;
+  const int bm = hbucket(max(m, n)), br = min(hbucket(r), kHR - 1);
+  atomicAdd(&d_hist_n[path][bm][br], 1ull);
+  atomicAdd(&d_hist_cyc[path][bm][br], (unsigned long long)(clock64() - t0));
+}
+// (stats mode) per-stage SM cycles of the single-CTA paths: [path][stage]
+// stages: 0 stage-in / W formation, 1 Householder QR of the factors, 2 RRQR of
+// the core, 3 Jacobi, 4 Q application / write-back; d_stage_sweeps counts sweeps
+__device__ unsigned long long d_stage_cyc[3][5], d_stage_sweeps[3], d_stage_jac[3];
+__device__ __forceinline__ void stage_add(int path, int st, long long& t) {
+  if (!d_hist_on || threadIdx.x != 0) return;
+  const long long now = clock64();
+  atomicAdd(&d_stage_cyc[path][st], (unsigned long long)(now - t));
+  t = now;
+}
+void truncate_hist_enable(bool on) {
+  const int v = on ? 1 : 0;
+  HMGP_CUDA(cudaMemcpyToSymbol(d_hist_on, &v, 4));
+}
+void truncate_hist_print() {
+  static unsigned long long hn[4][kHM][kHR], hc[4][kHM][kHR];
+  HMGP_CUDA(cudaMemcpyFromSymbol(hn, d_hist_n, sizeof(hn)));
+  HMGP_CUDA(cudaMemcpyFromSymbol(hc, d_hist_cyc, sizeof(hc)));
+  static unsigned long long sc[3][5], sw[3], sj[3];
+  HMGP_CUDA(cudaMemcpyFromSymbol(sc, d_stage_cyc, sizeof(sc)));
+  HMGP_CUDA(cudaMemcpyFromSymbol(sw, d_stage_sweeps, sizeof(sw)));
+  HMGP_CUDA(cudaMemcpyFromSymbol(sj, d_stage_jac, sizeof(sj)));
+  for (int p = 0; p < 3; ++p)
+    fprintf(stderr,
+            "[hmgp]   trunc %s stages (s, SM clock): stage-in %.2f qr %.2f rrqr %.2f jacobi %.2f apply %.2f;"
+            " jacobi calls %llu, sweeps/call %.2f\n",
+            p == 2 ? "pair" : p ? "large" : "small", sc[p][0] / 1.9e9, sc[p][1] / 1.9e9, sc[p][2] / 1.9e9, sc[p][3] / 1.9e9,
+            sc[p][4] / 1.9e9, sj[p], sj[p] ? (double)sw[p] / sj[p] : 0.0);
+  static const char* nm[4] = {"small", "large", "cluster", "pair"};
+  for (int p = 0; p < 4; ++p)
+    for (int a = 0; a < kHM; ++a)
+      for (int b = 0; b < kHR; ++b)
+        if (hn[p][a][b])
+          fprintf(stderr, "[hmgp]   trunc %-7s max(m,n)<=%6d r<=%5d: %8llu items, %8.1f us/item (SM clock)\n",
+                  nm[p], 16 << a, 16 << b, hn[p][a][b], hc[p][a][b] / (double)hn[p][a][b] / 1.9e3);
+}
+
 void truncate_counters_read_reset(double* flops, double* items) {
   double z = 0.0;
   HMGP_CUDA(cudaMemcpyFromSymbol(flops, d_cnt_trunc, 8));
@@ -138,11 +192,14 @@ __device__ void cta_apply_q(const double* QR, int m, int kq, const double* tau, 
 
 // One-sided Jacobi on W (p x q, ld p, p >= q); J (q x q) accumulates rotations.
 // Returns the algorithmic flops (6p per pair inspected, 6(p+q) per rotation).
-__device__ double cta_jacobi(double* W, int p, int q, double* J) {
+__device__ double cta_jacobi(double* W, int p, int q, double* J, int* sweeps_out = nullptr) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int idx = threadIdx.x; idx < q * q; idx += blockDim.x) J[idx] = (idx % (q + 1) == 0) ? 1.0 : 0.0;
   __syncthreads();
-  if (q < 2) return 0.0;
+  if (q < 2) {
+    if (sweeps_out && threadIdx.x == 0) *sweeps_out = 0;
+    return 0.0;
+  }
   const int qq = q + (q & 1);
   const int m1 = qq - 1;
   __shared__ int s_rot;
@@ -208,6 +265,7 @@ __device__ double cta_jacobi(double* W, int p, int q, double* J) {
     __syncthreads();
     if (!rot) break;
   }
+  if (sweeps_out && threadIdx.x == 0) *sweeps_out = sweeps;
   return (double)sweeps * (0.5 * q * (q - 1)) * 6.0 * p + (double)s_nrot * 6.0 * (p + q);
 }
 
@@ -225,7 +283,8 @@ struct RS {
 // (unpermuted rows), J (kq x kq) = X, s_sig / s_ord sorted descending and
 // keep = #{sigma_i > eps*sigma_0, sigma_i > 0} (hblock.cpp:151-153).
 __device__ RS cta_rrqr_svd(double* W, int p, int q, double eps, double* tau, int* piv, double* cn,
-                           double* G, double* J, double* s_sig, int* s_ord, double* red) {
+                           double* G, double* J, double* s_sig, int* s_ord, double* red,
+                           int path = 0, long long* tclk = nullptr) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   __shared__ double redv[32];
   __shared__ int redi[32];
@@ -371,13 +430,22 @@ __device__ RS cta_rrqr_svd(double* W, int p, int q, double eps, double* tau, int
     flops += 6.0 * (p - k) * (q - k);
   }
   const int kq = k;
+  if (tclk) stage_add(path, 2, *tclk);
   // G = (R P^T)^T : q x kq, row piv[j] holds R(:, j)
   for (int e = threadIdx.x; e < q * kq; e += blockDim.x) {
     const int j = e % q, i = e / q;
     G[(size_t)i * q + piv[j]] = (j >= i) ? W[(size_t)j * p + i] : 0.0;
   }
   __syncthreads();
-  flops += cta_jacobi(G, q, kq, J);
+  __shared__ int s_sweeps;
+  flops += cta_jacobi(G, q, kq, J, &s_sweeps);
+  if (tclk) {
+    stage_add(path, 3, *tclk);
+    if (d_hist_on && threadIdx.x == 0) {
+      atomicAdd(&d_stage_sweeps[path], (unsigned long long)s_sweeps);
+      atomicAdd(&d_stage_jac[path], 1ull);
+    }
+  }
   for (int c = threadIdx.x; c < kq; c += blockDim.x) {
     const double* gc = G + (size_t)c * q;
     double s = 0.0;
@@ -503,6 +571,7 @@ __device__ void lr_update(const TruncItem& it, double eps, int* err, int smem_w,
     return;
   }
   const int m = it.m, n = it.n;
+  const long long t0 = clock64();
   extern __shared__ double dsm[];
   if ((size_t)m * n <= (size_t)smem_w && m + n <= smem_mn) {
     // ---- small block: W = [U | aP][V | Q]^T explicitly, rank-revealing SVD of W.
@@ -552,7 +621,9 @@ __device__ void lr_update(const TruncItem& it, double eps, int* err, int smem_w,
     double* G = cn + 2 * n;
     const int kqmax = min(min(m, n), it.rcap);  // rank(W) <= r <= rcap
     double* J = G + (size_t)n * kqmax;
-    const RS rs = cta_rrqr_svd(W, m, n, eps, tau, piv, cn, G, J, s_sig, s_ord, red);
+    long long tc = t0;
+    stage_add(0, 0, tc);
+    const RS rs = cta_rrqr_svd(W, m, n, eps, tau, piv, cn, G, J, s_sig, s_ord, red, 0, &tc);
     if (rs.keep > it.cap) {
       if (threadIdx.x == 0) atomicOr(err, 4);
       return;
@@ -568,12 +639,14 @@ __device__ void lr_update(const TruncItem& it, double eps, int* err, int smem_w,
     }
     __syncthreads();
     cta_apply_q(W, m, kq, tau, it.U, keep);
+    stage_add(0, 4, tc);
     if (threadIdx.x == 0) {
       *it.rank = keep;
       if (it.compact) *it.compact = keep;
       atomicAdd(&d_cnt_trunc, 2.0 * m * n * r + rs.flops + 4.0 * keep * (double)m * kq);
       atomicAdd(&d_cnt_titems, 1.0);
     }
+    hist_add(0, m, n, r, t0);
     return;
   }
   // ---- large block: Householder QR of both stacked factors, core R_u R_v^T,
@@ -594,8 +667,11 @@ __device__ void lr_update(const TruncItem& it, double eps, int* err, int smem_w,
     WV[(size_t)(r0 + k) * n + i] = (qi >= 0 && qi < it.qr) ? it.Q[(size_t)k * it.ldq + qi] : 0.0;
   }
   __syncthreads();
+  long long tc = t0;
+  stage_add(1, 0, tc);
   cta_householder(WU, m, r, tu, red);
   cta_householder(WV, n, r, tv, red);
+  stage_add(1, 1, tc);
   const int ku = min(m, r), kv = min(n, r);
   // core(i,j) = sum_{l >= max(i,j)} Ru(i,l) Rv(j,l)  (ku x kv, ld ku)
   for (int idx = threadIdx.x; idx < ku * kv; idx += blockDim.x) {
@@ -612,7 +688,7 @@ __device__ void lr_update(const TruncItem& it, double eps, int* err, int smem_w,
   double* G = cn + 2 * kv;
   double* J = G + (size_t)kv * kqmax;
   double* Uc = J + (size_t)kqmax * kqmax;
-  const RS rs = cta_rrqr_svd(C, ku, kv, eps, tau, piv, cn, G, J, s_sig, s_ord, red);
+  const RS rs = cta_rrqr_svd(C, ku, kv, eps, tau, piv, cn, G, J, s_sig, s_ord, red, 1, &tc);
   if (rs.keep > it.cap) {
     if (threadIdx.x == 0) atomicOr(err, 4);
     return;
@@ -637,6 +713,7 @@ __device__ void lr_update(const TruncItem& it, double eps, int* err, int smem_w,
   __syncthreads();
   cta_apply_q(WU, m, ku, tu, it.U, keep);
   cta_apply_q(WV, n, kv, tv, it.V, keep);
+  stage_add(1, 4, tc);
   if (threadIdx.x == 0) {
     *it.rank = keep;
     if (it.compact) *it.compact = keep;
@@ -645,6 +722,7 @@ __device__ void lr_update(const TruncItem& it, double eps, int* err, int smem_w,
     atomicAdd(&d_cnt_trunc, fl);
     atomicAdd(&d_cnt_titems, 1.0);
   }
+  hist_add(1, m, n, r, t0);
 }
 
 // ===================================================================== //
@@ -817,6 +895,7 @@ __device__ void lr_update_cluster(cg::cluster_group& cl, CluShared& sh, const Tr
     cl.sync();
     return;
   }
+  const long long t0 = clock64();
   double* WU = it.ws;
   double* WV = WU + (size_t)m * it.rcap;
   double* tu = WV + (size_t)n * it.rcap;
@@ -912,6 +991,7 @@ __device__ void lr_update_cluster(cg::cluster_group& cl, CluShared& sh, const Tr
     atomicAdd(&d_cnt_trunc, fl);
     atomicAdd(&d_cnt_titems, 1.0);
   }
+  if (rank == 0) hist_add(2, m, n, r, t0);
   cl.sync();
 }
 
@@ -928,6 +1008,321 @@ __global__ void __cluster_dims__(kClu, 1, 1) __launch_bounds__(kTruncThreads)
       if (cl.block_rank() == 0) lr_post_solve(items[i]);
       cl.sync();
     }
+  }
+}
+
+// ===================================================================== //
+// Medium blocks: a CTA PAIR (cluster of 2) per target.  CTA 0 owns the U side,
+// CTA 1 the V side; each keeps its stacked factor [U | aP] or [V | Q] resident
+// in shared memory, so both Householder QRs run at once with one barrier per
+// column (the next column's tail norm is produced by the update that touches
+// it).  The r x r core R_u R_v^T is formed and decomposed redundantly by both
+// CTAs (identical arithmetic, identical results), and each side applies its Q
+// in compact WY form, I - Y T Y^T, with one pass that writes the new factor to
+// global memory.  Items whose factors do not fit fall back, on device, to the
+// single-CTA global-memory path run by CTA 0.
+// ===================================================================== //
+constexpr int kPairMaxR = 128;
+
+#include "trunc_lean.cuh"
+
+// out (mm x c, ld mm, global) = Q [E0; 0] with Q = H_0 ... H_{k-1} from
+// smem_qr(A) in compact WY form Q = I - Y T Y^T (T upper triangular, the
+// forward column-wise recurrence of dlarft).  E0 is k x c (ld k).  Scratch: S
+// and T (k x k), X (k x c); S may alias X's storage only after T is built, so
+// the caller passes distinct buffers for S/Z and T/X1 pairs as documented.
+__device__ void wy_apply(const double* A, int mm, int lda, int k, const double* tau, const double* E0,
+                         int c, double* out, double* S, double* T, double* X1) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  // S(l, q) = v_l^T v_q for l < q (ld k), four dots per warp in flight
+  const int np = k * (k - 1) / 2;
+  for (int pb = 4 * w; pb < np; pb += 4 * nw) {
+    int ls[4], qs[4];
+    double s[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      int p = min(pb + u, np - 1);
+      // pair index p -> (l, q) with q = floor((1 + sqrt(1 + 8p)) / 2)
+      int q = (int)((1.0 + sqrt(1.0 + 8.0 * p)) * 0.5);
+      while (q * (q - 1) / 2 > p) --q;
+      while ((q + 1) * q / 2 <= p) ++q;
+      ls[u] = p - q * (q - 1) / 2;
+      qs[u] = q;
+      s[u] = 0.0;
+    }
+    int qmin = qs[0];
+#pragma unroll
+    for (int u = 1; u < 4; ++u) qmin = min(qmin, qs[u]);
+    for (int i = qmin + 1 + lane; i < mm; i += 32) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (i > qs[u]) s[u] += A[(size_t)ls[u] * lda + i] * A[(size_t)qs[u] * lda + i];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double v = warp_sum(s[u]);
+      if (lane == 0 && pb + u < np) S[(size_t)qs[u] * k + ls[u]] = v + A[(size_t)ls[u] * lda + qs[u]];
+    }
+  }
+  __syncthreads();
+  // T recurrence: T(q,q) = tau_q, T(0:q, q) = -tau_q T(0:q, 0:q) S(0:q, q)
+  for (int q = 0; q < k; ++q) {
+    const double tq = tau[q];
+    for (int i = threadIdx.x; i < q; i += blockDim.x) {
+      double s = 0.0;
+      for (int l = i; l < q; ++l) s += T[(size_t)l * k + i] * S[(size_t)q * k + l];
+      T[(size_t)q * k + i] = -tq * s;
+    }
+    if (threadIdx.x == 0) T[(size_t)q * k + q] = tq;
+    for (int i = q + 1 + threadIdx.x; i < k; i += blockDim.x) T[(size_t)q * k + i] = 0.0;
+    __syncthreads();
+  }
+  // X1 = Y1^T E0 (Y1 = unit lower k x k top of Y), then Z = T X1 into S's storage
+  for (int e = threadIdx.x; e < k * c; e += blockDim.x) {
+    const int l = e % k, cc = e / k;
+    const double* ec = E0 + (size_t)cc * k;
+    double s = ec[l];
+    for (int i = l + 1; i < k; ++i) s += A[(size_t)l * lda + i] * ec[i];
+    X1[e] = s;
+  }
+  __syncthreads();
+  double* Z = S;
+  for (int e = threadIdx.x; e < k * c; e += blockDim.x) {
+    const int l = e % k, cc = e / k;
+    const double* xc = X1 + (size_t)cc * k;
+    double s = 0.0;
+    for (int j = l; j < k; ++j) s += T[(size_t)j * k + l] * xc[j];
+    Z[e] = s;
+  }
+  __syncthreads();
+  // out(i, cc) = [E0; 0](i, cc) - sum_{l <= min(i, k-1)} Y(i, l) Z(l, cc)
+  for (int e = threadIdx.x; e < mm * c; e += blockDim.x) {
+    const int i = e % mm, cc = e / mm;
+    const double* zc = Z + (size_t)cc * k;
+    double s = (i < k) ? E0[(size_t)cc * k + i] - zc[i] : 0.0;  // Y(i,i) = 1 term
+    const int lmax = min(i, k);
+    for (int l = 0; l < lmax; ++l) s -= A[(size_t)l * lda + i] * zc[l];
+    out[(size_t)cc * mm + i] = s;
+  }
+}
+
+// shared-memory doubles the pair path needs for an m x n target with r columns
+__host__ __device__ __forceinline__ size_t pair_smem_doubles(int m, int n, int r) {
+  return (size_t)(max(m, n) | 1) * r + 4 * (size_t)r * r + 5 * (size_t)r + 8;
+}
+
+__device__ void lr_update_pair(cg::cluster_group& cl, const TruncItem& it, double eps, int* err,
+                               int cap_dbl, double* sm) {
+  const int side = (int)cl.block_rank();  // 0: U side, 1: V side
+  __shared__ double red[32];
+  __shared__ double s_sig[kPairMaxR];
+  __shared__ int s_ord[kPairMaxR];
+  __shared__ double s_tail[2];
+  const int r0 = *it.rank;
+  const int add = it.P ? (it.addp ? *it.addp : it.addv) : 0;
+  const int r = r0 + add;
+  bool go;
+  switch (it.cond) {
+    case 1: go = r > 16; break;
+    case 2: go = r > *it.compact + 16; break;
+    case 3: go = r > 48; break;
+    case 4: go = false; break;
+    default: go = r > 0; break;
+  }
+  cl.sync();  // both CTAs have read rank / compact before either may change them
+  const int m = it.m, n = it.n;
+  const int mm = side ? n : m;
+  double* X = side ? it.V : it.U;
+  if (!go) {
+    if (add > 0 && r > it.cap) {
+      if (side == 0 && threadIdx.x == 0) atomicOr(err, 2);
+      cl.sync();
+      return;
+    }
+    for (size_t e = threadIdx.x; e < (size_t)mm * add; e += blockDim.x) {
+      const int i = (int)(e % mm), k = (int)(e / mm);
+      double v;
+      if (side == 0) {
+        const int pi = i - it.pro;
+        v = (pi >= 0 && pi < it.pr) ? it.alpha * it.P[(size_t)k * it.ldp + pi] : 0.0;
+      } else {
+        const int qi = i - it.qro;
+        v = (qi >= 0 && qi < it.qr) ? it.Q[(size_t)k * it.ldq + qi] : 0.0;
+      }
+      X[(size_t)(r0 + k) * mm + i] = v;
+    }
+    if (side == 0 && threadIdx.x == 0) {
+      *it.rank = r;
+      if (it.cond == 0 && it.compact) *it.compact = r;
+    }
+    cl.sync();
+    return;
+  }
+  if (r > it.rcap) {
+    if (side == 0 && threadIdx.x == 0) atomicOr(err, 1);
+    cl.sync();
+    return;
+  }
+  if (r > kPairMaxR || pair_smem_doubles(m, n, r) > (size_t)cap_dbl || (max(m, n) > 256 && r > 32)) {
+    // single-CTA paths on CTA 0 (W in shared memory when it fits, else global)
+    if (side == 0) lr_update(it, eps, err, kMaxSmemW, kMaxSmemMN);
+    cl.sync();
+    return;
+  }
+  const long long t0 = clock64();
+  const int ku = min(m, r), kv = min(n, r);
+  const int kme = side ? kv : ku, ko = side ? ku : kv, mo = side ? m : n;
+  const int lda = mm | 1, ldo = mo | 1;    // odd strides: conflict-free row-varying access
+  double* A = sm;                          // mm x r (ld lda)
+  double* Ro = A + (size_t)lda * r;        // other side's R (ko x r), later G, later X1
+  double* C = Ro + (size_t)r * r;          // core ku x kv, later T
+  double* J = C + (size_t)r * r;           // kq x kq, later S / Z
+  double* E0 = J + (size_t)r * r;          // kme x keep
+  double* tau = E0 + (size_t)r * r;        // r
+  double* tau_c = tau + r;                 // r
+  double* cn = tau_c + r;                  // 2r (double-buffered trailing norms)
+  int* phys = reinterpret_cast<int*>(cn + 2 * r);  // r ints: core pivot order
+  int* stepof = phys + r;                          // r ints
+  // stage [X | added] (mm x r)
+  for (size_t e = threadIdx.x; e < (size_t)mm * r; e += blockDim.x) {
+    const int i = (int)(e % mm), l = (int)(e / mm);
+    double v;
+    if (l < r0) {
+      v = X[e];
+    } else if (side == 0) {
+      const int pi = i - it.pro;
+      v = (pi >= 0 && pi < it.pr) ? it.alpha * it.P[(size_t)(l - r0) * it.ldp + pi] : 0.0;
+    } else {
+      const int qi = i - it.qro;
+      v = (qi >= 0 && qi < it.qr) ? it.Q[(size_t)(l - r0) * it.ldq + qi] : 0.0;
+    }
+    A[(size_t)l * lda + i] = v;
+  }
+  __syncthreads();
+  long long tc = t0;
+  stage_add(2, 0, tc);
+  {
+    __shared__ double s_vbuf[2 * 512];
+    __shared__ double s_sbuf[2];
+    if (!reg_qr_any(A, mm, lda, r, tau, s_vbuf, s_sbuf)) smem_qr(A, mm, lda, r, tau, s_tail);
+  }
+  stage_add(2, 1, tc);
+  cl.sync();
+  {  // other side's R through distributed shared memory
+    const double* Aot = cl.map_shared_rank(A, side ^ 1);
+    for (int e = threadIdx.x; e < ko * r; e += blockDim.x) {
+      const int i = e % ko, l = e / ko;
+      Ro[e] = (i <= l) ? Aot[(size_t)l * ldo + i] : 0.0;
+    }
+  }
+  __syncthreads();
+  // core(i,j) = sum_{l >= max(i,j)} Ru(i,l) Rv(j,l)  (ku x kv, ld ku)
+  {
+    const double* Ru = side ? Ro : A;
+    const double* Rv = side ? A : Ro;
+    const int ldu = side ? ku : lda, ldv = side ? lda : kv;
+    for (int idx = threadIdx.x; idx < ku * kv; idx += blockDim.x) {
+      const int i = idx % ku, j = idx / ku;
+      double s = 0.0;
+      for (int l = max(i, j); l < r; ++l) s += Ru[(size_t)l * ldu + i] * Rv[(size_t)l * ldv + j];
+      C[(size_t)j * ku + i] = s;
+    }
+  }
+  __syncthreads();
+  const RS rs = cta_rrqr_svd2(C, ku, kv, eps, tau_c, phys, cn, stepof, Ro, J, s_sig, s_ord, 2, &tc);
+  const int keep = rs.keep, kq = rs.kq;
+  if (keep > it.cap) {
+    if (side == 0 && threadIdx.x == 0) atomicOr(err, 4);
+    cl.sync();
+    return;
+  }
+  if (side == 0) {  // U_core = Q_core [J S; 0] (ku x keep)
+    for (int idx = threadIdx.x; idx < ku * keep; idx += blockDim.x) {
+      const int i = idx % ku, c = idx / ku, src = s_ord[c];
+      E0[idx] = i < kq ? J[(size_t)src * kq + i] * s_sig[src] : 0.0;
+    }
+    __syncthreads();
+    cta_apply_q_map(C, ku, ku, kq, tau_c, phys, E0, keep);
+  } else {  // Y (kv x keep)
+    for (int idx = threadIdx.x; idx < kv * keep; idx += blockDim.x) {
+      const int i = idx % kv, c = idx / kv, src = s_ord[c];
+      E0[idx] = Ro[(size_t)src * kv + i] / s_sig[src];
+    }
+  }
+  __syncthreads();
+  wy_apply(A, mm, lda, kme, tau, E0, keep, X, J, C, Ro);
+  stage_add(2, 4, tc);
+  cl.sync();
+  if (side == 0 && threadIdx.x == 0) {
+    *it.rank = keep;
+    if (it.compact) *it.compact = keep;
+    const double fl = qr_flops(m, r) + qr_flops(n, r) + (double)ku * kv * r + rs.flops +
+                      4.0 * keep * ((double)m * ku + (double)n * kv + (double)ku * kq);
+    atomicAdd(&d_cnt_trunc, fl);
+    atomicAdd(&d_cnt_titems, 1.0);
+  }
+  if (side == 0) hist_add(3, m, n, r, t0);
+  cl.sync();
+}
+
+// cluster b (CTA pair 2b, 2b+1) runs target b's sequence in order
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTruncThreads)
+    k_truncate_pair(const TruncItem* __restrict__ items, const int* __restrict__ off, double eps,
+                    int* err, int cap_dbl) {
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ double psm[];
+  const int b = blockIdx.x / 2;
+  for (int i = off[b]; i < off[b + 1]; ++i) {
+    const TruncItem& it = items[i];
+    lr_update_pair(cl, it, eps, err, cap_dbl, psm);
+    if (it.post_L) {
+      if (cl.block_rank() == 1) lr_post_solve(it);
+      cl.sync();
+    }
+  }
+}
+
+static int g_pair_cap = -1;
+static size_t g_pair_bytes = 0;
+void launch_truncate_pair(const TruncItem* d_items, const int* d_off, int targets, double eps,
+                          int* d_err, cudaStream_t st) {
+  if (targets <= 0) return;
+  if (g_pair_cap < 0) {
+    cudaFuncAttributes fa;
+    HMGP_CUDA(cudaFuncGetAttributes(&fa, k_truncate_pair));
+    int dev = 0, optin = 0;
+    HMGP_CUDA(cudaGetDevice(&dev));
+    HMGP_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    g_pair_bytes = (size_t)optin - fa.sharedSizeBytes - 1024;
+    HMGP_CUDA(cudaFuncSetAttribute(k_truncate_pair, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)g_pair_bytes));
+    g_pair_cap = (int)(g_pair_bytes / 8);
+  }
+  k_truncate_pair<<<targets * 2, kTruncThreads, g_pair_bytes, st>>>(d_items, d_off, eps, d_err,
+                                                                   g_pair_cap);
+  HMGP_LAUNCH_CHECK();
+}
+
+size_t trunc_ws_doubles_pair(int m, int n, int rcap) {  // the global-memory fallback
+  const size_t rc = (size_t)rcap, kq = std::min((size_t)std::min(m, n), rc);
+  return (size_t)(m + n) * rc + 5 * rc + rc * rc + 2 * rc * kq + kq * kq;
+}
+
+bool trunc_use_pair(int m, int n, int rcap) {
+  if ((size_t)m * n <= (size_t)kMaxSmemW / 4) return false;
+  const int mx = std::max(m, n);
+  return mx <= 256 || (mx <= 512 && rcap <= 32);
+}
+
+int trunc_route(int m, int n, int rcap) {
+  return trunc_use_pair(m, n, rcap) ? 1 : trunc_use_cluster(m, n) ? 2 : 0;
+}
+
+size_t trunc_ws_for(int m, int n, int rcap) {
+  switch (trunc_route(m, n, rcap)) {
+    case 2: return trunc_ws_doubles_cluster(m, n, rcap);
+    case 1: return trunc_ws_doubles_pair(m, n, rcap);
+    default: return trunc_ws_doubles(m, n, rcap);
   }
 }
 
