@@ -463,17 +463,19 @@ void assemble(HMat& h, Geometry& g, const MaternDev& p, double eps, bool fixed_r
           x.ws = c.ws + woff[t];
           ti.push_back(x);
         }
-        std::vector<TruncItem> tbig, tsmall, tmid;
+        std::vector<TruncItem> tbig, tsmall, tmid, tdef;
         for (const TruncItem& x : ti) {
           const int rt = trunc_route(x.m, x.n, x.rcap);
-          (rt == 2 ? tbig : rt == 1 ? tmid : tsmall).push_back(x);
+          (rt == 2 ? tbig : rt == 1 ? tmid : rt == 3 ? tdef : tsmall).push_back(x);
         }
-        if (!tmid.empty()) {  // medium blocks: one CTA pair each
-          TruncItem* d_tm = upload(tmid, st);
-          std::vector<int> off(tmid.size() + 1);
-          for (size_t q = 0; q <= tmid.size(); ++q) off[q] = (int)q;
+        for (int pass = 0; pass < 2; ++pass) {  // medium blocks: one CTA pair each
+          std::vector<TruncItem>& tm = pass ? tdef : tmid;
+          if (tm.empty()) continue;
+          TruncItem* d_tm = upload(tm, st);
+          std::vector<int> off(tm.size() + 1);
+          for (size_t q = 0; q <= tm.size(); ++q) off[q] = (int)q;
           int* d_off = upload(off, st);
-          launch_truncate_pair(d_tm, d_off, (int)tmid.size(), eps, d_err, st);
+          launch_truncate_pair(d_tm, d_off, (int)tm.size(), eps, d_err, st, pass == 1);
           HMGP_CUDA(cudaStreamSynchronize(st));
           cudaFree(d_tm);
           cudaFree(d_off);

@@ -220,19 +220,19 @@ struct Engine {
     if (v0.empty()) return;
     // large blocks -> one 8-CTA cluster each, medium -> one CTA pair each, the
     // rest -> one CTA each
-    std::vector<TruncItem> v, big, mid;
+    std::vector<TruncItem> v, big, mid, dfr;
     for (const TruncItem& t : v0) {
       const int rt = t.cond == 4 ? 0 : trunc_route(t.m, t.n, t.rcap);
-      (rt == 2 ? big : rt == 1 ? mid : v).push_back(t);
+      (rt == 2 ? big : rt == 1 ? mid : rt == 3 ? dfr : v).push_back(t);
     }
     v0.clear();
-    for (int pass = 0; pass < 2; ++pass) {
-      std::vector<TruncItem>& grp = pass ? mid : big;
+    for (int pass = 0; pass < 3; ++pass) {
+      std::vector<TruncItem>& grp = pass == 2 ? dfr : pass ? mid : big;
       if (grp.empty()) continue;
       std::vector<int> off(grp.size() + 1);
       for (size_t i = 0; i <= grp.size(); ++i) off[i] = (int)i;
       if (pass)
-        launch_truncate_pair(sg.put(grp), sg.put(off), (int)grp.size(), eps, d_err, st);
+        launch_truncate_pair(sg.put(grp), sg.put(off), (int)grp.size(), eps, d_err, st, pass == 2);
       else
         launch_truncate_cluster(sg.put(grp), sg.put(off), (int)grp.size(), eps, d_err, st);
       st_next = {};
@@ -701,10 +701,10 @@ struct Engine {
     const size_t mk = ar.mark();
     std::vector<GemmItem> g;
     std::vector<int> goff{0};
-    std::vector<TruncItem> t, tb, tp;
-    std::vector<int> toff{0}, tboff{0}, tpoff{0};
+    std::vector<TruncItem> t, tb, tp, td;
+    std::vector<int> toff{0}, tboff{0}, tpoff{0}, tdoff{0};
     int sw = 0, smn = 0;
-    std::array<int, 4> meta_t{}, meta_b{}, meta_p{};  // stats: max m, max n, targets, longest seq
+    std::array<int, 4> meta_t{}, meta_b{}, meta_p{}, meta_d{};  // stats: max m, max n, targets, longest seq
     auto meta = [](std::array<int, 4>& mt, int m, int n, int seq) {
       mt[0] = std::max(mt[0], m);
       mt[1] = std::max(mt[1], n);
@@ -737,7 +737,7 @@ struct Engine {
         for (int i : v) rcap = std::max(rcap, l.cap + flat[i].p.cols.v);
         const int rt = trunc_route(l.m, l.n, rcap);
         double* ws = ar.dbl(trunc_ws_for(l.m, l.n, rcap));
-        std::vector<TruncItem>& dst = rt == 2 ? tb : rt == 1 ? tp : t;
+        std::vector<TruncItem>& dst = rt == 2 ? tb : rt == 1 ? tp : rt == 3 ? td : t;
         for (int i : v) {
           const Add& a = flat[i];
           TruncItem ti = lritem(l.a, l.b, l.m, l.n, rankp(c), compp(c), 2, l.cap, &a.p, &a.q,
@@ -751,6 +751,9 @@ struct Engine {
         } else if (rt == 1) {
           tpoff.push_back((int)tp.size());
           meta(meta_p, l.m, l.n, (int)v.size());
+        } else if (rt == 3) {
+          tdoff.push_back((int)td.size());
+          meta(meta_d, l.m, l.n, (int)v.size());
         } else {
           toff.push_back((int)t.size());
           meta(meta_t, l.m, l.n, (int)v.size());
@@ -773,6 +776,12 @@ struct Engine {
       st_next = meta_p;
       st_next[0] = -st_next[0];
       stat(S_TRUNC, tp.size());
+    }
+    if (!td.empty()) {
+      launch_truncate_pair(sg.put(td), sg.put(tdoff), (int)tdoff.size() - 1, eps, d_err, st, true);
+      st_next = meta_d;
+      st_next[0] = -st_next[0];
+      stat(S_TRUNC, td.size());
     }
     if (!t.empty()) {
       launch_truncate_seq(sg.put(t), sg.put(toff), (int)toff.size() - 1, eps, d_err, st, sw, smn);

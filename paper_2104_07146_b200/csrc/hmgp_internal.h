@@ -140,8 +140,9 @@ void launch_truncate_cluster(const TruncItem* d_items, const int* d_off, int tar
 bool trunc_use_pair(int m, int n, int rcap);
 size_t trunc_ws_doubles_pair(int m, int n, int rcap);
 void launch_truncate_pair(const TruncItem* d_items, const int* d_off, int targets, double eps,
-                          int* d_err, cudaStream_t st);
-// 0 single CTA (small), 1 CTA pair, 2 8-CTA cluster; workspace for that route
+                          int* d_err, cudaStream_t st, bool defer_to_cluster = false);
+// 0 single CTA (small), 1 CTA pair, 2 8-CTA cluster, 3 pair handing over to the
+// cluster kernel what does not fit; workspace for that route
 int trunc_route(int m, int n, int rcap);
 size_t trunc_ws_for(int m, int n, int rcap);
 void truncate_hist_enable(bool on);

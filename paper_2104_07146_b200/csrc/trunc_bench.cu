@@ -119,8 +119,8 @@ extern "C" int hmgp_debug_trunc_bench(int m, int n, int r0, int add, int count, 
       cudaEventRecord(e0, st);
       if (route == 2)
         launch_truncate_cluster(ditems, doff, count, eps, derr, st);
-      else if (route == 1)
-        launch_truncate_pair(ditems, doff, count, eps, derr, st);
+      else if (route == 1 || route == 3)
+        launch_truncate_pair(ditems, doff, count, eps, derr, st, route == 3);
       else
         launch_truncate(ditems, count, eps, derr, st, sw, smn);
       cudaEventRecord(e1, st);

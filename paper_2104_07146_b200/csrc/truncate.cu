@@ -846,13 +846,12 @@ __device__ void clu_apply_q(cg::cluster_group& cl, CluShared& sh, const double* 
 }
 
 __device__ void lr_update_cluster(cg::cluster_group& cl, CluShared& sh, const TruncItem& it,
-                                  double eps, int* err) {
+                                  double eps, int* err, int r0) {
   const int rank = cl.block_rank();
   __shared__ double red[32];
   __shared__ double s_sig[kMaxTruncCols];
   __shared__ int s_ord[kMaxTruncCols];
   __shared__ int s_keep, s_kq;
-  const int r0 = *it.rank;
   const int add = it.P ? (it.addp ? *it.addp : it.addv) : 0;
   const int r = r0 + add;
   bool go;
@@ -995,17 +994,42 @@ __device__ void lr_update_cluster(cg::cluster_group& cl, CluShared& sh, const Tr
   cl.sync();
 }
 
+template <bool kFallback>
+__device__ bool lr_update_pair(cg::cluster_group& cl, const TruncItem& it, double eps, int* err,
+                               int cap_dbl, double* sm, bool may_defer, int r0, bool active);
+__device__ __forceinline__ bool pair_fits(int m, int n, int r, int cap_dbl);
+
 // cluster b (CTAs b*kClu .. b*kClu+kClu-1) runs target b's sequence in order
 __global__ void __cluster_dims__(kClu, 1, 1) __launch_bounds__(kTruncThreads)
     k_truncate_cluster(const TruncItem* __restrict__ items, const int* __restrict__ off, double eps,
-                       int* err) {
+                       int* err, const int* __restrict__ defer, int cap_dbl) {
   cg::cluster_group cl = cg::this_cluster();
   __shared__ CluShared sh;
+  extern __shared__ double csm[];
   const int b = blockIdx.x / kClu;
-  for (int i = off[b]; i < off[b + 1]; ++i) {
-    lr_update_cluster(cl, sh, items[i], eps, err);
-    if (items[i].post_L) {
-      if (cl.block_rank() == 0) lr_post_solve(items[i]);
+  int start = off[b];
+  if (defer) {  // only the sequence tail the pair kernel handed over
+    start = defer[b];
+    if (start < 0) return;
+  }
+  for (int i = start; i < off[b + 1]; ++i) {
+    const TruncItem& it = items[i];
+    const int r0 = *it.rank;
+    // every rank has read rank / compact before any may change them (the
+    // cluster path itself writes them only after its own cluster barriers)
+    if (cap_dbl > 0) cl.sync();
+    // items whose actual column count fits the pair layout run on ranks 0-1
+    bool pair = false;
+    if (cap_dbl > 0) {
+      const int r = r0 + (it.P ? (it.addp ? *it.addp : it.addv) : 0);
+      pair = pair_fits(it.m, it.n, r, cap_dbl);
+    }
+    if (pair)
+      lr_update_pair<false>(cl, it, eps, err, cap_dbl, csm, false, r0, cl.block_rank() < 2);
+    else
+      lr_update_cluster(cl, sh, it, eps, err, r0);
+    if (it.post_L) {
+      if (cl.block_rank() == (pair ? 1 : 0)) lr_post_solve(it);
       cl.sync();
     }
   }
@@ -1111,14 +1135,29 @@ __host__ __device__ __forceinline__ size_t pair_smem_doubles(int m, int n, int r
   return (size_t)(max(m, n) | 1) * r + 4 * (size_t)r * r + 5 * (size_t)r + 8;
 }
 
-__device__ void lr_update_pair(cg::cluster_group& cl, const TruncItem& it, double eps, int* err,
-                               int cap_dbl, double* sm) {
-  const int side = (int)cl.block_rank();  // 0: U side, 1: V side
-  __shared__ double red[32];
+// the pair path covers the item: columns, shared memory, register QR shape
+__device__ __forceinline__ bool pair_fits(int m, int n, int r, int cap_dbl) {
+  return r <= kPairMaxR && pair_smem_doubles(m, n, r) <= (size_t)cap_dbl && !(max(m, n) > 256 && r > 32) &&
+         max(m, n) <= 512;
+}
+
+// Pair-path recompression of one item.  The caller has read the item's rank
+// (r0) in every CTA of its cluster and synchronised the cluster.  `active` is
+// true on the two CTAs doing the work (cluster ranks 0: U side, 1: V side);
+// inside the 8-CTA cluster kernel the other ranks call it with active = false
+// and only take part in the cluster barriers (the barrier sequence depends
+// only on item data, identical in every rank).  Returns false (nothing done)
+// when the item does not fit and may_defer is set.  kFallback: run items that
+// do not fit on CTA 0's single-CTA paths (the cluster kernel never passes such
+// items).
+template <bool kFallback>
+__device__ bool lr_update_pair(cg::cluster_group& cl, const TruncItem& it, double eps, int* err,
+                               int cap_dbl, double* sm, bool may_defer, int r0, bool active) {
+  const int side = (int)cl.block_rank() & 1;  // 0: U side, 1: V side
+  const bool lead = cl.block_rank() == 0 && threadIdx.x == 0;
   __shared__ double s_sig[kPairMaxR];
   __shared__ int s_ord[kPairMaxR];
   __shared__ double s_tail[2];
-  const int r0 = *it.rank;
   const int add = it.P ? (it.addp ? *it.addp : it.addv) : 0;
   const int r = r0 + add;
   bool go;
@@ -1129,47 +1168,49 @@ __device__ void lr_update_pair(cg::cluster_group& cl, const TruncItem& it, doubl
     case 4: go = false; break;
     default: go = r > 0; break;
   }
-  cl.sync();  // both CTAs have read rank / compact before either may change them
   const int m = it.m, n = it.n;
   const int mm = side ? n : m;
   double* X = side ? it.V : it.U;
   if (!go) {
     if (add > 0 && r > it.cap) {
-      if (side == 0 && threadIdx.x == 0) atomicOr(err, 2);
+      if (lead) atomicOr(err, 2);
       cl.sync();
-      return;
+      return true;
     }
-    for (size_t e = threadIdx.x; e < (size_t)mm * add; e += blockDim.x) {
-      const int i = (int)(e % mm), k = (int)(e / mm);
-      double v;
-      if (side == 0) {
-        const int pi = i - it.pro;
-        v = (pi >= 0 && pi < it.pr) ? it.alpha * it.P[(size_t)k * it.ldp + pi] : 0.0;
-      } else {
-        const int qi = i - it.qro;
-        v = (qi >= 0 && qi < it.qr) ? it.Q[(size_t)k * it.ldq + qi] : 0.0;
+    if (active)
+      for (size_t e = threadIdx.x; e < (size_t)mm * add; e += blockDim.x) {
+        const int i = (int)(e % mm), k = (int)(e / mm);
+        double v;
+        if (side == 0) {
+          const int pi = i - it.pro;
+          v = (pi >= 0 && pi < it.pr) ? it.alpha * it.P[(size_t)k * it.ldp + pi] : 0.0;
+        } else {
+          const int qi = i - it.qro;
+          v = (qi >= 0 && qi < it.qr) ? it.Q[(size_t)k * it.ldq + qi] : 0.0;
+        }
+        X[(size_t)(r0 + k) * mm + i] = v;
       }
-      X[(size_t)(r0 + k) * mm + i] = v;
-    }
-    if (side == 0 && threadIdx.x == 0) {
+    if (lead) {
       *it.rank = r;
       if (it.cond == 0 && it.compact) *it.compact = r;
     }
     cl.sync();
-    return;
+    return true;
   }
   if (r > it.rcap) {
-    if (side == 0 && threadIdx.x == 0) atomicOr(err, 1);
+    if (lead) atomicOr(err, 1);
     cl.sync();
-    return;
+    return true;
   }
-  if (r > kPairMaxR || pair_smem_doubles(m, n, r) > (size_t)cap_dbl || (max(m, n) > 256 && r > 32)) {
+  if (!pair_fits(m, n, r, cap_dbl)) {
+    if (may_defer) return false;
     // single-CTA paths on CTA 0 (W in shared memory when it fits, else global)
-    if (side == 0) lr_update(it, eps, err, kMaxSmemW, kMaxSmemMN);
+    if (kFallback && cl.block_rank() == 0) lr_update(it, eps, err, kMaxSmemW, kMaxSmemMN);
     cl.sync();
-    return;
+    return true;
   }
   const long long t0 = clock64();
+  long long tc = t0;
   const int ku = min(m, r), kv = min(n, r);
   const int kme = side ? kv : ku, ko = side ? ku : kv, mo = side ? m : n;
   const int lda = mm | 1, ldo = mo | 1;    // odd strides: conflict-free row-varying access
@@ -1183,98 +1224,110 @@ __device__ void lr_update_pair(cg::cluster_group& cl, const TruncItem& it, doubl
   double* cn = tau_c + r;                  // 2r (double-buffered trailing norms)
   int* phys = reinterpret_cast<int*>(cn + 2 * r);  // r ints: core pivot order
   int* stepof = phys + r;                          // r ints
-  // stage [X | added] (mm x r)
-  for (size_t e = threadIdx.x; e < (size_t)mm * r; e += blockDim.x) {
-    const int i = (int)(e % mm), l = (int)(e / mm);
-    double v;
-    if (l < r0) {
-      v = X[e];
-    } else if (side == 0) {
-      const int pi = i - it.pro;
-      v = (pi >= 0 && pi < it.pr) ? it.alpha * it.P[(size_t)(l - r0) * it.ldp + pi] : 0.0;
-    } else {
-      const int qi = i - it.qro;
-      v = (qi >= 0 && qi < it.qr) ? it.Q[(size_t)(l - r0) * it.ldq + qi] : 0.0;
+  if (active) {
+    // stage [X | added] (mm x r)
+    for (size_t e = threadIdx.x; e < (size_t)mm * r; e += blockDim.x) {
+      const int i = (int)(e % mm), l = (int)(e / mm);
+      double v;
+      if (l < r0) {
+        v = X[e];
+      } else if (side == 0) {
+        const int pi = i - it.pro;
+        v = (pi >= 0 && pi < it.pr) ? it.alpha * it.P[(size_t)(l - r0) * it.ldp + pi] : 0.0;
+      } else {
+        const int qi = i - it.qro;
+        v = (qi >= 0 && qi < it.qr) ? it.Q[(size_t)(l - r0) * it.ldq + qi] : 0.0;
+      }
+      A[(size_t)l * lda + i] = v;
     }
-    A[(size_t)l * lda + i] = v;
-  }
-  __syncthreads();
-  long long tc = t0;
-  stage_add(2, 0, tc);
-  {
+    __syncthreads();
+    stage_add(2, 0, tc);
     __shared__ double s_vbuf[2 * 512];
     __shared__ double s_sbuf[2];
     if (!reg_qr_any(A, mm, lda, r, tau, s_vbuf, s_sbuf)) smem_qr(A, mm, lda, r, tau, s_tail);
+    stage_add(2, 1, tc);
   }
-  stage_add(2, 1, tc);
   cl.sync();
-  {  // other side's R through distributed shared memory
-    const double* Aot = cl.map_shared_rank(A, side ^ 1);
-    for (int e = threadIdx.x; e < ko * r; e += blockDim.x) {
-      const int i = e % ko, l = e / ko;
-      Ro[e] = (i <= l) ? Aot[(size_t)l * ldo + i] : 0.0;
-    }
-  }
-  __syncthreads();
-  // core(i,j) = sum_{l >= max(i,j)} Ru(i,l) Rv(j,l)  (ku x kv, ld ku)
-  {
-    const double* Ru = side ? Ro : A;
-    const double* Rv = side ? A : Ro;
-    const int ldu = side ? ku : lda, ldv = side ? lda : kv;
-    for (int idx = threadIdx.x; idx < ku * kv; idx += blockDim.x) {
-      const int i = idx % ku, j = idx / ku;
-      double s = 0.0;
-      for (int l = max(i, j); l < r; ++l) s += Ru[(size_t)l * ldu + i] * Rv[(size_t)l * ldv + j];
-      C[(size_t)j * ku + i] = s;
-    }
-  }
-  __syncthreads();
-  const RS rs = cta_rrqr_svd2(C, ku, kv, eps, tau_c, phys, cn, stepof, Ro, J, s_sig, s_ord, 2, &tc);
-  const int keep = rs.keep, kq = rs.kq;
-  if (keep > it.cap) {
-    if (side == 0 && threadIdx.x == 0) atomicOr(err, 4);
-    cl.sync();
-    return;
-  }
-  if (side == 0) {  // U_core = Q_core [J S; 0] (ku x keep)
-    for (int idx = threadIdx.x; idx < ku * keep; idx += blockDim.x) {
-      const int i = idx % ku, c = idx / ku, src = s_ord[c];
-      E0[idx] = i < kq ? J[(size_t)src * kq + i] * s_sig[src] : 0.0;
+  int keep = 0;
+  RS rs{0, 0, 0.0};
+  if (active) {
+    {  // other side's R through distributed shared memory
+      const double* Aot = cl.map_shared_rank(A, side ^ 1);
+      for (int e = threadIdx.x; e < ko * r; e += blockDim.x) {
+        const int i = e % ko, l = e / ko;
+        Ro[e] = (i <= l) ? Aot[(size_t)l * ldo + i] : 0.0;
+      }
     }
     __syncthreads();
-    cta_apply_q_map(C, ku, ku, kq, tau_c, phys, E0, keep);
-  } else {  // Y (kv x keep)
-    for (int idx = threadIdx.x; idx < kv * keep; idx += blockDim.x) {
-      const int i = idx % kv, c = idx / kv, src = s_ord[c];
-      E0[idx] = Ro[(size_t)src * kv + i] / s_sig[src];
+    // core(i,j) = sum_{l >= max(i,j)} Ru(i,l) Rv(j,l)  (ku x kv, ld ku); both sides
+    // form it with identical arithmetic
+    {
+      const double* Ru = side ? Ro : A;
+      const double* Rv = side ? A : Ro;
+      const int ldu = side ? ku : lda, ldv = side ? lda : kv;
+      for (int idx = threadIdx.x; idx < ku * kv; idx += blockDim.x) {
+        const int i = idx % ku, j = idx / ku;
+        double s = 0.0;
+        for (int l = max(i, j); l < r; ++l) s += Ru[(size_t)l * ldu + i] * Rv[(size_t)l * ldv + j];
+        C[(size_t)j * ku + i] = s;
+      }
+    }
+    __syncthreads();
+    rs = cta_rrqr_svd2(C, ku, kv, eps, tau_c, phys, cn, stepof, Ro, J, s_sig, s_ord, 2, &tc);
+    keep = rs.keep;
+    const int kq = rs.kq;
+    if (keep > it.cap) {
+      if (lead) atomicOr(err, 4);
+    } else {
+      if (side == 0) {  // U_core = Q_core [J S; 0] (ku x keep)
+        for (int idx = threadIdx.x; idx < ku * keep; idx += blockDim.x) {
+          const int i = idx % ku, c = idx / ku, src = s_ord[c];
+          E0[idx] = i < kq ? J[(size_t)src * kq + i] * s_sig[src] : 0.0;
+        }
+        __syncthreads();
+        cta_apply_q_map(C, ku, ku, kq, tau_c, phys, E0, keep);
+      } else {  // Y (kv x keep)
+        for (int idx = threadIdx.x; idx < kv * keep; idx += blockDim.x) {
+          const int i = idx % kv, c = idx / kv, src = s_ord[c];
+          E0[idx] = Ro[(size_t)src * kv + i] / s_sig[src];
+        }
+      }
+      __syncthreads();
+      wy_apply(A, mm, lda, kme, tau, E0, keep, X, J, C, Ro);
+      stage_add(2, 4, tc);
     }
   }
-  __syncthreads();
-  wy_apply(A, mm, lda, kme, tau, E0, keep, X, J, C, Ro);
-  stage_add(2, 4, tc);
   cl.sync();
-  if (side == 0 && threadIdx.x == 0) {
+  if (lead && keep <= it.cap) {
     *it.rank = keep;
     if (it.compact) *it.compact = keep;
     const double fl = qr_flops(m, r) + qr_flops(n, r) + (double)ku * kv * r + rs.flops +
-                      4.0 * keep * ((double)m * ku + (double)n * kv + (double)ku * kq);
+                      4.0 * keep * ((double)m * ku + (double)n * kv + (double)ku * rs.kq);
     atomicAdd(&d_cnt_trunc, fl);
     atomicAdd(&d_cnt_titems, 1.0);
   }
-  if (side == 0) hist_add(3, m, n, r, t0);
+  if (cl.block_rank() == 0) hist_add(3, m, n, r, t0);
   cl.sync();
+  return true;
 }
 
 // cluster b (CTA pair 2b, 2b+1) runs target b's sequence in order
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTruncThreads)
     k_truncate_pair(const TruncItem* __restrict__ items, const int* __restrict__ off, double eps,
-                    int* err, int cap_dbl) {
+                    int* err, int cap_dbl, int* defer) {
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ double psm[];
   const int b = blockIdx.x / 2;
+  const bool lead = cl.block_rank() == 0 && threadIdx.x == 0;
+  if (defer && lead) defer[b] = -1;
   for (int i = off[b]; i < off[b + 1]; ++i) {
     const TruncItem& it = items[i];
-    lr_update_pair(cl, it, eps, err, cap_dbl, psm);
+    const int r0 = *it.rank;
+    cl.sync();  // both CTAs have read rank / compact before either may change them
+    if (!lr_update_pair<true>(cl, it, eps, err, cap_dbl, psm, defer != nullptr, r0, true)) {
+      if (lead) defer[b] = i;  // items[i..] go to the cluster kernel, in order
+      break;
+    }
     if (it.post_L) {
       if (cl.block_rank() == 1) lr_post_solve(it);
       cl.sync();
@@ -1285,8 +1338,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTruncThreads)
 static int g_pair_cap = -1;
 static size_t g_pair_bytes = 0;
 void launch_truncate_pair(const TruncItem* d_items, const int* d_off, int targets, double eps,
-                          int* d_err, cudaStream_t st) {
+                          int* d_err, cudaStream_t st, bool defer_to_cluster) {
   if (targets <= 0) return;
+  // per-target hand-over index for items that do not fit the pair layout
+  static thread_local int* d_defer = nullptr;
+  static thread_local int defer_cap = 0;
+  if (defer_to_cluster && targets > defer_cap) {
+    if (d_defer) {
+      HMGP_CUDA(cudaStreamSynchronize(st));
+      cudaFree(d_defer);
+    }
+    defer_cap = std::max(targets, 1 << 16);
+    HMGP_CUDA(cudaMalloc(&d_defer, (size_t)defer_cap * 4));
+  }
   if (g_pair_cap < 0) {
     cudaFuncAttributes fa;
     HMGP_CUDA(cudaFuncGetAttributes(&fa, k_truncate_pair));
@@ -1298,9 +1362,14 @@ void launch_truncate_pair(const TruncItem* d_items, const int* d_off, int target
                                    (int)g_pair_bytes));
     g_pair_cap = (int)(g_pair_bytes / 8);
   }
+  int* dfr = defer_to_cluster ? d_defer : nullptr;
   k_truncate_pair<<<targets * 2, kTruncThreads, g_pair_bytes, st>>>(d_items, d_off, eps, d_err,
-                                                                   g_pair_cap);
+                                                                   g_pair_cap, dfr);
   HMGP_LAUNCH_CHECK();
+  if (dfr) {
+    k_truncate_cluster<<<targets * kClu, kTruncThreads, 0, st>>>(d_items, d_off, eps, d_err, dfr, 0);
+    HMGP_LAUNCH_CHECK();
+  }
 }
 
 size_t trunc_ws_doubles_pair(int m, int n, int rcap) {  // the global-memory fallback
@@ -1309,17 +1378,23 @@ size_t trunc_ws_doubles_pair(int m, int n, int rcap) {  // the global-memory fal
 }
 
 bool trunc_use_pair(int m, int n, int rcap) {
+  (void)rcap;
   if ((size_t)m * n <= (size_t)kMaxSmemW / 4) return false;
-  const int mx = std::max(m, n);
-  return mx <= 256 || (mx <= 512 && rcap <= 32);
+  return std::max(m, n) <= 256;
 }
 
+// 1: pair (device fallback to one CTA), 3: pair with hand-over of items that
+// do not fit (rank known only on device) to the 8-CTA cluster kernel,
+// 2: cluster, 0: one CTA
 int trunc_route(int m, int n, int rcap) {
-  return trunc_use_pair(m, n, rcap) ? 1 : trunc_use_cluster(m, n) ? 2 : 0;
+  if (trunc_use_pair(m, n, rcap)) return 1;
+  if (trunc_use_cluster(m, n)) return 2;  // (the cluster kernel runs fitting items as a pair)
+  return 0;
 }
 
 size_t trunc_ws_for(int m, int n, int rcap) {
   switch (trunc_route(m, n, rcap)) {
+    case 3:
     case 2: return trunc_ws_doubles_cluster(m, n, rcap);
     case 1: return trunc_ws_doubles_pair(m, n, rcap);
     default: return trunc_ws_doubles(m, n, rcap);
@@ -1338,7 +1413,10 @@ bool trunc_use_cluster(int m, int n) {
 void launch_truncate_cluster(const TruncItem* d_items, const int* d_off, int targets, double eps,
                              int* d_err, cudaStream_t st) {
   if (targets <= 0) return;
-  k_truncate_cluster<<<targets * kClu, kTruncThreads, 0, st>>>(d_items, d_off, eps, d_err);
+  // No pair-layout dispatch here (cap_dbl = 0): the global-memory cluster path
+  // depends on L1 holding its row slices, and a pair-sized dynamic
+  // shared-memory carve-out would take that L1 away from every item.
+  k_truncate_cluster<<<targets * kClu, kTruncThreads, 0, st>>>(d_items, d_off, eps, d_err, nullptr, 0);
   HMGP_LAUNCH_CHECK();
 }
 
