@@ -485,7 +485,7 @@ void assemble(HMat& h, Geometry& g, const MaternDev& p, double eps, bool fixed_r
           std::vector<int> off(tbig.size() + 1);
           for (size_t q = 0; q <= tbig.size(); ++q) off[q] = (int)q;
           int* d_off = upload(off, st);
-          launch_truncate_cluster(d_tb, d_off, (int)tbig.size(), eps, d_err, st);
+          launch_truncate_cluster(d_tb, d_off, (int)tbig.size(), eps, d_err, st, false);
           HMGP_CUDA(cudaStreamSynchronize(st));
           cudaFree(d_tb);
           cudaFree(d_off);

@@ -171,12 +171,21 @@ struct Engine {
   bool stats_on = getenv("HMGP_STATS") != nullptr;
   std::vector<std::pair<int, cudaEvent_t>> st_ev;
   cudaEvent_t st_prev = nullptr;
-  std::vector<std::array<int, 4>> st_meta;  // per event: max m, max n, items, max seq length
-  std::array<int, 4> st_next{};
+  std::vector<std::array<int, 5>> st_meta;  // per event: max m, max n, items, max seq length, slot
+  std::array<int, 5> st_next{};
+  int st_slot = 0;
+  // (stats mode) give the next truncation launch its own per-launch maxima slot
+  void tslot() {
+    if (stats_on) {
+      ++st_slot;
+      truncate_launch_slot(st_slot, st);
+    }
+  }
   void stat(int k, size_t items) {
     ++st_launch[k];
     st_items[k] += (long long)items;
     if (stats_on) {
+      st_next[4] = k == S_TRUNC ? st_slot : 0;
       cudaEvent_t e;
       cudaEventCreate(&e);
       cudaEventRecord(e, st);
@@ -216,6 +225,45 @@ struct Engine {
     st_next[2] = items;
     st_next[3] = std::max(st_next[3], seq);
   }
+  // Cluster targets: those up to 2048 rows run with the resident (pair /
+  // register) dispatch, larger ones on the global-memory path without a
+  // shared-memory carve-out; the two launches are independent and run on the
+  // main and a side stream (fork / join through events).
+  void cluster_launch(const std::vector<TruncItem>& items, const std::vector<int>& off) {
+    std::vector<TruncItem> ir, ig;
+    std::vector<int> offr{0}, offg{0};
+    for (size_t b = 0; b + 1 < off.size(); ++b) {
+      const TruncItem& h = items[off[b]];
+      const bool res = trunc_cluster_resident(h.m, h.n);
+      std::vector<TruncItem>& dst = res ? ir : ig;
+      for (int i = off[b]; i < off[b + 1]; ++i) dst.push_back(items[i]);
+      (res ? offr : offg).push_back((int)dst.size());
+    }
+    const TruncItem* dr = ir.empty() ? nullptr : sg.put(ir);
+    const int* dor = ir.empty() ? nullptr : sg.put(offr);
+    const TruncItem* dg = ig.empty() ? nullptr : sg.put(ig);
+    const int* dog = ig.empty() ? nullptr : sg.put(offg);
+    if (dr && dg) {
+      static thread_local cudaStream_t st2 = nullptr;
+      static thread_local cudaEvent_t evf = nullptr, evj = nullptr;
+      if (!st2) {
+        HMGP_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
+        HMGP_CUDA(cudaEventCreateWithFlags(&evf, cudaEventDisableTiming));
+        HMGP_CUDA(cudaEventCreateWithFlags(&evj, cudaEventDisableTiming));
+      }
+      HMGP_CUDA(cudaEventRecord(evf, st));
+      HMGP_CUDA(cudaStreamWaitEvent(st2, evf, 0));
+      launch_truncate_cluster(dg, dog, (int)offg.size() - 1, eps, d_err, st2, false);
+      HMGP_CUDA(cudaEventRecord(evj, st2));
+      launch_truncate_cluster(dr, dor, (int)offr.size() - 1, eps, d_err, st, true);
+      HMGP_CUDA(cudaStreamWaitEvent(st, evj, 0));
+    } else if (dr) {
+      launch_truncate_cluster(dr, dor, (int)offr.size() - 1, eps, d_err, st, true);
+    } else if (dg) {
+      launch_truncate_cluster(dg, dog, (int)offg.size() - 1, eps, d_err, st, false);
+    }
+  }
+
   void lrupd(std::vector<TruncItem>& v0) {
     if (v0.empty()) return;
     // large blocks -> one 8-CTA cluster each, medium -> one CTA pair each, the
@@ -231,10 +279,11 @@ struct Engine {
       if (grp.empty()) continue;
       std::vector<int> off(grp.size() + 1);
       for (size_t i = 0; i <= grp.size(); ++i) off[i] = (int)i;
+      tslot();
       if (pass)
         launch_truncate_pair(sg.put(grp), sg.put(off), (int)grp.size(), eps, d_err, st, pass == 2);
       else
-        launch_truncate_cluster(sg.put(grp), sg.put(off), (int)grp.size(), eps, d_err, st);
+        cluster_launch(grp, off);
       st_next = {};
       for (const TruncItem& t : grp) {
         st_next[0] = std::min(st_next[0], -t.m);
@@ -251,6 +300,7 @@ struct Engine {
       if (t.cond != 4) trunc_smem_dims(t.m, t.n, &sw, &smn);
       if (stats_on) note_dims(t.m, t.n, (int)v.size(), 1);
     }
+    tslot();
     launch_truncate(sg.put(v), (int)v.size(), eps, d_err, st, sw, smn);
     stat(S_TRUNC, v.size());
     v.clear();
@@ -270,6 +320,33 @@ struct Engine {
       prev = pe.second;
     }
     truncate_hist_print();
+    {  // launch wall time vs its slowest item / slowest target sequence, by size class
+      std::vector<unsigned long long> mx, sq;
+      truncate_launch_read(mx, sq);
+      std::map<int, std::array<double, 4>> agg;
+      cudaEvent_t pv = st_prev;
+      for (size_t i = 0; i < st_ev.size(); ++i) {
+        float t = 0.f;
+        if (pv) cudaEventElapsedTime(&t, pv, st_ev[i].second);
+        pv = st_ev[i].second;
+        if (st_ev[i].first != S_TRUNC) continue;
+        const auto& mt = st_meta[i];
+        int b = 1;
+        while (b < std::max(std::abs(mt[0]), mt[1])) b <<= 1;
+        auto& a = agg[mt[0] < 0 ? -b : b];
+        const int sl = mt[4] & ((1 << 17) - 1);
+        a[0] += t;
+        a[1] += mx[sl] / 1.9e6;
+        a[2] += sq[sl] / 1.9e6;
+        a[3] += 1;
+      }
+      for (const auto& kv : agg)
+        fprintf(stderr,
+                "[hmgp]   lrupd %s max-dim <= %6d: wall %8.1f ms, sum of slowest item %8.1f ms, "
+                "slowest sequence %8.1f ms (%d launches)\n",
+                kv.first < 0 ? "cluster" : "cta    ", std::abs(kv.first), kv.second[0], kv.second[1],
+                kv.second[2], (int)kv.second[3]);
+    }
     std::sort(tr.begin(), tr.end(), [](auto& a, auto& b) { return a.first > b.first; });
     for (size_t q = 0; q < tr.size() && q < 12; ++q) {
       const auto& m = st_meta[tr[q].second];
@@ -704,8 +781,8 @@ struct Engine {
     std::vector<TruncItem> t, tb, tp, td;
     std::vector<int> toff{0}, tboff{0}, tpoff{0}, tdoff{0};
     int sw = 0, smn = 0;
-    std::array<int, 4> meta_t{}, meta_b{}, meta_p{}, meta_d{};  // stats: max m, max n, targets, longest seq
-    auto meta = [](std::array<int, 4>& mt, int m, int n, int seq) {
+    std::array<int, 5> meta_t{}, meta_b{}, meta_p{}, meta_d{};  // stats: max m, max n, targets, longest seq
+    auto meta = [](std::array<int, 5>& mt, int m, int n, int seq) {
       mt[0] = std::max(mt[0], m);
       mt[1] = std::max(mt[1], n);
       ++mt[2];
@@ -766,24 +843,28 @@ struct Engine {
       stat(S_GEMM, g.size());
     }
     if (!tb.empty()) {
-      launch_truncate_cluster(sg.put(tb), sg.put(tboff), (int)tboff.size() - 1, eps, d_err, st);
+      tslot();
+      cluster_launch(tb, tboff);
       st_next = meta_b;
       st_next[0] = -st_next[0];  // negative m marks a cluster launch
       stat(S_TRUNC, tb.size());
     }
     if (!tp.empty()) {
+      tslot();
       launch_truncate_pair(sg.put(tp), sg.put(tpoff), (int)tpoff.size() - 1, eps, d_err, st);
       st_next = meta_p;
       st_next[0] = -st_next[0];
       stat(S_TRUNC, tp.size());
     }
     if (!td.empty()) {
+      tslot();
       launch_truncate_pair(sg.put(td), sg.put(tdoff), (int)tdoff.size() - 1, eps, d_err, st, true);
       st_next = meta_d;
       st_next[0] = -st_next[0];
       stat(S_TRUNC, td.size());
     }
     if (!t.empty()) {
+      tslot();
       launch_truncate_seq(sg.put(t), sg.put(toff), (int)toff.size() - 1, eps, d_err, st, sw, smn);
       st_next = meta_t;
       stat(S_TRUNC, t.size());

@@ -135,7 +135,9 @@ void launch_truncate(const TruncItem* d_items, int count, double eps, int* d_err
 bool trunc_use_cluster(int m, int n);
 size_t trunc_ws_doubles_cluster(int m, int n, int rcap);
 void launch_truncate_cluster(const TruncItem* d_items, const int* d_off, int targets, double eps,
-                             int* d_err, cudaStream_t st);
+                             int* d_err, cudaStream_t st, bool resident = false);
+// launch cluster targets of this size with the resident (pair / register) dispatch
+bool trunc_cluster_resident(int m, int n);
 // medium blocks: one CTA pair (U side, V side) per target sequence, factors in smem
 bool trunc_use_pair(int m, int n, int rcap);
 size_t trunc_ws_doubles_pair(int m, int n, int rcap);
@@ -146,6 +148,8 @@ void launch_truncate_pair(const TruncItem* d_items, const int* d_off, int target
 int trunc_route(int m, int n, int rcap);
 size_t trunc_ws_for(int m, int n, int rcap);
 void truncate_hist_enable(bool on);
+void truncate_launch_slot(int idx, cudaStream_t st);
+void truncate_launch_read(std::vector<unsigned long long>& mx, std::vector<unsigned long long>& sq);
 void truncate_hist_print();
 // per-target ordered sequences: CTA b runs items[off[b]..off[b+1]) in order
 void launch_truncate_seq(const TruncItem* d_items, const int* d_off, int targets, double eps,

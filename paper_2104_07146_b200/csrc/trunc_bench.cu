@@ -118,7 +118,7 @@ extern "C" int hmgp_debug_trunc_bench(int m, int n, int r0, int add, int count, 
       HMGP_CUDA(cudaMemsetAsync(derr, 0, 4, st));
       cudaEventRecord(e0, st);
       if (route == 2)
-        launch_truncate_cluster(ditems, doff, count, eps, derr, st);
+        launch_truncate_cluster(ditems, doff, count, eps, derr, st, trunc_cluster_resident(m, n));
       else if (route == 1 || route == 3)
         launch_truncate_pair(ditems, doff, count, eps, derr, st, route == 3);
       else

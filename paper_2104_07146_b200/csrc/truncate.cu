@@ -14,6 +14,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "common.cuh"
 #include "hmgp_internal.h"
@@ -39,8 +40,26 @@ __device__ __forceinline__ int hbucket(int v) {
   while (b < kHM - 1 && (16 << b) < v) ++b;
   return b;
 }
+// (stats mode) per-launch maxima: slowest item and slowest target sequence
+constexpr int kLaunchSlots = 1 << 17;
+__device__ int d_lidx;
+__device__ unsigned long long d_lmax[kLaunchSlots], d_lseq[kLaunchSlots];
+__device__ __forceinline__ void seq_done(long long ts) {
+  if (!d_hist_on || threadIdx.x != 0) return;
+  atomicMax(&d_lseq[d_lidx & (kLaunchSlots - 1)], (unsigned long long)(clock64() - ts));
+}
+void truncate_launch_slot(int idx, cudaStream_t st) {
+  HMGP_CUDA(cudaMemcpyToSymbolAsync(d_lidx, &idx, 4, 0, cudaMemcpyHostToDevice, st));
+}
+void truncate_launch_read(std::vector<unsigned long long>& mx, std::vector<unsigned long long>& sq) {
+  mx.resize(kLaunchSlots);
+  sq.resize(kLaunchSlots);
+  HMGP_CUDA(cudaMemcpyFromSymbol(mx.data(), d_lmax, kLaunchSlots * 8));
+  HMGP_CUDA(cudaMemcpyFromSymbol(sq.data(), d_lseq, kLaunchSlots * 8));
+}
 __device__ __forceinline__ void hist_add(int path, int m, int n, int r, long long t0) {
   if (!d_hist_on || threadIdx.x != 0) return;
+  atomicMax(&d_lmax[d_lidx & (kLaunchSlots - 1)], (unsigned long long)(clock64() - t0));
   const int bm = hbucket(max(m, n)), br = min(hbucket(r), kHR - 1);
   atomicAdd(&d_hist_n[path][bm][br], 1ull);
   atomicAdd(&d_hist_cyc[path][bm][br], (unsigned long long)(clock64() - t0));
@@ -99,8 +118,8 @@ size_t trunc_ws_doubles(int m, int n, int rcap) {
   const size_t mn = (size_t)min(m, n);
   const size_t kq = std::min(mn, (size_t)rcap), rc = (size_t)rcap;
   if ((size_t)m * n <= (size_t)kMaxSmemW && m + n <= kMaxSmemMN)  // small-block path only
-    return 3 * (size_t)n + (size_t)n * kq + kq * kq;
-  return (size_t)(m + n) * rc + 5 * rc + rc * rc + 2 * rc * kq + kq * kq;
+    return 4 * (size_t)n + (size_t)n * kq + kq * kq;
+  return (size_t)(m + n) * rc + 6 * rc + rc * rc + 2 * rc * kq + kq * kq;
 }
 
 void trunc_smem_dims(int m, int n, int* smem_w, int* smem_mn) {
@@ -471,6 +490,8 @@ __device__ RS cta_rrqr_svd(double* W, int p, int q, double eps, double* tau, int
   return RS{kq, s_keep, flops};
 }
 
+#include "trunc_lean.cuh"
+
 __device__ void lr_update(const TruncItem& it, double eps, int* err, int smem_w, int smem_mn);
 
 // Fused trsm_lower_t post-op (hfactor.cpp:198-202): V <- L^{-1} V, V /= d.
@@ -497,12 +518,14 @@ __device__ void lr_post_solve(const TruncItem& it) {
 __global__ void __launch_bounds__(kTruncThreads) k_truncate(const TruncItem* __restrict__ items,
                                                             double eps, int* err, int smem_w,
                                                             int smem_mn) {
+  const long long ts = clock64();
   const TruncItem& it = items[blockIdx.x];
   lr_update(it, eps, err, smem_w, smem_mn);
   if (it.post_L) {
     __syncthreads();
     lr_post_solve(it);
   }
+  seq_done(ts);
 }
 
 // One CTA per target: its updates items[off[b] .. off[b+1]) run in order (the
@@ -511,10 +534,12 @@ __global__ void __launch_bounds__(kTruncThreads) k_truncate_seq(const TruncItem*
                                                                 const int* __restrict__ off,
                                                                 double eps, int* err, int smem_w,
                                                                 int smem_mn) {
+  const long long ts = clock64();
   for (int i = off[blockIdx.x]; i < off[blockIdx.x + 1]; ++i) {
     lr_update(items[i], eps, err, smem_w, smem_mn);
     __syncthreads();
   }
+  seq_done(ts);
 }
 
 __device__ void lr_update(const TruncItem& it, double eps, int* err, int smem_w, int smem_mn) {
@@ -606,24 +631,48 @@ __device__ void lr_update(const TruncItem& it, double eps, int* err, int smem_w,
         sV[(size_t)(e / n) * n + j] = v;
       }
       __syncthreads();
-      for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
-        const int i = e % m, j = e / m;
-        double s = 0.0;
-        for (int l = 0; l < lc; ++l) s += sU[(size_t)l * m + i] * sV[(size_t)l * n + j];
-        W[e] += s;
+      // W += sU sV^T in 4 x 4 register tiles (8 shared loads per 16 FMAs)
+      const int tmi = (m + 3) >> 2, tiles = tmi * ((n + 3) >> 2);
+      for (int tt = threadIdx.x; tt < tiles; tt += blockDim.x) {
+        const int i0 = (tt % tmi) << 2, j0 = (tt / tmi) << 2;
+        double acc[4][4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+          for (int a = 0; a < 4; ++a) acc[b][a] = 0.0;
+        for (int l = 0; l < lc; ++l) {
+          double u[4], v[4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            u[a] = (i0 + a < m) ? sU[(size_t)l * m + i0 + a] : 0.0;
+            v[a] = (j0 + a < n) ? sV[(size_t)l * n + j0 + a] : 0.0;
+          }
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+#pragma unroll
+            for (int a = 0; a < 4; ++a) acc[b][a] += u[a] * v[b];
+        }
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+            if (i0 + a < m && j0 + b < n) W[(size_t)(j0 + b) * m + i0 + a] += acc[b][a];
       }
     }
     __syncthreads();
     double* ws = it.ws;
     double* tau = ws;
-    double* cn = tau + n;
-    int* piv = reinterpret_cast<int*>(cn + n);
-    double* G = cn + 2 * n;
+    double* cn = tau + n;                                 // 2n (double-buffered in rrqr2)
+    int* piv = reinterpret_cast<int*>(cn + 2 * n);        // n ints
+    int* stepof = piv + n;                                // n ints
+    double* G = cn + 3 * n;
     const int kqmax = min(min(m, n), it.rcap);  // rank(W) <= r <= rcap
     double* J = G + (size_t)n * kqmax;
     long long tc = t0;
     stage_add(0, 0, tc);
-    const RS rs = cta_rrqr_svd(W, m, n, eps, tau, piv, cn, G, J, s_sig, s_ord, red, 0, &tc);
+    const bool lean = n <= 128 && blockDim.x == 512;
+    const RS rs = lean ? cta_rrqr_svd2(W, m, n, eps, tau, piv, cn, stepof, G, J, s_sig, s_ord, 0, &tc)
+                       : cta_rrqr_svd(W, m, n, eps, tau, piv, cn, G, J, s_sig, s_ord, red, 0, &tc);
     if (rs.keep > it.cap) {
       if (threadIdx.x == 0) atomicOr(err, 4);
       return;
@@ -638,7 +687,10 @@ __device__ void lr_update(const TruncItem& it, double eps, int* err, int smem_w,
       it.V[idx] = G[(size_t)src * n + i] / s_sig[src];
     }
     __syncthreads();
-    cta_apply_q(W, m, kq, tau, it.U, keep);
+    if (lean)
+      cta_apply_q_map(W, m, m, kq, tau, piv, it.U, keep);
+    else
+      cta_apply_q(W, m, kq, tau, it.U, keep);
     stage_add(0, 4, tc);
     if (threadIdx.x == 0) {
       *it.rank = keep;
@@ -669,8 +721,11 @@ __device__ void lr_update(const TruncItem& it, double eps, int* err, int smem_w,
   __syncthreads();
   long long tc = t0;
   stage_add(1, 0, tc);
-  cta_householder(WU, m, r, tu, red);
-  cta_householder(WV, n, r, tv, red);
+  {
+    __shared__ double s_tail2[2];
+    smem_qr(WU, m, m, r, tu, s_tail2);  // one barrier per column (generic memory)
+    smem_qr(WV, n, n, r, tv, s_tail2);
+  }
   stage_add(1, 1, tc);
   const int ku = min(m, r), kv = min(n, r);
   // core(i,j) = sum_{l >= max(i,j)} Ru(i,l) Rv(j,l)  (ku x kv, ld ku)
@@ -683,12 +738,15 @@ __device__ void lr_update(const TruncItem& it, double eps, int* err, int smem_w,
   __syncthreads();
   const int kqmax = min(ku, kv);
   double* tau = C + (size_t)ku * kv;
-  double* cn = tau + kv;
-  int* piv = reinterpret_cast<int*>(cn + kv);
-  double* G = cn + 2 * kv;
+  double* cn = tau + kv;                            // 2 kv
+  int* piv = reinterpret_cast<int*>(cn + 2 * kv);   // kv ints
+  int* stepof = piv + kv;                           // kv ints
+  double* G = cn + 3 * kv;
   double* J = G + (size_t)kv * kqmax;
   double* Uc = J + (size_t)kqmax * kqmax;
-  const RS rs = cta_rrqr_svd(C, ku, kv, eps, tau, piv, cn, G, J, s_sig, s_ord, red, 1, &tc);
+  const bool lean = kv <= 128 && blockDim.x == 512;
+  const RS rs = lean ? cta_rrqr_svd2(C, ku, kv, eps, tau, piv, cn, stepof, G, J, s_sig, s_ord, 1, &tc)
+                     : cta_rrqr_svd(C, ku, kv, eps, tau, piv, cn, G, J, s_sig, s_ord, red, 1, &tc);
   if (rs.keep > it.cap) {
     if (threadIdx.x == 0) atomicOr(err, 4);
     return;
@@ -700,7 +758,10 @@ __device__ void lr_update(const TruncItem& it, double eps, int* err, int smem_w,
     Uc[idx] = i < kq ? J[(size_t)src * kq + i] * s_sig[src] : 0.0;
   }
   __syncthreads();
-  cta_apply_q(C, ku, kq, tau, Uc, keep);
+  if (lean)
+    cta_apply_q_map(C, ku, ku, kq, tau, piv, Uc, keep);
+  else
+    cta_apply_q(C, ku, kq, tau, Uc, keep);
   // E_u = [U_core; 0] -> it.U, E_v = [Y; 0] -> it.V, then apply Q_u, Q_v.
   for (int idx = threadIdx.x; idx < m * keep; idx += blockDim.x) {
     const int i = idx % m, c = idx / m;
@@ -851,7 +912,7 @@ __device__ void lr_update_cluster(cg::cluster_group& cl, CluShared& sh, const Tr
   __shared__ double red[32];
   __shared__ double s_sig[kMaxTruncCols];
   __shared__ int s_ord[kMaxTruncCols];
-  __shared__ int s_keep, s_kq;
+  __shared__ int s_kq;
   const int add = it.P ? (it.addp ? *it.addp : it.addv) : 0;
   const int r = r0 + add;
   bool go;
@@ -957,7 +1018,6 @@ __device__ void lr_update_cluster(cg::cluster_group& cl, CluShared& sh, const Tr
       gord[c] = s_ord[c];
     }
     if (threadIdx.x == 0) {
-      s_keep = rs.keep;
       s_kq = rs.kq;
       gord[kqmax] = rs.keep;  // published to the cluster through global memory
     }
@@ -994,46 +1054,6 @@ __device__ void lr_update_cluster(cg::cluster_group& cl, CluShared& sh, const Tr
   cl.sync();
 }
 
-template <bool kFallback>
-__device__ bool lr_update_pair(cg::cluster_group& cl, const TruncItem& it, double eps, int* err,
-                               int cap_dbl, double* sm, bool may_defer, int r0, bool active);
-__device__ __forceinline__ bool pair_fits(int m, int n, int r, int cap_dbl);
-
-// cluster b (CTAs b*kClu .. b*kClu+kClu-1) runs target b's sequence in order
-__global__ void __cluster_dims__(kClu, 1, 1) __launch_bounds__(kTruncThreads)
-    k_truncate_cluster(const TruncItem* __restrict__ items, const int* __restrict__ off, double eps,
-                       int* err, const int* __restrict__ defer, int cap_dbl) {
-  cg::cluster_group cl = cg::this_cluster();
-  __shared__ CluShared sh;
-  extern __shared__ double csm[];
-  const int b = blockIdx.x / kClu;
-  int start = off[b];
-  if (defer) {  // only the sequence tail the pair kernel handed over
-    start = defer[b];
-    if (start < 0) return;
-  }
-  for (int i = start; i < off[b + 1]; ++i) {
-    const TruncItem& it = items[i];
-    const int r0 = *it.rank;
-    // every rank has read rank / compact before any may change them (the
-    // cluster path itself writes them only after its own cluster barriers)
-    if (cap_dbl > 0) cl.sync();
-    // items whose actual column count fits the pair layout run on ranks 0-1
-    bool pair = false;
-    if (cap_dbl > 0) {
-      const int r = r0 + (it.P ? (it.addp ? *it.addp : it.addv) : 0);
-      pair = pair_fits(it.m, it.n, r, cap_dbl);
-    }
-    if (pair)
-      lr_update_pair<false>(cl, it, eps, err, cap_dbl, csm, false, r0, cl.block_rank() < 2);
-    else
-      lr_update_cluster(cl, sh, it, eps, err, r0);
-    if (it.post_L) {
-      if (cl.block_rank() == (pair ? 1 : 0)) lr_post_solve(it);
-      cl.sync();
-    }
-  }
-}
 
 // ===================================================================== //
 // Medium blocks: a CTA PAIR (cluster of 2) per target.  CTA 0 owns the U side,
@@ -1048,7 +1068,6 @@ __global__ void __cluster_dims__(kClu, 1, 1) __launch_bounds__(kTruncThreads)
 // ===================================================================== //
 constexpr int kPairMaxR = 128;
 
-#include "trunc_lean.cuh"
 
 // out (mm x c, ld mm, global) = Q [E0; 0] with Q = H_0 ... H_{k-1} from
 // smem_qr(A) in compact WY form Q = I - Y T Y^T (T upper triangular, the
@@ -1319,6 +1338,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTruncThreads)
   extern __shared__ double psm[];
   const int b = blockIdx.x / 2;
   const bool lead = cl.block_rank() == 0 && threadIdx.x == 0;
+  const long long ts = clock64();
   if (defer && lead) defer[b] = -1;
   for (int i = off[b]; i < off[b + 1]; ++i) {
     const TruncItem& it = items[i];
@@ -1333,6 +1353,69 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTruncThreads)
       cl.sync();
     }
   }
+  if (cl.block_rank() == 0) seq_done(ts);
+}
+
+#include "trunc_dist.cuh"
+
+// cluster b (CTAs b*kClu .. b*kClu+kClu-1) runs target b's sequence in order
+__global__ void __cluster_dims__(kClu, 1, 1) __launch_bounds__(kTruncThreads)
+    k_truncate_cluster(const TruncItem* __restrict__ items, const int* __restrict__ off, double eps,
+                       int* err, const int* __restrict__ defer, int cap_dbl) {
+  cg::cluster_group cl = cg::this_cluster();
+  __shared__ CluShared sh;
+  __shared__ double s_sig_d[64];
+  __shared__ int s_ord_d[64];
+  extern __shared__ double csm[];
+  // the register path's exchange area sits at the end of the dynamic region
+  // (same offset in every CTA, so DSMEM addresses line up)
+  constexpr int kDsDbl = (int)((sizeof(DistShared) + 7) / 8);
+  DistShared& dsh = *reinterpret_cast<DistShared*>(csm + max(cap_dbl - kDsDbl, 0));
+  const int cap_dist = cap_dbl - kDsDbl;
+  const long long ts = clock64();
+  const int b = blockIdx.x / kClu;
+  int start = off[b];
+  if (defer) {  // only the sequence tail the pair kernel handed over
+    start = defer[b];
+    if (start < 0) return;
+  }
+  for (int i = start; i < off[b + 1]; ++i) {
+    const TruncItem& it = items[i];
+    const int r0 = *it.rank;
+    // every rank has read rank / compact before any may change them (the
+    // cluster path itself writes them only after its own cluster barriers)
+    if (cap_dbl > 0) cl.sync();
+    // with a shared-memory carve-out (cap_dbl > 0), items whose actual column
+    // count fits run on ranks 0-1 as a pair, or register-resident over all
+    // eight ranks; the rest take the global-memory cluster path
+    bool pair = false, dist = false;
+    if (cap_dbl > 0) {
+      const int add = it.P ? (it.addp ? *it.addp : it.addv) : 0;
+      const int r = r0 + add;
+      bool go;
+      switch (it.cond) {
+        case 1: go = r > 16; break;
+        case 2: go = r > *it.compact + 16; break;
+        case 3: go = r > 48; break;
+        case 4: go = false; break;
+        default: go = r > 0; break;
+      }
+      if (go && r <= it.rcap) {
+        pair = pair_fits(it.m, it.n, r, cap_dbl);
+        dist = !pair && dist_fits(it.m, it.n, r, cap_dist);
+        if (dist) lr_update_dist_any(cl, it, eps, err, r0, r, add, csm, dsh, s_sig_d, s_ord_d);
+      }
+    }
+    if (pair)
+      lr_update_pair<false>(cl, it, eps, err, cap_dbl, csm, false, r0, cl.block_rank() < 2);
+    else if (!dist)
+      lr_update_cluster(cl, sh, it, eps, err, r0);
+    if (it.post_L) {
+      if (cl.block_rank() == (pair ? 1 : 0)) lr_post_solve(it);
+      cl.sync();
+    }
+  }
+  if (cl.block_rank() == 0) seq_done(ts);
 }
 
 static int g_pair_cap = -1;
@@ -1372,9 +1455,10 @@ void launch_truncate_pair(const TruncItem* d_items, const int* d_off, int target
   }
 }
 
-size_t trunc_ws_doubles_pair(int m, int n, int rcap) {  // the global-memory fallback
+size_t trunc_ws_doubles_pair(int m, int n, int rcap) {  // the single-CTA fallbacks (either path)
   const size_t rc = (size_t)rcap, kq = std::min((size_t)std::min(m, n), rc);
-  return (size_t)(m + n) * rc + 5 * rc + rc * rc + 2 * rc * kq + kq * kq;
+  return std::max(trunc_ws_doubles(m, n, rcap),
+                  (size_t)(m + n) * rc + 6 * rc + rc * rc + 2 * rc * kq + kq * kq);
 }
 
 bool trunc_use_pair(int m, int n, int rcap) {
@@ -1406,17 +1490,34 @@ size_t trunc_ws_doubles_cluster(int m, int n, int rcap) {
   return (size_t)(m + n) * rc + 5 * rc + rc * rc + 3 * rc * kq + kq * kq + 2 * kq + 2;
 }
 
+bool trunc_cluster_resident(int m, int n) { return std::max(m, n) <= 2048; }
+
 bool trunc_use_cluster(int m, int n) {
   return !((size_t)m * n <= (size_t)kMaxSmemW && m + n <= kMaxSmemMN) && std::max(m, n) >= 512;
 }
 
 void launch_truncate_cluster(const TruncItem* d_items, const int* d_off, int targets, double eps,
-                             int* d_err, cudaStream_t st) {
+                             int* d_err, cudaStream_t st, bool resident) {
   if (targets <= 0) return;
-  // No pair-layout dispatch here (cap_dbl = 0): the global-memory cluster path
-  // depends on L1 holding its row slices, and a pair-sized dynamic
-  // shared-memory carve-out would take that L1 away from every item.
-  k_truncate_cluster<<<targets * kClu, kTruncThreads, 0, st>>>(d_items, d_off, eps, d_err, nullptr, 0);
+  // resident = false: no shared-memory carve-out (cap_dbl = 0), everything on the
+  // global-memory cluster path, which depends on L1 holding its row slices.
+  // resident = true: pair / register-resident dispatch per item (targets up to
+  // 2048 rows, where most items fit).
+  static int cap = -1;
+  static size_t bytes = 0;
+  if (resident && cap < 0) {
+    cudaFuncAttributes fa;
+    HMGP_CUDA(cudaFuncGetAttributes(&fa, k_truncate_cluster));
+    int dev = 0, optin = 0;
+    HMGP_CUDA(cudaGetDevice(&dev));
+    HMGP_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    bytes = (size_t)optin - fa.sharedSizeBytes - 1024;
+    HMGP_CUDA(cudaFuncSetAttribute(k_truncate_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)bytes));
+    cap = (int)(bytes / 8);
+  }
+  k_truncate_cluster<<<targets * kClu, kTruncThreads, resident ? bytes : 0, st>>>(
+      d_items, d_off, eps, d_err, nullptr, resident ? cap : 0);
   HMGP_LAUNCH_CHECK();
 }
 
