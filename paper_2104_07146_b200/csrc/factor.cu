@@ -14,6 +14,7 @@
 // hfactor.cpp:170) are evaluated inside the update kernel.  Temporaries come from
 // a stream-ordered stack arena with structural capacity bounds.
 #include <algorithm>
+#include <functional>
 #include <climits>
 #include <cmath>
 #include <cstring>
@@ -225,11 +226,43 @@ struct Engine {
     st_next[2] = items;
     st_next[3] = std::max(st_next[3], seq);
   }
-  // Cluster targets: those up to 2048 rows run with the resident (pair /
-  // register) dispatch, larger ones on the global-memory path without a
-  // shared-memory carve-out; the two launches are independent and run on the
-  // main and a side stream (fork / join through events).
-  void cluster_launch(const std::vector<TruncItem>& items, const std::vector<int>& off) {
+  // Independent launches (disjoint targets) queued as jobs: job 0 runs on the
+  // main stream, the others on side streams forked from it and joined back
+  // through events, so one step costs its slowest group rather than the sum.
+  // Stats mode runs them in order on the main stream so that the per-launch
+  // timing stays attributable.
+  std::vector<std::function<void(cudaStream_t)>> jobs;
+  void run_jobs() {
+    if (jobs.empty()) return;
+    if (jobs.size() == 1 || stats_on) {
+      for (auto& j : jobs) j(st);
+      jobs.clear();
+      return;
+    }
+    constexpr int kSide = 7;
+    static thread_local cudaStream_t side[kSide] = {};
+    static thread_local cudaEvent_t evf = nullptr, evj[kSide] = {};
+    if (!side[0]) {
+      HMGP_CUDA(cudaEventCreateWithFlags(&evf, cudaEventDisableTiming));
+      for (int i = 0; i < kSide; ++i) {
+        HMGP_CUDA(cudaStreamCreateWithFlags(&side[i], cudaStreamNonBlocking));
+        HMGP_CUDA(cudaEventCreateWithFlags(&evj[i], cudaEventDisableTiming));
+      }
+    }
+    const int ns = std::min((int)jobs.size() - 1, kSide);
+    HMGP_CUDA(cudaEventRecord(evf, st));
+    for (int i = 0; i < ns; ++i) HMGP_CUDA(cudaStreamWaitEvent(side[i], evf, 0));
+    for (size_t k = 1; k < jobs.size(); ++k) jobs[k](side[(k - 1) % kSide]);
+    for (int i = 0; i < ns; ++i) HMGP_CUDA(cudaEventRecord(evj[i], side[i]));
+    jobs[0](st);
+    for (int i = 0; i < ns; ++i) HMGP_CUDA(cudaStreamWaitEvent(st, evj[i], 0));
+    jobs.clear();
+  }
+
+  // Cluster targets: those up to 2048 rows with the resident (pair / register)
+  // dispatch, larger ones on the global-memory path without a shared-memory
+  // carve-out; queued as two independent jobs.
+  void cluster_jobs(const std::vector<TruncItem>& items, const std::vector<int>& off) {
     std::vector<TruncItem> ir, ig;
     std::vector<int> offr{0}, offg{0};
     for (size_t b = 0; b + 1 < off.size(); ++b) {
@@ -239,71 +272,76 @@ struct Engine {
       for (int i = off[b]; i < off[b + 1]; ++i) dst.push_back(items[i]);
       (res ? offr : offg).push_back((int)dst.size());
     }
-    const TruncItem* dr = ir.empty() ? nullptr : sg.put(ir);
-    const int* dor = ir.empty() ? nullptr : sg.put(offr);
-    const TruncItem* dg = ig.empty() ? nullptr : sg.put(ig);
-    const int* dog = ig.empty() ? nullptr : sg.put(offg);
-    if (dr && dg) {
-      static thread_local cudaStream_t st2 = nullptr;
-      static thread_local cudaEvent_t evf = nullptr, evj = nullptr;
-      if (!st2) {
-        HMGP_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
-        HMGP_CUDA(cudaEventCreateWithFlags(&evf, cudaEventDisableTiming));
-        HMGP_CUDA(cudaEventCreateWithFlags(&evj, cudaEventDisableTiming));
-      }
-      HMGP_CUDA(cudaEventRecord(evf, st));
-      HMGP_CUDA(cudaStreamWaitEvent(st2, evf, 0));
-      launch_truncate_cluster(dg, dog, (int)offg.size() - 1, eps, d_err, st2, false);
-      HMGP_CUDA(cudaEventRecord(evj, st2));
-      launch_truncate_cluster(dr, dor, (int)offr.size() - 1, eps, d_err, st, true);
-      HMGP_CUDA(cudaStreamWaitEvent(st, evj, 0));
-    } else if (dr) {
-      launch_truncate_cluster(dr, dor, (int)offr.size() - 1, eps, d_err, st, true);
-    } else if (dg) {
-      launch_truncate_cluster(dg, dog, (int)offg.size() - 1, eps, d_err, st, false);
+    const double e = eps;
+    int* er = d_err;
+    if (!ir.empty()) {
+      const TruncItem* dr = sg.put(ir);
+      const int* dor = sg.put(offr);
+      const int nr = (int)offr.size() - 1;
+      jobs.push_back([=](cudaStream_t s) { launch_truncate_cluster(dr, dor, nr, e, er, s, true); });
+    }
+    if (!ig.empty()) {
+      const TruncItem* dg = sg.put(ig);
+      const int* dog = sg.put(offg);
+      const int ng = (int)offg.size() - 1;
+      jobs.push_back([=](cudaStream_t s) { launch_truncate_cluster(dg, dog, ng, e, er, s, false); });
     }
   }
 
   void lrupd(std::vector<TruncItem>& v0) {
     if (v0.empty()) return;
     // large blocks -> one 8-CTA cluster each, medium -> one CTA pair each, the
-    // rest -> one CTA each
+    // rest -> one CTA each; the groups touch disjoint targets and run as jobs
     std::vector<TruncItem> v, big, mid, dfr;
     for (const TruncItem& t : v0) {
       const int rt = t.cond == 4 ? 0 : trunc_route(t.m, t.n, t.rcap);
       (rt == 2 ? big : rt == 1 ? mid : rt == 3 ? dfr : v).push_back(t);
     }
     v0.clear();
+    const double e = eps;
+    int* er = d_err;
+    size_t nitems = 0;
+    std::array<int, 5> mt{};
     for (int pass = 0; pass < 3; ++pass) {
       std::vector<TruncItem>& grp = pass == 2 ? dfr : pass ? mid : big;
       if (grp.empty()) continue;
       std::vector<int> off(grp.size() + 1);
       for (size_t i = 0; i <= grp.size(); ++i) off[i] = (int)i;
-      tslot();
-      if (pass)
-        launch_truncate_pair(sg.put(grp), sg.put(off), (int)grp.size(), eps, d_err, st, pass == 2);
-      else
-        cluster_launch(grp, off);
-      st_next = {};
-      for (const TruncItem& t : grp) {
-        st_next[0] = std::min(st_next[0], -t.m);
-        st_next[1] = std::max(st_next[1], t.n);
+      if (pass) {
+        const TruncItem* di = sg.put(grp);
+        const int* doff = sg.put(off);
+        const int cnt = (int)grp.size();
+        const bool dfer = pass == 2;
+        jobs.push_back([=](cudaStream_t s) { launch_truncate_pair(di, doff, cnt, e, er, s, dfer); });
+      } else {
+        cluster_jobs(grp, off);
       }
-      st_next[2] = (int)grp.size();
-      st_next[3] = 1;
-      stat(S_TRUNC, grp.size());
+      for (const TruncItem& t : grp) {
+        mt[0] = std::min(mt[0], -t.m);
+        mt[1] = std::max(mt[1], t.n);
+      }
+      nitems += grp.size();
     }
-    if (v.empty()) return;
-    int sw = 0, smn = 0;
-    st_next = {};
-    for (const TruncItem& t : v) {
-      if (t.cond != 4) trunc_smem_dims(t.m, t.n, &sw, &smn);
-      if (stats_on) note_dims(t.m, t.n, (int)v.size(), 1);
+    if (!v.empty()) {
+      int sw = 0, smn = 0;
+      for (const TruncItem& t : v) {
+        if (t.cond != 4) trunc_smem_dims(t.m, t.n, &sw, &smn);
+        mt[0] = mt[0] < 0 ? mt[0] : std::max(mt[0], t.m);
+        mt[1] = std::max(mt[1], t.n);
+      }
+      const TruncItem* di = sg.put(v);
+      const int cnt = (int)v.size();
+      jobs.push_back([=](cudaStream_t s) { launch_truncate(di, cnt, e, er, s, sw, smn); });
+      nitems += v.size();
+      v.clear();
     }
+    if (jobs.empty()) return;
     tslot();
-    launch_truncate(sg.put(v), (int)v.size(), eps, d_err, st, sw, smn);
-    stat(S_TRUNC, v.size());
-    v.clear();
+    run_jobs();
+    mt[2] = (int)nitems;
+    mt[3] = 1;
+    st_next = mt;
+    stat(S_TRUNC, nitems);
   }
   void print_stats() const {
     static const char* nm[S_N] = {"gemm", "copy", "lrupd", "trsm_left", "trsm_right", "leaf"};
@@ -838,36 +876,64 @@ struct Engine {
         }
       }
     }
+    // the four groups touch disjoint targets: queue them as concurrent jobs
+    const double e = eps;
+    int* er = d_err;
+    size_t ntr = 0;
+    std::array<int, 5> mt{};
     if (!g.empty()) {
-      launch_gemm_seq(sg.put(g), sg.put(goff), (int)goff.size() - 1, st);
-      stat(S_GEMM, g.size());
+      const GemmItem* dg = sg.put(g);
+      const int* dgo = sg.put(goff);
+      const int ng = (int)goff.size() - 1;
+      jobs.push_back([=](cudaStream_t s) { launch_gemm_seq(dg, dgo, ng, s); });
+      st_launch[S_GEMM]++;
+      st_items[S_GEMM] += (long long)g.size();
     }
     if (!tb.empty()) {
-      tslot();
-      cluster_launch(tb, tboff);
-      st_next = meta_b;
-      st_next[0] = -st_next[0];  // negative m marks a cluster launch
-      stat(S_TRUNC, tb.size());
+      cluster_jobs(tb, tboff);
+      ntr += tb.size();
+      mt[0] = std::min(mt[0], -meta_b[0]);
+      mt[1] = std::max(mt[1], meta_b[1]);
+      mt[3] = std::max(mt[3], meta_b[3]);
     }
-    if (!tp.empty()) {
-      tslot();
-      launch_truncate_pair(sg.put(tp), sg.put(tpoff), (int)tpoff.size() - 1, eps, d_err, st);
-      st_next = meta_p;
-      st_next[0] = -st_next[0];
-      stat(S_TRUNC, tp.size());
-    }
-    if (!td.empty()) {
-      tslot();
-      launch_truncate_pair(sg.put(td), sg.put(tdoff), (int)tdoff.size() - 1, eps, d_err, st, true);
-      st_next = meta_d;
-      st_next[0] = -st_next[0];
-      stat(S_TRUNC, td.size());
+    for (int pass = 0; pass < 2; ++pass) {
+      const std::vector<TruncItem>& tq = pass ? td : tp;
+      const std::vector<int>& to = pass ? tdoff : tpoff;
+      const std::array<int, 5>& mq = pass ? meta_d : meta_p;
+      if (tq.empty()) continue;
+      const TruncItem* di = sg.put(tq);
+      const int* doff = sg.put(to);
+      const int cnt = (int)to.size() - 1;
+      const bool dfer = pass == 1;
+      jobs.push_back([=](cudaStream_t s) { launch_truncate_pair(di, doff, cnt, e, er, s, dfer); });
+      ntr += tq.size();
+      mt[0] = std::min(mt[0], -mq[0]);
+      mt[1] = std::max(mt[1], mq[1]);
+      mt[3] = std::max(mt[3], mq[3]);
     }
     if (!t.empty()) {
-      tslot();
-      launch_truncate_seq(sg.put(t), sg.put(toff), (int)toff.size() - 1, eps, d_err, st, sw, smn);
-      st_next = meta_t;
-      stat(S_TRUNC, t.size());
+      const TruncItem* di = sg.put(t);
+      const int* doff = sg.put(toff);
+      const int cnt = (int)toff.size() - 1;
+      jobs.push_back([=](cudaStream_t s) { launch_truncate_seq(di, doff, cnt, e, er, s, sw, smn); });
+      ntr += t.size();
+      if (mt[0] >= 0) mt[0] = std::max(mt[0], meta_t[0]);
+      mt[1] = std::max(mt[1], meta_t[1]);
+      mt[3] = std::max(mt[3], meta_t[3]);
+    }
+    if (!jobs.empty()) {
+      if (ntr) tslot();
+      run_jobs();
+      if (ntr) {
+        mt[2] = (int)ntr;
+        st_next = mt;
+        stat(S_TRUNC, ntr);
+        st_launch[S_TRUNC] += 0;
+      } else {
+        st_launch[S_GEMM]--;  // counted above; record the event against gemm
+        st_items[S_GEMM] -= (long long)g.size();
+        stat(S_GEMM, g.size());
+      }
     }
     ar.release(mk);
   }
