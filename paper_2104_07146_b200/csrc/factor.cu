@@ -38,14 +38,18 @@ struct Arena {
   size_t cap = 0, top = 0, peak = 0;
   void init(size_t bytes) {  // persistent: reallocate only to grow
     top = peak = 0;
+    hold = 0;
     if (base && cap >= bytes) return;
     if (base) cudaFree(base);
     base = nullptr;
     cap = bytes;
     HMGP_CUDA(cudaMalloc(&base, cap));
   }
+  int hold = 0;  // > 0 while a side-stream section is being enqueued: no reuse
   size_t mark() const { return top; }
-  void release(size_t m) { top = m; }
+  void release(size_t m) {
+    if (!hold) top = m;
+  }
   void* raw(size_t bytes) {
     const size_t a = (top + 255) & ~size_t(255);
     if (a + bytes > cap) throw Error(6, "factorize: device temporary arena exhausted");
@@ -62,9 +66,15 @@ struct Stager {
   char* h = nullptr;
   char* d = nullptr;
   size_t cap = 0, off = 0;
-  cudaStream_t st = nullptr;
+  cudaStream_t st = nullptr;          // stream of the next copy (the engine's current one)
+  std::vector<cudaStream_t> used;     // streams that may still read the ring
+  void use(cudaStream_t s) {
+    st = s;
+    if (std::find(used.begin(), used.end(), s) == used.end()) used.push_back(s);
+  }
   void init(size_t bytes, cudaStream_t s) {  // persistent across factorizations
     st = s;
+    used.assign(1, s);
     off = 0;
     if (h) return;
     cap = bytes;
@@ -75,8 +85,9 @@ struct Stager {
   const T* put(const std::vector<T>& v) {
     const size_t bytes = (v.size() * sizeof(T) + 255) & ~size_t(255);
     if (bytes > cap) throw Error(6, "item batch exceeds staging ring");
-    if (off + bytes > cap) {
-      HMGP_CUDA(cudaStreamSynchronize(st));
+    if (off + bytes > cap) {  // wrap: every stream that read the ring must be done
+      for (cudaStream_t s : used) HMGP_CUDA(cudaStreamSynchronize(s));
+      used.assign(1, st);
       off = 0;
     }
     std::memcpy(h + off, v.data(), v.size() * sizeof(T));
@@ -257,6 +268,72 @@ struct Engine {
     jobs[0](st);
     for (int i = 0; i < ns; ++i) HMGP_CUDA(cudaStreamWaitEvent(st, evj[i], 0));
     jobs.clear();
+  }
+
+  // Side-stream sections: independent parts of a recursion step (disjoint
+  // targets) are enqueued on their own stream, forked from the current one,
+  // and joined back before the step returns.  While a section is enqueued the
+  // arena does not reuse memory (its kernels may still run); the caller
+  // releases after the join.  Stats mode runs everything in order.
+  struct Sec {
+    cudaStream_t s;
+    cudaEvent_t done;
+  };
+  bool sections_on = !stats_on && getenv("HMGP_SERIAL") == nullptr;
+  cudaStream_t sec_stream() {
+    constexpr int kPool = 12;
+    static thread_local cudaStream_t pool[kPool] = {};
+    static thread_local int next = 0;
+    cudaStream_t& s = pool[next];
+    next = (next + 1) % kPool;
+    if (!s) HMGP_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    return s;
+  }
+  static std::vector<cudaEvent_t>& ev_pool() {
+    static thread_local std::vector<cudaEvent_t> p;
+    return p;
+  }
+  cudaEvent_t ev_get() {
+    auto& p = ev_pool();
+    if (p.empty()) {
+      cudaEvent_t e;
+      HMGP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      return e;
+    }
+    cudaEvent_t e = p.back();
+    p.pop_back();
+    return e;
+  }
+  void ev_put(cudaEvent_t e) { ev_pool().push_back(e); }
+  template <class Fn>
+  void section(std::vector<Sec>& secs, Fn&& fn) {
+    if (!sections_on) {
+      fn();
+      return;
+    }
+    cudaEvent_t fe = ev_get();
+    HMGP_CUDA(cudaEventRecord(fe, st));
+    const cudaStream_t s = sec_stream();
+    HMGP_CUDA(cudaStreamWaitEvent(s, fe, 0));
+    ev_put(fe);  // the wait captured the record; the event may be recorded again
+    const cudaStream_t saved = st;
+    st = s;
+    sg.use(s);
+    ++ar.hold;
+    fn();
+    --ar.hold;
+    cudaEvent_t de = ev_get();
+    HMGP_CUDA(cudaEventRecord(de, s));
+    st = saved;
+    sg.use(saved);
+    secs.push_back(Sec{s, de});
+  }
+  void join(std::vector<Sec>& secs) {
+    for (const Sec& x : secs) {
+      HMGP_CUDA(cudaStreamWaitEvent(st, x.done, 0));
+      ev_put(x.done);
+    }
+    secs.clear();
   }
 
   // Cluster targets: those up to 2048 rows with the resident (pair / register)
@@ -702,53 +779,70 @@ struct Engine {
     if (xs.empty()) return;
     std::vector<int> lr, dn, br;
     for (int x : xs) (kind(x) == LOWRANK ? lr : kind(x) == DENSE ? dn : br).push_back(x);
+    // the low-rank, dense and branch targets are disjoint: the first two run as
+    // side-stream sections while the branch recursion proceeds on this stream
+    const size_t mk0 = ar.mark();
+    std::vector<Sec> secs;
+    const int parts = !lr.empty() + !dn.empty() + !br.empty();
+    auto part = [&](bool last, auto&& fn) {
+      if (parts > 1 && !last)
+        section(secs, fn);
+      else
+        fn();
+    };
     if (kind(l) == DENSE) {
       const LeafDev& L = LF(l);
-      if (!lr.empty()) {
-        // compress_low_rank + V <- L^{-1} V (+ D^{-1}) fused in one launch
-        const size_t mk = ar.mark();
-        std::vector<TruncItem> v;
-        for (int x : lr) {
-          const LeafDev& lx = LF(x);
-          TruncItem t = lritem(lx.a, lx.b, lx.m, lx.n, rankp(x), compp(x), 0, lx.cap, nullptr,
-                               nullptr, 0, 0, 1.0, lx.cap);
-          t.post_L = L.a;
-          t.post_ldl_ld = L.m;
-          t.post_d = ldl ? dseg(rb(l)) : nullptr;
-          v.push_back(t);
-        }
-        lrupd_ws(v);
-        ar.release(mk);
-      }
-      if (!dn.empty()) {
-        std::vector<MV> d;
-        for (int x : dn) d.push_back(Dv(x));
-        trsm_dense(d, l);
-      }
+      if (!lr.empty())
+        part(dn.empty() && br.empty(), [&] {
+          // compress_low_rank + V <- L^{-1} V (+ D^{-1}) fused in one launch
+          const size_t mk = ar.mark();
+          std::vector<TruncItem> v;
+          for (int x : lr) {
+            const LeafDev& lx = LF(x);
+            TruncItem t = lritem(lx.a, lx.b, lx.m, lx.n, rankp(x), compp(x), 0, lx.cap, nullptr,
+                                 nullptr, 0, 0, 1.0, lx.cap);
+            t.post_L = L.a;
+            t.post_ldl_ld = L.m;
+            t.post_d = ldl ? dseg(rb(l)) : nullptr;
+            v.push_back(t);
+          }
+          lrupd_ws(v);
+          ar.release(mk);
+        });
+      if (!dn.empty())
+        part(br.empty(), [&] {
+          std::vector<MV> d;
+          for (int x : dn) d.push_back(Dv(x));
+          trsm_dense(d, l);
+        });
       if (!br.empty()) {
         std::vector<int> ch;
         for (int x : br)
           for (int i = 0; i < N(x).kr; ++i) ch.push_back(kid(x, i, 0));
         trsm(ch, l);
       }
+      join(secs);
+      ar.release(mk0);
       return;
     }
-    if (!lr.empty()) {
-      compress(lr);
-      std::vector<MV> vs;
-      for (int x : lr) vs.push_back(Vv(x));
-      solve_lower_multi(l, vs);
-      if (ldl) {
-        std::vector<CopyScaleItem> c;
-        for (const MV& V : vs) c.push_back(cpy(V.p, V.ld, V, V.cols, 0, 1.0, dseg(rb(l)), 2));
-        copy(c);
-      }
-    }
-    if (!dn.empty()) {
-      std::vector<MV> d;
-      for (int x : dn) d.push_back(Dv(x));
-      trsm_dense(d, l);
-    }
+    if (!lr.empty())
+      part(dn.empty() && br.empty(), [&] {
+        compress(lr);
+        std::vector<MV> vs;
+        for (int x : lr) vs.push_back(Vv(x));
+        solve_lower_multi(l, vs);
+        if (ldl) {
+          std::vector<CopyScaleItem> c;
+          for (const MV& V : vs) c.push_back(cpy(V.p, V.ld, V, V.cols, 0, 1.0, dseg(rb(l)), 2));
+          copy(c);
+        }
+      });
+    if (!dn.empty())
+      part(br.empty(), [&] {
+        std::vector<MV> d;
+        for (int x : dn) d.push_back(Dv(x));
+        trsm_dense(d, l);
+      });
     if (!br.empty()) {
       std::vector<int> l0, l1;
       std::vector<Trip> tr;
@@ -762,6 +856,8 @@ struct Engine {
       subprod(tr);
       trsm(l1, kid(l, 1, 1));
     }
+    join(secs);
+    ar.release(mk0);
   }
 
   // ------------------------------------------------------ add_low_rank ---

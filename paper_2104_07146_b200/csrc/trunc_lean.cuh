@@ -185,7 +185,11 @@ __device__ void cta_apply_q_map(const double* QR, int m, int ldq, int kq, const 
 
 // One-sided Jacobi with the rotations and stopping rule of cta_jacobi; the
 // three dot products of a pair are reduced together, one barrier per round.
-__device__ double cta_jacobi2(double* W, int p, int q, double* J, int* sweeps_out) {
+// tol: rotate a pair while |w_a . w_b| > tol * |w_a| |w_b|.  R = J G^T holds
+// exactly whatever the convergence state, so the truncation error is bounded by
+// the norms of the dropped columns in any case; a tolerance tied to the cut
+// (tol <= 1e-4 eps) only spares the final sweeps.
+__device__ double cta_jacobi2(double* W, int p, int q, double* J, int* sweeps_out, double tol) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int idx = threadIdx.x; idx < q * q; idx += blockDim.x) J[idx] = (idx % (q + 1) == 0) ? 1.0 : 0.0;
   __shared__ unsigned s_nrot2;
@@ -197,6 +201,7 @@ __device__ double cta_jacobi2(double* W, int p, int q, double* J, int* sweeps_ou
   }
   const int qq = q + (q & 1);
   const int m1 = qq - 1;
+  const double tol2 = tol * tol;
   unsigned nrot = 0;
   int sweeps = 0;
   for (int sweep = 0; sweep < 60; ++sweep) {
@@ -232,7 +237,7 @@ __device__ double cta_jacobi2(double* W, int p, int q, double* J, int* sweeps_ou
         warp_sum_n<3>(sv);
         const double sa = sv[0], sb = sv[1], sc = sv[2];
         // |sc| <= 1e-15 sqrt(sa sb), squared (sa, sb >= 0)
-        if (sc * sc <= 1e-30 * (sa * sb) || sc == 0.0) continue;
+        if (sc * sc <= tol2 * (sa * sb) || sc == 0.0) continue;
         rot = 1;
         ++nrot;
         // tan of the rotation angle, zeta = (sb - sa) / (2 sc):
@@ -425,7 +430,7 @@ __device__ RS cta_rrqr_svd2(double* W, int p, int q, double eps, double* tau, in
   }
   __syncthreads();
   __shared__ int s_sweeps2;
-  flops += cta_jacobi2(G, q, kq, J, &s_sweeps2);
+  flops += cta_jacobi2(G, q, kq, J, &s_sweeps2, fmax(1e-15, fmin(1e-10, 1e-4 * eps)));
   if (tclk) {
     stage_add(path, 3, *tclk);
     if (d_hist_on && threadIdx.x == 0) {
