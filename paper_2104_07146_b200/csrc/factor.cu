@@ -365,6 +365,58 @@ struct Engine {
     }
   }
 
+  // Ordered sequences of updates, one target per sequence (e.g. the kk = 0, 1
+  // accumulations of a product part): one job per route, every sequence runs in
+  // order on its CTA(s), the targets concurrently.  Workspaces from the arena
+  // (the caller releases).
+  void lrupd_seq(const std::vector<std::vector<TruncItem>>& seqs) {
+    std::vector<TruncItem> t, tp, tb;
+    std::vector<int> toff{0}, tpoff{0}, tboff{0};
+    int sw = 0, smn = 0;
+    size_t nitems = 0;
+    for (const auto& sq : seqs) {
+      if (sq.empty()) continue;
+      const TruncItem& h = sq[0];
+      int rcap = 0;
+      bool append_only = true;
+      for (const TruncItem& x : sq) {
+        rcap = std::max(rcap, x.rcap);
+        append_only = append_only && x.cond == 4;
+      }
+      const int rt = append_only ? 0 : trunc_route(h.m, h.n, rcap);
+      double* ws = append_only ? nullptr : ar.dbl(trunc_ws_for(h.m, h.n, rcap));
+      std::vector<TruncItem>& dst = rt == 2 ? tb : rt == 1 || rt == 3 ? tp : t;
+      for (TruncItem x : sq) {
+        x.ws = ws;
+        dst.push_back(x);
+        if (x.cond != 4 && rt == 0) trunc_smem_dims(x.m, x.n, &sw, &smn);
+      }
+      (rt == 2 ? tboff : rt == 1 || rt == 3 ? tpoff : toff).push_back((int)dst.size());
+      nitems += sq.size();
+    }
+    if (!nitems) return;
+    const double e = eps;
+    int* er = d_err;
+    if (!tb.empty()) cluster_jobs(tb, tboff);
+    if (!tp.empty()) {
+      const TruncItem* di = sg.put(tp);
+      const int* doff = sg.put(tpoff);
+      const int cnt = (int)tpoff.size() - 1;
+      jobs.push_back([=](cudaStream_t s) { launch_truncate_pair(di, doff, cnt, e, er, s, false); });
+    }
+    if (!t.empty()) {
+      const TruncItem* di = sg.put(t);
+      const int* doff = sg.put(toff);
+      const int cnt = (int)toff.size() - 1;
+      jobs.push_back([=](cudaStream_t s) { launch_truncate_seq(di, doff, cnt, e, er, s, sw, smn); });
+    }
+    tslot();
+    run_jobs();
+    st_next = {};
+    st_next[2] = (int)nitems;
+    stat(S_TRUNC, nitems);
+  }
+
   void lrupd(std::vector<TruncItem>& v0) {
     if (v0.empty()) return;
     // large blocks -> one 8-CTA cluster each, medium -> one CTA pair each, the
@@ -1126,8 +1178,12 @@ struct Engine {
       }
     }
     const size_t mk = ar.mark();
-    // simple cases
-    {
+    // simple cases; independent of the branch x branch products below, so they
+    // run as a side-stream section when both kinds are present
+    std::vector<Sec> psecs;
+    bool any_simple = false, any_branch = false;
+    for (size_t i = 0; i < n; ++i) (cls[i] == 4 ? any_branch : any_simple) = true;
+    auto simple = [&] {
       std::vector<int> mb;
       std::vector<MV> mx, my;
       std::vector<CopyScaleItem> c;
@@ -1187,6 +1243,12 @@ struct Engine {
       }
       copy(c);
       if (!mb.empty()) multiply_into(mb, mx, my);
+    };
+    if (any_simple) {
+      if (any_branch)
+        section(psecs, simple);
+      else
+        simple();
     }
     // branch x branch (hfactor.cpp:150-190)
     std::vector<size_t> bi;
@@ -1237,18 +1299,16 @@ struct Engine {
       if (!sub.empty()) {
         const size_t mk2 = ar.mark();
         std::vector<Pair> tp = product_lr(sub);
-        for (int kk = 0; kk < 2; ++kk) {
-          std::vector<TruncItem> upd;
-          const size_t mk3 = ar.mark();
+        // per part: kk = 0 then kk = 1, one launch of ordered sequences
+        std::vector<std::vector<TruncItem>> seqs(parts.size());
+        for (int kk = 0; kk < 2; ++kk)
           for (size_t s = 0; s < sub.size(); ++s) {
             if (whokk[s] != kk) continue;
             Part& pt = parts[who[s]];
-            upd.push_back(lritem(pt.p.p, pt.q.p, pt.p.rows, pt.q.rows, pt.cols, nullptr, 3, TCAP,
-                                 &tp[s].p, &tp[s].q, 0, 0, 1.0, TCAP + tp[s].p.cols.v));
+            seqs[who[s]].push_back(lritem(pt.p.p, pt.q.p, pt.p.rows, pt.q.rows, pt.cols, nullptr, 3, TCAP,
+                                          &tp[s].p, &tp[s].q, 0, 0, 1.0, TCAP + tp[s].p.cols.v));
           }
-          lrupd_ws(upd);
-          ar.release(mk3);
-        }
+        lrupd_seq(seqs);
         ar.release(mk2);
       }
       // embed parts into out (pure appends; one launch per part index so the
@@ -1257,18 +1317,21 @@ struct Engine {
       std::vector<std::vector<size_t>> byitem(n);
       for (size_t t = 0; t < parts.size(); ++t) byitem[parts[t].item].push_back(t);
       for (size_t i : bi) maxparts = std::max(maxparts, byitem[i].size());
-      for (size_t q = 0; q < maxparts; ++q) {
-        std::vector<TruncItem> ap;
+      {  // per item: its parts appended in order (one launch of sequences)
+        std::vector<std::vector<TruncItem>> seqs;
         for (size_t i : bi) {
-          if (q >= byitem[i].size()) continue;
-          const Part& pt = parts[byitem[i][q]];
-          const int a = abs[i].first, b = abs[i].second;
-          ap.push_back(lritem(out[i].p.p, out[i].q.p, nr(a), nr(b), const_cast<int*>(out[i].p.cols.p),
-                              nullptr, 4, TCAP, &pt.p, &pt.q, rb(pt.a0) - rb(a), rb(pt.b0) - rb(b), 1.0,
-                              TCAP));
+          seqs.emplace_back();
+          for (size_t q = 0; q < byitem[i].size(); ++q) {
+            const Part& pt = parts[byitem[i][q]];
+            const int a = abs[i].first, b = abs[i].second;
+            seqs.back().push_back(lritem(out[i].p.p, out[i].q.p, nr(a), nr(b),
+                                         const_cast<int*>(out[i].p.cols.p), nullptr, 4, TCAP, &pt.p, &pt.q,
+                                         rb(pt.a0) - rb(a), rb(pt.b0) - rb(b), 1.0, TCAP));
+          }
         }
-        lrupd(ap);
+        lrupd_seq(seqs);
       }
+      (void)maxparts;
       std::vector<TruncItem> tr;
       for (size_t i : bi) {
         const int a = abs[i].first, b = abs[i].second;
@@ -1277,6 +1340,7 @@ struct Engine {
       }
       lrupd_ws(tr);
     }
+    join(psecs);
     ar.release(mk);
     return out;
   }
@@ -1405,8 +1469,15 @@ struct Engine {
       }
     }
     copy(c);
-    if (!mb.empty()) multiply_into(mb, mx, my);
-    std::vector<int> leaf_pos(ts.size(), -1);
+    // the block products (into fresh temporaries) and the leaf-level low-rank
+    // products are independent: the former run as a side-stream section
+    std::vector<Sec> secs;
+    if (!mb.empty()) {
+      if (!leafc.empty())
+        section(secs, [&] { multiply_into(mb, mx, my); });
+      else
+        multiply_into(mb, mx, my);
+    }
     if (!leafc.empty()) {
       std::vector<std::pair<int, int>> ab;
       for (const Trip& t : leafc) ab.push_back({t.a, t.b});
@@ -1414,6 +1485,7 @@ struct Engine {
       for (size_t i = 0; i < leafc.size(); ++i)
         adds.push_back(Add{leafc[i].c, pr[i].p, pr[i].q, -1.0, rb(leafc[i].a), rb(leafc[i].b)});
     }
+    join(secs);
     // restore the reference order of the terms (leafc terms were appended last)
     std::vector<Add> ordered;
     ordered.reserve(adds.size());
