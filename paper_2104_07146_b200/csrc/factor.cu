@@ -690,14 +690,10 @@ struct Engine {
     if (!lr.empty()) {
       const size_t mk = ar.mark();
       std::vector<MV> T;
-      std::vector<CopyScaleItem> z;
       for (const Ap& a : lr) {
         const LeafDev& l = LF(a.b);
-        MV t = temp(l.cap, a.x.cols);
-        z.push_back(cpy(nullptr, 0, t, a.x.cols, 0, 0.0, nullptr, 0));
-        T.push_back(t);
+        T.push_back(temp(l.cap, a.x.cols));
       }
-      copy(z);
       for (size_t i = 0; i < lr.size(); ++i) {  // T = (trans ? U : V)^T x   (rank x c)
         const Ap& a = lr[i];
         const LeafDev& l = LF(a.b);
@@ -713,6 +709,7 @@ struct Engine {
         gi.N = a.x.cols;
         gi.K = dimv(a.trans ? l.m : l.n);
         gi.alpha = 1.0;
+        gi.atomic = 2;  // T is this item's own: overwrite (no zero fill)
         g.push_back(gi);
       }
       gemm(g);

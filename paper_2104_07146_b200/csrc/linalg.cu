@@ -118,8 +118,10 @@ __device__ void gemm_item(const GemmItem& it, int tile0, int tstride, bool count
       for (int p = 0; p < 4; ++p) {
         const int gi = i0 + tx + 16 * p;
         if (gi < M) {
-          if (it.atomic)
+          if (it.atomic == 1)
             atomicAdd(&it.C[(size_t)gj * it.ldc + gi], it.alpha * acc[p][q]);
+          else if (it.atomic == 2)
+            it.C[(size_t)gj * it.ldc + gi] = it.alpha * acc[p][q];
           else
             it.C[(size_t)gj * it.ldc + gi] += it.alpha * acc[p][q];
         }

@@ -25,7 +25,8 @@ struct GemmItem {
   Dim M, N, K;
   int ta, tb;
   double alpha;
-  int atomic;  // accumulate with FP64 atomics (several items share C rows)
+  int atomic;  // 0: C += ..., 1: accumulate with FP64 atomics (several items share C
+               // rows), 2: C = ... (overwrite; the item owns its C)
 };
 
 // M (b x cols) <- L^{-1} M (trans = 0) or L^{-T} M (trans = 1); L b x b lower,
