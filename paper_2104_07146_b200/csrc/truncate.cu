@@ -1511,7 +1511,10 @@ void launch_truncate_cluster(const TruncItem* d_items, const int* d_off, int tar
     int dev = 0, optin = 0;
     HMGP_CUDA(cudaGetDevice(&dev));
     HMGP_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    bytes = (size_t)optin - fa.sharedSizeBytes - 1024;
+    // ~112 KB: enough for the register path's slices (ms <= 256 at r <= 32,
+    // ms <= 128 at r <= 40) while leaving L1 for the items that fall back to
+    // the global-memory path
+    bytes = std::min((size_t)optin - fa.sharedSizeBytes - 1024, (size_t)14336 * 8);
     HMGP_CUDA(cudaFuncSetAttribute(k_truncate_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)bytes));
     cap = (int)(bytes / 8);
