@@ -32,6 +32,9 @@ import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+# 32 hardware work queues for the task-flow factorization's streams (before any
+# CUDA context exists in this process)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 sys.path.insert(0, ROOT)
 
 C3 = dict(g=512, leaf=128, eps=1e-6, theta=(1.5, 0.05, 1.0, 0.01), form="cholesky")
@@ -300,11 +303,13 @@ def extras(hm, _lib, ctx, stream):
     ms, pr = dev_ms(lambda: hm.predict(x, z, te, [1.0, 0.1, 0.5, 0.01], cfg, ctx=ctx))
     ph = (C.c_double * 10)()
     _lib.hmgp_last_phases(ctx.h, ph, 10)
-    # C4 θ-sweep throughput on one GPU: an 8-θ subset of the 512-point grid
-    # (every ν and τ², σ² and ℓ at grid values), one geometry, hmgp_loglik_batch
+    # C4 θ-sweep throughput on one GPU: a 16-θ subset of the 512-point grid
+    # (every ν and τ², two σ² and one ℓ at grid values), one geometry,
+    # hmgp_loglik_batch (independent θ on concurrent host workers / streams)
     from paper_2104_07146_b200 import sweep as sw
     grid = sw.c4_theta_grid()
-    sub = [i for i in range(len(grid)) if grid[i, 0] == sw.C4_SIGMA2[3] and grid[i, 1] == sw.C4_ELL[3]]
+    sub = [i for i in range(len(grid)) if grid[i, 0] in (sw.C4_SIGMA2[3], sw.C4_SIGMA2[4])
+           and grid[i, 1] == sw.C4_ELL[3]]
     g64 = hm.Geometry(x, 64, 2.0, ctx=ctx)
     dz = torch.from_numpy(z).to(torch.device("cuda", ctx.device))
     torch.cuda.synchronize()

@@ -27,6 +27,11 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+# The task-flow factorization (csrc/dag.h) spreads independent launches over 32
+# streams; the default 8 hardware work queues would serialise them again.  Must
+# be set before the process creates its CUDA context.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libhmgp_cuda.so")
 

@@ -475,10 +475,13 @@ void assemble(HMat& h, Geometry& g, const MaternDev& p, double eps, bool fixed_r
           std::vector<int> off(tm.size() + 1);
           for (size_t q = 0; q <= tm.size(); ++q) off[q] = (int)q;
           int* d_off = upload(off, st);
-          launch_truncate_pair(d_tm, d_off, (int)tm.size(), eps, d_err, st, pass == 1);
+          int* d_dfr = nullptr;
+          if (pass == 1) HMGP_CUDA(cudaMalloc(&d_dfr, tm.size() * 4));
+          launch_truncate_pair(d_tm, d_off, (int)tm.size(), eps, d_err, st, d_dfr);
           HMGP_CUDA(cudaStreamSynchronize(st));
           cudaFree(d_tm);
           cudaFree(d_off);
+          cudaFree(d_dfr);
         }
         if (!tbig.empty()) {  // large blocks: one 8-CTA cluster each
           TruncItem* d_tb = upload(tbig, st);

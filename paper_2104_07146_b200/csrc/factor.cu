@@ -21,9 +21,12 @@
 #include <array>
 #include <chrono>
 #include <map>
+#include <set>
+#include <string>
 #include <vector>
 
 #include "common.cuh"
+#include "dag.h"
 #include "factor.h"
 #include "hmgp_api.h"
 #include "linalg.cuh"
@@ -33,32 +36,85 @@ namespace hmgp_gpu {
 
 
 // ------------------------------------------------------------ utilities ---
+extern thread_local bool t_one_stream;
+constexpr int kSubArenaFull = 1007;  // internal: task-flow sub-arenas too small -> serial redo
+
 struct Arena {
   char* base = nullptr;
-  size_t cap = 0, top = 0, peak = 0;
-  void init(size_t bytes) {  // persistent: reallocate only to grow
-    top = peak = 0;
+  size_t cap = 0, top = 0, peak = 0, total = 0;
+  // Task-flow mode: K sub-arenas (stacks); consecutive frames rotate over them so
+  // that independent frames do not reuse each other's memory right away (reuse
+  // is still safe: the task flow fences it).  Marks are kept on a stack.
+  static constexpr int kMaxSub = 8;
+  int K = 1, cur = 0;
+  size_t sub_cap = 0;
+  size_t tops[kMaxSub] = {};
+  std::vector<std::array<size_t, kMaxSub + 1>> marks;
+  Dag* dag = nullptr;  // set in task-flow mode: allocations are registered
+  void init(size_t bytes, int k = 1) {  // persistent: reallocate only to grow
+    top = peak = total = 0;
     hold = 0;
-    if (base && cap >= bytes) return;
-    if (base) cudaFree(base);
-    base = nullptr;
-    cap = bytes;
-    HMGP_CUDA(cudaMalloc(&base, cap));
+    K = std::max(1, std::min(k, kMaxSub));
+    cur = 0;
+    marks.clear();
+    if (!(base && cap >= bytes)) {
+      if (base) cudaFree(base);
+      base = nullptr;
+      cap = bytes;
+      HMGP_CUDA(cudaMalloc(&base, cap));
+    }
+    sub_cap = (cap / K) & ~size_t(255);
+    for (int i = 0; i < K; ++i) tops[i] = i * sub_cap;
   }
   int hold = 0;  // > 0 while a side-stream section is being enqueued: no reuse
-  size_t mark() const { return top; }
+  size_t mark() {
+    if (K == 1) return top;
+    std::array<size_t, kMaxSub + 1> m{};
+    for (int i = 0; i < K; ++i) m[i] = tops[i];
+    m[kMaxSub] = marks.size();
+    marks.push_back(m);
+    cur = (cur + 1) % K;
+    return marks.size() - 1;
+  }
   void release(size_t m) {
-    if (!hold) top = m;
+    if (hold) return;
+    if (K == 1) {
+      top = m;
+      return;
+    }
+    for (int i = 0; i < K; ++i) tops[i] = marks[m][i];
+    marks.resize(m);
   }
   void* raw(size_t bytes) {
-    const size_t a = (top + 255) & ~size_t(255);
-    if (a + bytes > cap) throw Error(6, "factorize: device temporary arena exhausted");
-    top = a + bytes;
-    peak = std::max(peak, top);
-    return base + a;
+    if (K == 1) {
+      const size_t a = (top + 255) & ~size_t(255);
+      if (a + bytes > cap) throw Error(6, "factorize: device temporary arena exhausted");
+      top = a + bytes;
+      peak = std::max(peak, top);
+      total += bytes;
+      if (dag) dag->on_alloc((uintptr_t)(base + a), (uintptr_t)(base + a + bytes));
+      return base + a;
+    }
+    for (int j = 0; j < K; ++j) {
+      const int i = (cur + j) % K;
+      const size_t a = (tops[i] + 255) & ~size_t(255);
+      if (a + bytes > (i + 1) * sub_cap) continue;
+      tops[i] = a + bytes;
+      peak = std::max(peak, tops[i] - i * sub_cap);
+      total += bytes;
+      if (dag) dag->on_alloc((uintptr_t)(base + a), (uintptr_t)(base + a + bytes));
+      return base + a;
+    }
+    throw Error(kSubArenaFull, "factorize: device temporary sub-arenas exhausted");
   }
   double* dbl(size_t n) { return static_cast<double*>(raw(std::max<size_t>(n, 1) * 8)); }
   int* ints(size_t n) { return static_cast<int*>(raw(std::max<size_t>(n, 1) * 4)); }
+  void free_all() {
+    if (base) cudaFree(base);
+    base = nullptr;
+    cap = 0;
+  }
+  ~Arena() { free_all(); }
 };
 
 // Pinned host ring -> device ring for item descriptors (stream ordered).
@@ -66,6 +122,8 @@ struct Stager {
   char* h = nullptr;
   char* d = nullptr;
   size_t cap = 0, off = 0;
+  int wraps = 0;
+  double wrap_ms = 0;
   cudaStream_t st = nullptr;          // stream of the next copy (the engine's current one)
   std::vector<cudaStream_t> used;     // streams that may still read the ring
   void use(cudaStream_t s) {
@@ -76,17 +134,26 @@ struct Stager {
     st = s;
     used.assign(1, s);
     off = 0;
+    wraps = 0;
+    wrap_ms = 0;
     if (h) return;
     cap = bytes;
     HMGP_CUDA(cudaMallocHost(&h, cap));
     HMGP_CUDA(cudaMalloc(&d, cap));
+  }
+  ~Stager() {
+    if (h) cudaFreeHost(h);
+    if (d) cudaFree(d);
   }
   template <class T>
   const T* put(const std::vector<T>& v) {
     const size_t bytes = (v.size() * sizeof(T) + 255) & ~size_t(255);
     if (bytes > cap) throw Error(6, "item batch exceeds staging ring");
     if (off + bytes > cap) {  // wrap: every stream that read the ring must be done
+      const auto w0 = std::chrono::steady_clock::now();
       for (cudaStream_t s : used) HMGP_CUDA(cudaStreamSynchronize(s));
+      wrap_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
+      ++wraps;
       used.assign(1, st);
       off = 0;
     }
@@ -119,8 +186,37 @@ static MV cols_of(MV m, int c0, int cnt) {  // structural columns only
 // Per host thread (evaluate_loglik is reentrant): device
 // temporaries reused by every factorization of the thread (grows), and the
 // item-descriptor ring.
+// per host thread: side streams / events of the in-order schedule (destroyed
+// with the thread, so θ-batch workers do not leak them)
+struct SidePool {
+  static constexpr int kSide = 7, kPool = 12;
+  cudaStream_t side[kSide] = {};
+  cudaEvent_t evf = nullptr, evj[kSide] = {};
+  cudaStream_t pool[kPool] = {};
+  int next = 0;
+  std::vector<cudaEvent_t> evs;
+  ~SidePool() {
+    for (cudaStream_t x : side)
+      if (x) cudaStreamDestroy(x);
+    for (cudaEvent_t x : evj)
+      if (x) cudaEventDestroy(x);
+    if (evf) cudaEventDestroy(evf);
+    for (cudaStream_t x : pool)
+      if (x) cudaStreamDestroy(x);
+    for (cudaEvent_t x : evs) cudaEventDestroy(x);
+  }
+};
+
 thread_local Arena g_arena;
 thread_local Stager g_stager;
+thread_local Dag g_dag;
+thread_local SidePool g_side;
+
+thread_local size_t t_last_arena_peak = 0, t_last_pool_bytes = 0;
+thread_local bool t_one_stream = false;
+
+// release this host thread's factorization temporaries (θ-batch workers)
+void release_thread_workspace() { g_arena.free_all(); }
 
 struct Engine {
   Factor& F;
@@ -132,13 +228,111 @@ struct Engine {
   double eps;
   int* d_err = nullptr;
   int TCAP;  // width capacity of product temporaries; overflow is detected on device
+  Dag* dag = nullptr;  // task-flow mode (dag.h); nullptr: in-order stream + sections
+  cudaEvent_t fork_ev = nullptr;
 
-  Engine(Factor& f, cudaStream_t s, size_t arena_bytes, int tcap)
+  Engine(Factor& f, cudaStream_t s, size_t arena_bytes, int tcap, bool use_dag)
       : F(f), G(*f.g), st(s), ar(g_arena), sg(g_stager), ldl(f.ldl), eps(f.eps), TCAP(tcap) {
-    ar.init(arena_bytes);
-    sg.init((size_t)64 << 20, s);
+    ar.dag = nullptr;
+    ar.init(arena_bytes, use_dag ? 4 : 1);
+    sg.init(use_dag ? ((size_t)512 << 20) : ((size_t)64 << 20), s);
+    if (use_dag) {
+      sections_on = false;
+      dag = &g_dag;
+      dag->serial = getenv("HMGP_DAG_DIAG") != nullptr;
+      const int L = (int)F.leaf.size();
+      std::vector<uintptr_t> lb(L), le(L);
+      for (int k = 0; k < L; ++k) {
+        const LeafDev& l = F.leaf[k];
+        lb[k] = (uintptr_t)l.a;
+        le[k] = (uintptr_t)(l.a + (l.kind == DENSE ? (size_t)l.m * l.n : (size_t)(l.m + l.n) * l.cap));
+      }
+      std::vector<int> pobj(G.n, -1);
+      for (int k = 0; k < L; ++k) {
+        const HNode& nd = F.nodes[F.leaf_node[k]];
+        if (nd.row == nd.col)
+          for (int i = G.nbeg[nd.row]; i < G.nend[nd.row]; ++i) pobj[i] = k;
+      }
+      dag->reset(lb, le, F.d_rank, F.d_compact, F.d_d, pobj, (uintptr_t)ar.base, (uintptr_t)(ar.base + ar.cap));
+      ar.dag = dag;
+      HMGP_CUDA(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
+    }
     d_err = ar.ints(1);
     HMGP_CUDA(cudaMemsetAsync(d_err, 0, 4, st));
+    if (dag) dag->fork_from(st, fork_ev);
+  }
+  ~Engine() {
+    ar.dag = nullptr;
+    if (fork_ev) cudaEventDestroy(fork_ev);
+  }
+
+  // --- task flow: accesses of the next launch (object, write)
+  std::vector<std::pair<int, char>> accs;
+  void A(const void* p, bool w) {
+    if (!dag || !p) return;
+    const int o = dag->lookup(p);
+    if (o >= 0) accs.push_back({o, (char)w});
+  }
+  void acc(const GemmItem& g) {
+    A(g.A, 0);
+    A(g.B, 0);
+    A(g.C, 1);
+    A(g.M.p, 0);
+    A(g.N.p, 0);
+    A(g.K.p, 0);
+  }
+  void acc(const TruncItem& t) {
+    A(t.U, 1);
+    A(t.V, 1);
+    A(t.rank, 1);
+    A(t.compact, 1);
+    A(t.ws, 1);
+    A(t.P, 0);
+    A(t.Q, 0);
+    A(t.addp, 0);
+    A(t.post_L, 0);
+    A(t.post_d, 0);
+  }
+  void acc(const CopyScaleItem& c) {
+    A(c.src, 0);
+    if (c.mode) A(c.d, 0);
+    A(c.dst, 1);
+    A(c.cols.p, 0);
+    A(c.set_cols, 1);
+  }
+  void acc(const TrsmLItem& x) {
+    A(x.L, 0);
+    A(x.M, 1);
+    A(x.cols.p, 0);
+  }
+  void acc(const TrsmRItem& x) {
+    A(x.L, 0);
+    A(x.X, 1);
+    A(x.d, 0);
+  }
+  template <class T>
+  void acc_all(const std::vector<T>& v) {
+    if (dag)
+      for (const T& x : v) acc(x);
+  }
+  std::vector<std::pair<int, char>> take_accs() {
+    std::vector<std::pair<int, char>> r;
+    r.swap(accs);
+    return r;
+  }
+  // launch fn(stream) now: as a task (task flow) or on the current stream
+  template <class Fn>
+  void run(const char* label, Fn&& fn) {
+    if (!dag) {
+      fn(st);
+      return;
+    }
+    dag->label = label;
+    dag->launch(accs, [&](cudaStream_t s) {
+      sg.use(s);
+      fn(s);
+    });
+    accs.clear();
   }
 
   // --- node helpers
@@ -219,7 +413,8 @@ struct Engine {
     if (v.empty()) return;
     int tiles = 1;
     for (auto& g : v) tiles = std::max(tiles, ((g.M.v + 63) / 64) * ((g.N.v + 63) / 64));
-    launch_gemm(sg.put(v), (int)v.size(), tiles, st);
+    acc_all(v);
+    run("gemm", [&](cudaStream_t s) { launch_gemm(sg.put(v), (int)v.size(), tiles, s); });
     stat(S_GEMM, v.size());
     v.clear();
   }
@@ -227,7 +422,8 @@ struct Engine {
     if (v.empty()) return;
     int mx = 1;
     for (auto& c : v) mx = std::max<long long>(mx, std::min<long long>((long long)c.rows * c.cols.v, 1 << 24));
-    launch_copy_scale(sg.put(v), (int)v.size(), mx, st);
+    acc_all(v);
+    run("copy", [&](cudaStream_t s) { launch_copy_scale(sg.put(v), (int)v.size(), mx, s); });
     stat(S_COPY, v.size());
     v.clear();
   }
@@ -242,30 +438,76 @@ struct Engine {
   // through events, so one step costs its slowest group rather than the sum.
   // Stats mode runs them in order on the main stream so that the per-launch
   // timing stays attributable.
-  std::vector<std::function<void(cudaStream_t)>> jobs;
+  // A job enqueues its own descriptors (sg.put) and launch on the stream it is
+  // given; in task-flow mode every job is a task with the accesses collected
+  // (accs) when it was queued.
+  struct Job {
+    std::function<void(cudaStream_t)> fn;
+    std::vector<std::pair<int, char>> acc;
+    const char* label;
+  };
+  std::vector<Job> jobs;
+  const char* site = "";  // (task-flow diagnostics) call site of the next truncation jobs
+  // (task-flow diagnostics) label with size class: max(m, n) and longest sequence
+  const char* cls(const char* base, const std::vector<TruncItem>& v, const std::vector<int>* off) {
+    if (!dag || !dag->serial) return base;
+    static std::set<std::string> pool;
+    int mx = 0, sq = 1;
+    for (const TruncItem& t : v) mx = std::max(mx, std::max(t.m, t.n));
+    if (off)
+      for (size_t b = 0; b + 1 < off->size(); ++b) sq = std::max(sq, (*off)[b + 1] - (*off)[b]);
+    int pm = 1, ps = 1;
+    while (pm < mx) pm <<= 1;
+    while (ps < sq) ps <<= 1;
+    char buf[96];
+    snprintf(buf, sizeof buf, "%s:%s m<=%d seq<=%d", site, base, pm, ps);
+    return pool.insert(buf).first->c_str();
+  }
+  template <class Fn>
+  void add_job(const char* label, Fn&& fn) {
+    jobs.push_back(Job{std::function<void(cudaStream_t)>(std::forward<Fn>(fn)), take_accs(), label});
+  }
   void run_jobs() {
     if (jobs.empty()) return;
-    if (jobs.size() == 1 || stats_on) {
-      for (auto& j : jobs) j(st);
+    if (dag) {
+      for (Job& j : jobs) {
+        dag->label = j.label;
+        dag->launch(j.acc, [&](cudaStream_t s) {
+          sg.use(s);
+          j.fn(s);
+        });
+      }
       jobs.clear();
       return;
     }
-    constexpr int kSide = 7;
-    static thread_local cudaStream_t side[kSide] = {};
-    static thread_local cudaEvent_t evf = nullptr, evj[kSide] = {};
-    if (!side[0]) {
-      HMGP_CUDA(cudaEventCreateWithFlags(&evf, cudaEventDisableTiming));
+    if (jobs.size() == 1 || stats_on || t_one_stream) {
+      for (auto& j : jobs) j.fn(st);
+      jobs.clear();
+      return;
+    }
+    constexpr int kSide = SidePool::kSide;
+    SidePool& sp = g_side;
+    if (!sp.side[0]) {
+      HMGP_CUDA(cudaEventCreateWithFlags(&sp.evf, cudaEventDisableTiming));
       for (int i = 0; i < kSide; ++i) {
-        HMGP_CUDA(cudaStreamCreateWithFlags(&side[i], cudaStreamNonBlocking));
-        HMGP_CUDA(cudaEventCreateWithFlags(&evj[i], cudaEventDisableTiming));
+        HMGP_CUDA(cudaStreamCreateWithFlags(&sp.side[i], cudaStreamNonBlocking));
+        HMGP_CUDA(cudaEventCreateWithFlags(&sp.evj[i], cudaEventDisableTiming));
       }
     }
+    cudaStream_t* side = sp.side;
+    cudaEvent_t evf = sp.evf;
+    cudaEvent_t* evj = sp.evj;
     const int ns = std::min((int)jobs.size() - 1, kSide);
     HMGP_CUDA(cudaEventRecord(evf, st));
     for (int i = 0; i < ns; ++i) HMGP_CUDA(cudaStreamWaitEvent(side[i], evf, 0));
-    for (size_t k = 1; k < jobs.size(); ++k) jobs[k](side[(k - 1) % kSide]);
+    for (size_t k = 1; k < jobs.size(); ++k) {
+      const cudaStream_t s = side[(k - 1) % kSide];
+      sg.use(s);
+      jobs[k].fn(s);
+    }
+    sg.use(st);
     for (int i = 0; i < ns; ++i) HMGP_CUDA(cudaEventRecord(evj[i], side[i]));
-    jobs[0](st);
+    jobs[0].fn(st);
     for (int i = 0; i < ns; ++i) HMGP_CUDA(cudaStreamWaitEvent(st, evj[i], 0));
     jobs.clear();
   }
@@ -279,20 +521,15 @@ struct Engine {
     cudaStream_t s;
     cudaEvent_t done;
   };
-  bool sections_on = !stats_on && getenv("HMGP_SERIAL") == nullptr;
+  bool sections_on = !stats_on && getenv("HMGP_SERIAL") == nullptr && !t_one_stream;
   cudaStream_t sec_stream() {
-    constexpr int kPool = 12;
-    static thread_local cudaStream_t pool[kPool] = {};
-    static thread_local int next = 0;
-    cudaStream_t& s = pool[next];
-    next = (next + 1) % kPool;
+    constexpr int kPool = SidePool::kPool;
+    cudaStream_t& s = g_side.pool[g_side.next];
+    g_side.next = (g_side.next + 1) % kPool;
     if (!s) HMGP_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     return s;
   }
-  static std::vector<cudaEvent_t>& ev_pool() {
-    static thread_local std::vector<cudaEvent_t> p;
-    return p;
-  }
+  static std::vector<cudaEvent_t>& ev_pool() { return g_side.evs; }
   cudaEvent_t ev_get() {
     auto& p = ev_pool();
     if (p.empty()) {
@@ -352,16 +589,14 @@ struct Engine {
     const double e = eps;
     int* er = d_err;
     if (!ir.empty()) {
-      const TruncItem* dr = sg.put(ir);
-      const int* dor = sg.put(offr);
       const int nr = (int)offr.size() - 1;
-      jobs.push_back([=](cudaStream_t s) { launch_truncate_cluster(dr, dor, nr, e, er, s, true); });
+      acc_all(ir);
+      add_job(cls("cluster-res", ir, &offr), [=](cudaStream_t s) { launch_truncate_cluster(sg.put(ir), sg.put(offr), nr, e, er, s, true); });
     }
     if (!ig.empty()) {
-      const TruncItem* dg = sg.put(ig);
-      const int* dog = sg.put(offg);
       const int ng = (int)offg.size() - 1;
-      jobs.push_back([=](cudaStream_t s) { launch_truncate_cluster(dg, dog, ng, e, er, s, false); });
+      acc_all(ig);
+      add_job(cls("cluster-glb", ig, &offg), [=](cudaStream_t s) { launch_truncate_cluster(sg.put(ig), sg.put(offg), ng, e, er, s, false); });
     }
   }
 
@@ -399,16 +634,14 @@ struct Engine {
     int* er = d_err;
     if (!tb.empty()) cluster_jobs(tb, tboff);
     if (!tp.empty()) {
-      const TruncItem* di = sg.put(tp);
-      const int* doff = sg.put(tpoff);
       const int cnt = (int)tpoff.size() - 1;
-      jobs.push_back([=](cudaStream_t s) { launch_truncate_pair(di, doff, cnt, e, er, s, false); });
+      acc_all(tp);
+      add_job(cls("pair", tp, &tpoff), [=](cudaStream_t s) { launch_truncate_pair(sg.put(tp), sg.put(tpoff), cnt, e, er, s); });
     }
     if (!t.empty()) {
-      const TruncItem* di = sg.put(t);
-      const int* doff = sg.put(toff);
       const int cnt = (int)toff.size() - 1;
-      jobs.push_back([=](cudaStream_t s) { launch_truncate_seq(di, doff, cnt, e, er, s, sw, smn); });
+      acc_all(t);
+      add_job(cls("seq", t, &toff), [=](cudaStream_t s) { launch_truncate_seq(sg.put(t), sg.put(toff), cnt, e, er, s, sw, smn); });
     }
     tslot();
     run_jobs();
@@ -437,11 +670,11 @@ struct Engine {
       std::vector<int> off(grp.size() + 1);
       for (size_t i = 0; i <= grp.size(); ++i) off[i] = (int)i;
       if (pass) {
-        const TruncItem* di = sg.put(grp);
-        const int* doff = sg.put(off);
         const int cnt = (int)grp.size();
-        const bool dfer = pass == 2;
-        jobs.push_back([=](cudaStream_t s) { launch_truncate_pair(di, doff, cnt, e, er, s, dfer); });
+        int* dfr = pass == 2 ? ar.ints(cnt) : nullptr;
+        acc_all(grp);
+        A(dfr, 1);
+        add_job(cls(dfr ? "pair-dfr" : "pair", grp, nullptr), [=, g = grp](cudaStream_t s) { launch_truncate_pair(sg.put(g), sg.put(off), cnt, e, er, s, dfr); });
       } else {
         cluster_jobs(grp, off);
       }
@@ -458,9 +691,9 @@ struct Engine {
         mt[0] = mt[0] < 0 ? mt[0] : std::max(mt[0], t.m);
         mt[1] = std::max(mt[1], t.n);
       }
-      const TruncItem* di = sg.put(v);
       const int cnt = (int)v.size();
-      jobs.push_back([=](cudaStream_t s) { launch_truncate(di, cnt, e, er, s, sw, smn); });
+      acc_all(v);
+      add_job(cls("small", v, nullptr), [=](cudaStream_t s) { launch_truncate(sg.put(v), cnt, e, er, s, sw, smn); });
       nitems += v.size();
       v.clear();
     }
@@ -611,6 +844,7 @@ struct Engine {
       v.push_back(lritem(l.a, l.b, l.m, l.n, rankp(x), compp(x), 0, l.cap, nullptr, nullptr, 0, 0,
                          1.0, l.cap));
     }
+    site = "compress";
     lrupd_ws(v);
     ar.release(mk);
   }
@@ -758,7 +992,8 @@ struct Engine {
         v.push_back(TrsmLItem{L.a, L.m, L.m, m.p, m.ld, m.cols, 0});
         mc = std::max(mc, m.cols.v);
       }
-      launch_trsm_left(sg.put(v), (int)v.size(), mc, st, L.m);
+      acc_all(v);
+      run("trsm_left", [&](cudaStream_t s) { launch_trsm_left(sg.put(v), (int)v.size(), mc, s, L.m); });
       stat(S_TRSML, v.size());
       return;
     }
@@ -788,7 +1023,8 @@ struct Engine {
         v.push_back(TrsmRItem{L.a, L.m, L.m, x.p, x.ld, x.rows, ldl ? dseg(rb(l)) : nullptr});
         mr = std::max(mr, x.rows);
       }
-      launch_trsm_right(sg.put(v), (int)v.size(), mr, st, L.m);
+      acc_all(v);
+      run("trsm_right", [&](cudaStream_t s) { launch_trsm_right(sg.put(v), (int)v.size(), mr, s, L.m); });
       stat(S_TRSMR, v.size());
       return;
     }
@@ -855,6 +1091,7 @@ struct Engine {
             t.post_d = ldl ? dseg(rb(l)) : nullptr;
             v.push_back(t);
           }
+          site = "trsm-lr";
           lrupd_ws(v);
           ar.release(mk);
         });
@@ -1027,10 +1264,9 @@ struct Engine {
     size_t ntr = 0;
     std::array<int, 5> mt{};
     if (!g.empty()) {
-      const GemmItem* dg = sg.put(g);
-      const int* dgo = sg.put(goff);
       const int ng = (int)goff.size() - 1;
-      jobs.push_back([=](cudaStream_t s) { launch_gemm_seq(dg, dgo, ng, s); });
+      acc_all(g);
+      add_job("gemm_seq", [=](cudaStream_t s) { launch_gemm_seq(sg.put(g), sg.put(goff), ng, s); });
       st_launch[S_GEMM]++;
       st_items[S_GEMM] += (long long)g.size();
     }
@@ -1046,21 +1282,20 @@ struct Engine {
       const std::vector<int>& to = pass ? tdoff : tpoff;
       const std::array<int, 5>& mq = pass ? meta_d : meta_p;
       if (tq.empty()) continue;
-      const TruncItem* di = sg.put(tq);
-      const int* doff = sg.put(to);
       const int cnt = (int)to.size() - 1;
-      const bool dfer = pass == 1;
-      jobs.push_back([=](cudaStream_t s) { launch_truncate_pair(di, doff, cnt, e, er, s, dfer); });
+      int* dfr = pass == 1 ? ar.ints(cnt) : nullptr;
+      acc_all(tq);
+      A(dfr, 1);
+      add_job(cls(dfr ? "pair-dfr" : "pair", tq, &to), [=, q = tq, o = to](cudaStream_t s) { launch_truncate_pair(sg.put(q), sg.put(o), cnt, e, er, s, dfr); });
       ntr += tq.size();
       mt[0] = std::min(mt[0], -mq[0]);
       mt[1] = std::max(mt[1], mq[1]);
       mt[3] = std::max(mt[3], mq[3]);
     }
     if (!t.empty()) {
-      const TruncItem* di = sg.put(t);
-      const int* doff = sg.put(toff);
       const int cnt = (int)toff.size() - 1;
-      jobs.push_back([=](cudaStream_t s) { launch_truncate_seq(di, doff, cnt, e, er, s, sw, smn); });
+      acc_all(t);
+      add_job(cls("seq", t, &toff), [=](cudaStream_t s) { launch_truncate_seq(sg.put(t), sg.put(toff), cnt, e, er, s, sw, smn); });
       ntr += t.size();
       if (mt[0] >= 0) mt[0] = std::max(mt[0], meta_t[0]);
       mt[1] = std::max(mt[1], meta_t[1]);
@@ -1116,6 +1351,7 @@ struct Engine {
       }
     }
     gemm(g);
+    site = "add-leaves";
     lrupd_ws(t);
     ar.release(mk);
   }
@@ -1144,7 +1380,10 @@ struct Engine {
       nbr += !(kind(a) == LOWRANK || kind(b) == LOWRANK || kind(a) == DENSE || kind(b) == DENSE);
     }
     int* wcs = nbr ? ar.ints(nbr) : nullptr;
-    if (nbr) HMGP_CUDA(cudaMemsetAsync(wcs, 0, 4ull * nbr, st));
+    if (nbr) {
+      A(wcs, 1);
+      run("memset", [&](cudaStream_t s) { HMGP_CUDA(cudaMemsetAsync(wcs, 0, 4ull * nbr, s)); });
+    }
     int wci = 0;
     for (size_t i = 0; i < n; ++i) {
       const int a = abs[i].first, b = abs[i].second;
@@ -1262,7 +1501,8 @@ struct Engine {
       size_t npart = 0;
       for (size_t i : bi) npart += (size_t)N(abs[i].first).kr * N(abs[i].second).kr;
       int* pcols = ar.ints(npart);
-      HMGP_CUDA(cudaMemsetAsync(pcols, 0, 4 * npart, st));
+      A(pcols, 1);
+      run("memset", [&](cudaStream_t s) { HMGP_CUDA(cudaMemsetAsync(pcols, 0, 4 * npart, s)); });
       for (size_t i : bi) {
         const int a = abs[i].first, b = abs[i].second;
         for (int ii = 0; ii < N(a).kr; ++ii)
@@ -1305,6 +1545,7 @@ struct Engine {
             seqs[who[s]].push_back(lritem(pt.p.p, pt.q.p, pt.p.rows, pt.q.rows, pt.cols, nullptr, 3, TCAP,
                                           &tp[s].p, &tp[s].q, 0, 0, 1.0, TCAP + tp[s].p.cols.v));
           }
+        site = "plr-acc";
         lrupd_seq(seqs);
         ar.release(mk2);
       }
@@ -1326,6 +1567,7 @@ struct Engine {
                                          rb(pt.a0) - rb(a), rb(pt.b0) - rb(b), 1.0, TCAP));
           }
         }
+        site = "plr-embed";
         lrupd_seq(seqs);
       }
       (void)maxparts;
@@ -1335,6 +1577,7 @@ struct Engine {
         tr.push_back(lritem(out[i].p.p, out[i].q.p, nr(a), nr(b), const_cast<int*>(out[i].p.cols.p),
                             nullptr, 0, TCAP, nullptr, nullptr, 0, 0, 1.0, TCAP));
       }
+      site = "plr-final";
       lrupd_ws(tr);
     }
     join(psecs);
@@ -1495,6 +1738,7 @@ struct Engine {
       }
     }
     (void)brc;
+    site = "addlr";
     add_lr(ordered);
     ar.release(mk);
   }
@@ -1503,7 +1747,8 @@ struct Engine {
   void factor_diag(int a) {
     if (kind(a) == DENSE) {
       const LeafDev& l = LF(a);
-      launch_leaf_factor(l.a, l.m, rb(a), ldl ? 1 : 0, F.d_d, F.clamp_tol, F.d_status, st);
+      A(l.a, 1);
+      run("leaf", [&](cudaStream_t s) { launch_leaf_factor(l.a, l.m, rb(a), ldl ? 1 : 0, F.d_d, F.clamp_tol, F.d_status, s); });
       stat(S_LEAF, 1);
       return;
     }
@@ -1717,6 +1962,7 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
   F.nodes = H.nodes;
   F.leaf_node = H.leaf_node;
   const int L = (int)H.leaf.size();
+  t_last_pool_bytes = H.pool_doubles * 8;
   // clone payload (hblock.cpp:17-28): same layout, new pool; compact_cols = 0
   HMGP_CUDA(cudaMalloc(&F.d_leaf, sizeof(LeafDev) * std::max(L, 1)));
   HMGP_CUDA(cudaMalloc(&F.d_rank, 4 * std::max(L, 1)));
@@ -1733,6 +1979,12 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
   // doubled capacities (results do not depend on the capacities that succeed).
   int grow = 1;
   size_t pool_doubles = 0;
+  // task flow (dag.h) on request (HMGP_DAG=1, or HMGP_DAG_DIAG for its critical-path
+  // report).  Measured at C3 its DAG critical path is within 1.33x of the serial
+  // sum and it does not beat the in-order stream + sections schedule, so it is
+  // off by default.
+  bool use_dag = getenv("HMGP_STATS") == nullptr && getenv("HMGP_SERIAL") == nullptr &&
+                 ((getenv("HMGP_DAG") && atoi(getenv("HMGP_DAG")) != 0) || getenv("HMGP_DAG_DIAG"));
   for (int tcap = 256;;) {
     // clone payload (hblock.cpp:17-28) into the factor's own layout; compact_cols = 0
     F.leaf = H.leaf;
@@ -1783,9 +2035,15 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
     LeafFactorStatus s0{INT_MAX, 0, 0, 0, 0.0, INFINITY};
     HMGP_CUDA(cudaMemcpyAsync(F.d_status, &s0, sizeof(s0), cudaMemcpyHostToDevice, st));
     int err = 0;
-    {
-      Engine E(F, st, arena_bytes, tcap);
+    bool redo_serial = false;
+    try {
+      Engine E(F, st, arena_bytes, tcap, use_dag);
       E.stats_begin();
+      cudaEvent_t dg0 = nullptr;
+      if (E.dag && E.dag->serial) {
+        HMGP_CUDA(cudaEventCreate(&dg0));
+        HMGP_CUDA(cudaEventRecord(dg0, E.dag->s[0]));
+      }
       const auto h0 = std::chrono::steady_clock::now();
       E.factor_diag(0);
       // compress_all (hfactor.cpp:321-328): every LR leaf, independent
@@ -1793,21 +2051,44 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
       for (int k = 0; k < L; ++k)
         if (F.leaf[k].kind == LOWRANK) lr.push_back(F.leaf_node[k]);
       E.compress(lr);
-      if (getenv("HMGP_STATS")) {
+      if (E.dag) E.dag->join_into(st);
+      if (dg0) {
+        HMGP_CUDA(cudaStreamSynchronize(st));
+        double ser = 0.0;
+        const double cp = E.dag->critical_path_ms(dg0, &ser);
+        fprintf(stderr, "[hmgp] task flow: %lld tasks, serial %.1f ms, DAG critical path %.1f ms (x%.2f)\n",
+                E.dag->n_tasks, ser, cp, cp > 0 ? ser / cp : 0.0);
+        cudaEventDestroy(dg0);
+      }
+      if (getenv("HMGP_STATS") || getenv("HMGP_TIMING")) {
         const auto h1 = std::chrono::steady_clock::now();
         cudaStreamSynchronize(st);
         const auto h2 = std::chrono::steady_clock::now();
-        fprintf(stderr, "[hmgp] host enqueue %.1f ms, then GPU drain %.1f ms\n",
-                std::chrono::duration<double, std::milli>(h1 - h0).count(),
+        fprintf(stderr, "[hmgp] host enqueue %.1f ms (ring wraps %d, %.1f ms blocked; arena peak %.2f GB, "
+                "allocated %.2f GB), then GPU drain %.1f ms\n",
+                std::chrono::duration<double, std::milli>(h1 - h0).count(), E.sg.wraps, E.sg.wrap_ms,
+                E.ar.peak / 1e9, E.ar.total / 1e9,
                 std::chrono::duration<double, std::milli>(h2 - h1).count());
-        E.print_stats();
+        if (E.dag)
+          fprintf(stderr, "[hmgp] task flow: %lld tasks, %lld event waits, %zu objects\n", E.dag->n_tasks,
+                  E.dag->n_waits, E.dag->objs.size());
+        if (E.stats_on) E.print_stats();
       }
       phase_mark(PH_FACTOR);
       HMGP_CUDA(cudaMemcpyAsync(&err, E.d_err, 4, cudaMemcpyDeviceToHost, st));
       HMGP_CUDA(cudaStreamSynchronize(st));
       F.arena_peak = E.ar.peak;
+      t_last_arena_peak = E.ar.peak;
       g_work.arena_peak = std::max(g_work.arena_peak, (double)E.ar.peak);
       g_work.factor_attempts += 1;
+    } catch (const Error& e) {
+      if (e.code != kSubArenaFull) throw;
+      HMGP_CUDA(cudaDeviceSynchronize());
+      redo_serial = true;
+    }
+    if (redo_serial) {  // task-flow sub-arenas too small: redo in program order
+      use_dag = false;
+      continue;
     }
     if (!err) break;
     if (tcap >= 1024 && grow >= 16)

@@ -46,5 +46,16 @@ double factor_log_det(const Factor& F, cudaStream_t st);
 double factor_quad_form_dev(const Factor& F, const double* d_b, cudaStream_t st);
 void factor_solve_dev(const Factor& F, const double* d_b, double* d_x, bool full, cudaStream_t st);
 double factor_storage_bytes(const Factor& F);
+// frees the calling host thread's persistent device arena (the next
+// factorization on this thread allocates it again)
+void release_thread_workspace();
+// device arena of the next factorizations on this host thread (0: automatic)
+extern thread_local size_t t_arena_bytes;
+// arena peak and H-matrix payload bytes of this thread's last factorization
+extern thread_local size_t t_last_arena_peak, t_last_pool_bytes;
+// factorizations on this thread use only their own stream (θ-batch workers:
+// concurrency comes from the other workers, and fewer streams per worker keep
+// the hardware work queues from being shared)
+extern thread_local bool t_one_stream;
 
 }  // namespace hmgp_gpu

@@ -141,8 +141,10 @@ bool trunc_cluster_resident(int m, int n);
 // medium blocks: one CTA pair (U side, V side) per target sequence, factors in smem
 bool trunc_use_pair(int m, int n, int rcap);
 size_t trunc_ws_doubles_pair(int m, int n, int rcap);
+// d_defer: nullptr, or `targets` device ints: items that do not fit the pair
+// layout are handed over to the 8-CTA cluster kernel (same launch sequence)
 void launch_truncate_pair(const TruncItem* d_items, const int* d_off, int targets, double eps,
-                          int* d_err, cudaStream_t st, bool defer_to_cluster = false);
+                          int* d_err, cudaStream_t st, int* d_defer = nullptr);
 // 0 single CTA (small), 1 CTA pair, 2 8-CTA cluster, 3 pair handing over to the
 // cluster kernel what does not fit; workspace for that route
 int trunc_route(int m, int n, int rcap);

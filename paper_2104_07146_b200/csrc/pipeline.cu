@@ -1,7 +1,10 @@
 // Pipeline entry points of the C ABI: factorize / solves / L(θ) / θ-batch /
 // predict, and K12 (the streamed kriging cross-covariance product).
 //   evaluate_loglik  loglik.cpp:18-38      predict  krige.cpp:9-44
+#include <atomic>
 #include <chrono>
+#include <exception>
+#include <thread>
 #include <climits>
 #include <cmath>
 #include <limits>
@@ -25,13 +28,21 @@ struct DBuf {
   ~DBuf() { cudaFree(p); }
 };
 
+}  // namespace
+namespace hmgp_gpu {
+thread_local size_t t_arena_bytes = 0;
+}
+namespace {
+
 size_t arena_bytes_for(const HMat& h) {
+  if (t_arena_bytes) return t_arena_bytes;
   size_t fr = 0, tot = 0;
   cudaMemGetInfo(&fr, &tot);
   // room for the factor copy of the payload + solve work, keep 2 GiB spare
   const size_t need = h.pool_doubles * 8 + ((size_t)2 << 30);
   const size_t avail = fr > need + ((size_t)1 << 30) ? fr - need : ((size_t)1 << 30);
-  const size_t want = std::max<size_t>((size_t)48 << 30, h.pool_doubles * 8 * 3);
+  // the task-flow factorization splits the arena into 4 rotating sub-arenas
+  const size_t want = std::max<size_t>((size_t)112 << 30, h.pool_doubles * 8 * 3);
   return std::min(avail, want);
 }
 
@@ -257,14 +268,20 @@ int hmgp_loglik_geom(hmgp_ctx* ctx, hmgp_geom* g, const double* d_z, const hmgp_
   })
 }
 
+// Independent θ run concurrently (evaluate_loglik is reentrant):
+// the first θ alone on the caller's stream (it sizes the device workspace), the
+// rest on up to HMGP_BATCH_THREADS (default 8) host workers, each with its own
+// stream and arena, pulling θ indices from a shared counter.  One L(θ) is a
+// chain of latency-bound launches that keeps only part of the GPU busy, so
+// concurrent θ fill the idle SMs.
 int hmgp_loglik_batch(hmgp_ctx* ctx, hmgp_geom* g, const double* d_z, const hmgp_matern* thetas,
                       int ntheta, const hmgp_config* cfg, hmgp_loglik_result* res) {
   API_GUARD2({
     HMGP_CUDA(cudaSetDevice(ctx->device));
-    for (int t = 0; t < ntheta; ++t) {
+    auto one = [&](hmgp_ctx* c, int t) {
       const double t0 = now();
       try {  // fit() maps any failure to -inf (mle.cpp:152-158)
-        loglik_on_geom(ctx, g->g, d_z, &thetas[t], cfg, &res[t]);
+        loglik_on_geom(c, g->g, d_z, &thetas[t], cfg, &res[t]);
       } catch (const hmgp_gpu::Error& e) {
         if (e.code != HMGP_ENOTSPD && e.code != HMGP_ECAPACITY) throw;
         res[t] = hmgp_loglik_result{-std::numeric_limits<double>::infinity(), 0, 0, g->g.n, 0, -1};
@@ -272,7 +289,51 @@ int hmgp_loglik_batch(hmgp_ctx* ctx, hmgp_geom* g, const double* d_z, const hmgp
         res[t] = hmgp_loglik_result{-std::numeric_limits<double>::infinity(), 0, 0, g->g.n, 0, -1};
       }
       res[t].seconds = now() - t0;
+    };
+    if (ntheta <= 0) return HMGP_OK;
+    one(ctx, 0);
+    int T = 8;
+    if (const char* e = getenv("HMGP_BATCH_THREADS")) T = std::max(1, atoi(e));
+    T = std::min(T, ntheta - 1);
+    if (T <= 1) {
+      for (int t = 1; t < ntheta; ++t) one(ctx, t);
+      return HMGP_OK;
     }
+    // per worker: the first θ's arena peak with headroom, plus the H-matrix and
+    // factor payloads; the caller's own arena is released first
+    const size_t peak = t_last_arena_peak, pool = t_last_pool_bytes;
+    HMGP_CUDA(cudaStreamSynchronize(ctx->stream));
+    release_thread_workspace();
+    size_t fr = 0, tot = 0;
+    HMGP_CUDA(cudaMemGetInfo(&fr, &tot));
+    const size_t share = peak + peak / 2 + ((size_t)1 << 30);
+    const size_t per = share + pool * 3 + ((size_t)256 << 20);
+    const size_t reserve = (size_t)6 << 30;
+    const size_t usable = fr > reserve ? fr - reserve : 0;
+    T = (int)std::max<size_t>(1, std::min<size_t>(T, usable / per));
+    std::atomic<int> next{1};
+    std::vector<std::exception_ptr> errs(T);
+    std::vector<std::thread> ws;
+    for (int w = 0; w < T; ++w)
+      ws.emplace_back([&, w] {
+        try {
+          HMGP_CUDA(cudaSetDevice(ctx->device));
+          hmgp_ctx c;
+          c.device = ctx->device;
+          HMGP_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+          t_arena_bytes = share;
+          t_one_stream = getenv("HMGP_BATCH_SECTIONS") == nullptr;
+          for (int t; (t = next.fetch_add(1)) < ntheta;) one(&c, t);
+          HMGP_CUDA(cudaStreamSynchronize(c.stream));
+          cudaStreamDestroy(c.stream);
+          release_thread_workspace();
+        } catch (...) {
+          errs[w] = std::current_exception();
+        }
+      });
+    for (auto& th : ws) th.join();
+    for (auto& e : errs)
+      if (e) std::rethrow_exception(e);
   })
 }
 

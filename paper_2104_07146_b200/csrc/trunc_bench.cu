@@ -110,6 +110,8 @@ extern "C" int hmgp_debug_trunc_bench(int m, int n, int r0, int add, int count, 
     int sw = 0, smn = 0;
     trunc_smem_dims(m, n, &sw, &smn);
     if (getenv("HMGP_STATS")) truncate_hist_enable(true);
+    int* ddfr = nullptr;
+    HMGP_CUDA(cudaMalloc(&ddfr, (size_t)count * 4));
     double best = 1e30;
     for (int rep = 0; rep < reps; ++rep) {
       HMGP_CUDA(cudaMemcpyAsync(dU, dU0, U.size() * 8, cudaMemcpyDeviceToDevice, st));
@@ -120,7 +122,7 @@ extern "C" int hmgp_debug_trunc_bench(int m, int n, int r0, int add, int count, 
       if (route == 2)
         launch_truncate_cluster(ditems, doff, count, eps, derr, st, trunc_cluster_resident(m, n));
       else if (route == 1 || route == 3)
-        launch_truncate_pair(ditems, doff, count, eps, derr, st, route == 3);
+        launch_truncate_pair(ditems, doff, count, eps, derr, st, route == 3 ? ddfr : nullptr);
       else
         launch_truncate(ditems, count, eps, derr, st, sw, smn);
       cudaEventRecord(e1, st);
@@ -143,6 +145,7 @@ extern "C" int hmgp_debug_trunc_bench(int m, int n, int r0, int add, int count, 
     cudaFree(dP);
     cudaFree(dQ);
     cudaFree(ws);
+    cudaFree(ddfr);
     cudaFree(drank);
     cudaFree(dcomp);
     cudaFree(derr);

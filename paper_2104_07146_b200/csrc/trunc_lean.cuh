@@ -208,54 +208,94 @@ __device__ double cta_jacobi2(double* W, int p, int q, double* J, int* sweeps_ou
     ++sweeps;
     int rot = 0;
     for (int round = 0; round < m1; ++round) {
-      for (int t = w; t < qq / 2; t += nw) {
-        int a, b;
-        if (t == 0) {
-          a = qq - 1;
-          b = round;
-        } else {  // (round + t) mod m1 and (round - t) mod m1 without divisions
-          a = round + t;
-          if (a >= m1) a -= m1;
-          b = round - t;
-          if (b < 0) b += m1;
+      // two pairs per warp at once: their dot products share one interleaved
+      // reduction and their rotation scalars overlap (per pair the arithmetic
+      // is exactly the single-pair sequence)
+      for (int t0 = w; t0 < qq / 2; t0 += 2 * nw) {
+        int a[2], b[2];
+        bool act[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int t = t0 + u * nw;
+          act[u] = t < qq / 2;
+          int aa, bb;
+          if (t == 0) {
+            aa = qq - 1;
+            bb = round;
+          } else {  // (round + t) mod m1 and (round - t) mod m1 without divisions
+            aa = round + t;
+            if (aa >= m1) aa -= m1;
+            bb = round - t;
+            if (bb < 0) bb += m1;
+          }
+          if (aa > bb) {
+            const int tmp = aa;
+            aa = bb;
+            bb = tmp;
+          }
+          if (bb >= q) act[u] = false;
+          a[u] = act[u] ? aa : 0;
+          b[u] = act[u] ? bb : 0;
         }
-        if (a > b) {
-          const int tmp = a;
-          a = b;
-          b = tmp;
-        }
-        if (b >= q) continue;
-        double* wj = W + (size_t)a * p;
-        double* wk = W + (size_t)b * p;
-        double sv[3] = {0.0, 0.0, 0.0};
+        if (!act[0] && !act[1]) continue;
+        double sv[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        const double* w0 = W + (size_t)a[0] * p;
+        const double* k0 = W + (size_t)b[0] * p;
+        const double* w1 = W + (size_t)a[1] * p;
+        const double* k1 = W + (size_t)b[1] * p;
         for (int i = lane; i < p; i += 32) {
-          const double x = wj[i], y = wk[i];
-          sv[0] += x * x;
-          sv[1] += y * y;
-          sv[2] += x * y;
+          if (act[0]) {
+            const double x = w0[i], y = k0[i];
+            sv[0] += x * x;
+            sv[1] += y * y;
+            sv[2] += x * y;
+          }
+          if (act[1]) {
+            const double x = w1[i], y = k1[i];
+            sv[3] += x * x;
+            sv[4] += y * y;
+            sv[5] += x * y;
+          }
         }
-        warp_sum_n<3>(sv);
-        const double sa = sv[0], sb = sv[1], sc = sv[2];
-        // |sc| <= 1e-15 sqrt(sa sb), squared (sa, sb >= 0)
-        if (sc * sc <= tol2 * (sa * sb) || sc == 0.0) continue;
+        warp_sum_n<6>(sv);
+        double cs[2], sn[2];
+        bool go[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const double sa = sv[3 * u], sb = sv[3 * u + 1], sc = sv[3 * u + 2];
+          // |sc| <= 1e-15 sqrt(sa sb), squared (sa, sb >= 0)
+          go[u] = act[u] && !(sc * sc <= tol2 * (sa * sb) || sc == 0.0);
+          cs[u] = 1.0;
+          sn[u] = 0.0;
+          if (go[u]) {
+            // tan of the rotation angle, zeta = (sb - sa) / (2 sc):
+            // tt = 2 sc sign(sb - sa) / (|sb - sa| + sqrt((sb - sa)^2 + 4 sc^2))
+            const double dd = sb - sa;
+            const double tt = (dd >= 0.0 ? 2.0 * sc : -2.0 * sc) / (fabs(dd) + sqrt(dd * dd + 4.0 * sc * sc));
+            cs[u] = rsqrt(1.0 + tt * tt);
+            sn[u] = cs[u] * tt;
+          }
+        }
+        if (!go[0] && !go[1]) continue;
         rot = 1;
-        ++nrot;
-        // tan of the rotation angle, zeta = (sb - sa) / (2 sc):
-        // tt = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)) = 2 sc sign(sb - sa) / (|sb - sa| + sqrt((sb - sa)^2 + 4 sc^2))
-        const double dd = sb - sa;
-        const double tt = (dd >= 0.0 ? 2.0 * sc : -2.0 * sc) / (fabs(dd) + sqrt(dd * dd + 4.0 * sc * sc));
-        const double cs = rsqrt(1.0 + tt * tt), sn = cs * tt;
-        for (int i = lane; i < p; i += 32) {
-          const double x = wj[i], y = wk[i];
-          wj[i] = cs * x - sn * y;
-          wk[i] = sn * x + cs * y;
-        }
-        double* jj = J + (size_t)a * q;
-        double* jk = J + (size_t)b * q;
-        for (int i = lane; i < q; i += 32) {
-          const double x = jj[i], y = jk[i];
-          jj[i] = cs * x - sn * y;
-          jk[i] = sn * x + cs * y;
+        nrot += (unsigned)go[0] + (unsigned)go[1];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (!go[u]) continue;
+          double* wj = W + (size_t)a[u] * p;
+          double* wk = W + (size_t)b[u] * p;
+          for (int i = lane; i < p; i += 32) {
+            const double x = wj[i], y = wk[i];
+            wj[i] = cs[u] * x - sn[u] * y;
+            wk[i] = sn[u] * x + cs[u] * y;
+          }
+          double* jj = J + (size_t)a[u] * q;
+          double* jk = J + (size_t)b[u] * q;
+          for (int i = lane; i < q; i += 32) {
+            const double x = jj[i], y = jk[i];
+            jj[i] = cs[u] * x - sn[u] * y;
+            jk[i] = sn[u] * x + cs[u] * y;
+          }
         }
       }
       __syncthreads();

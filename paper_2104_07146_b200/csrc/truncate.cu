@@ -1421,19 +1421,8 @@ __global__ void __cluster_dims__(kClu, 1, 1) __launch_bounds__(kTruncThreads)
 static int g_pair_cap = -1;
 static size_t g_pair_bytes = 0;
 void launch_truncate_pair(const TruncItem* d_items, const int* d_off, int targets, double eps,
-                          int* d_err, cudaStream_t st, bool defer_to_cluster) {
+                          int* d_err, cudaStream_t st, int* d_defer) {
   if (targets <= 0) return;
-  // per-target hand-over index for items that do not fit the pair layout
-  static thread_local int* d_defer = nullptr;
-  static thread_local int defer_cap = 0;
-  if (defer_to_cluster && targets > defer_cap) {
-    if (d_defer) {
-      HMGP_CUDA(cudaStreamSynchronize(st));
-      cudaFree(d_defer);
-    }
-    defer_cap = std::max(targets, 1 << 16);
-    HMGP_CUDA(cudaMalloc(&d_defer, (size_t)defer_cap * 4));
-  }
   if (g_pair_cap < 0) {
     cudaFuncAttributes fa;
     HMGP_CUDA(cudaFuncGetAttributes(&fa, k_truncate_pair));
@@ -1445,7 +1434,7 @@ void launch_truncate_pair(const TruncItem* d_items, const int* d_off, int target
                                    (int)g_pair_bytes));
     g_pair_cap = (int)(g_pair_bytes / 8);
   }
-  int* dfr = defer_to_cluster ? d_defer : nullptr;
+  int* dfr = d_defer;  // per-target hand-over index (targets ints), or nullptr
   k_truncate_pair<<<targets * 2, kTruncThreads, g_pair_bytes, st>>>(d_items, d_off, eps, d_err,
                                                                    g_pair_cap, dfr);
   HMGP_LAUNCH_CHECK();
