@@ -13,6 +13,8 @@
 // low-rank widths from device ints and the watermark rules (hblock.cpp:200,
 // hfactor.cpp:170) are evaluated inside the update kernel.  Temporaries come from
 // a stream-ordered stack arena with structural capacity bounds.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <functional>
 #include <climits>
@@ -33,6 +35,7 @@
 #include "phases.h"
 
 namespace hmgp_gpu {
+namespace cg = cooperative_groups;
 
 
 // ------------------------------------------------------------ utilities ---
@@ -1941,6 +1944,347 @@ __global__ void k_collect_diag(const LeafDev* __restrict__ lf, const int* __rest
   for (int i = threadIdx.x; i < L.m; i += blockDim.x) d[base[t] + i] = L.a[(size_t)i * L.m + i];
 }
 
+// ------------------------------------------------- persistent H-solves ---
+// One cooperative launch per sweep (K10).  Step t of the column sweep: CTA 0
+// solves diagonal leaf t on-chip, grid barrier, then every block of the step
+// (the blocks whose column range ends in leaf t for the forward sweep, whose
+// row range starts in leaf t for the backward one) is applied by the whole
+// grid: dense blocks and small low-rank blocks one CTA each, big low-rank
+// blocks split into 2048-row chunks (phase A: V^T x partials per input chunk,
+// barrier, phase B: y -= U (sum of partials, fixed order) per output chunk).
+// Blocks of one step write disjoint rows (they share the column range's end /
+// row range's start, so the lower-triangle partition makes their outputs
+// disjoint), so no atomics are needed and the result is deterministic.
+struct SUnit {
+  int leaf;
+  int kind;       // 0 dense, 1 small low-rank, 2 big phase A, 3 big phase B
+  int in0, out0;  // v offsets of the block's input / output ranges
+  int a0, a1;     // chunk of input (kind 2) or output (kind 3) rows, block-local
+  int p0, p1;     // kind 2: partial slot p0; kind 3: slots [p0, p1)
+};
+struct SStep {
+  int dleaf, base;
+  int u2b, u2e, u3b, u3e;
+};
+constexpr int kSolveChunk = 2048;
+__device__ int d_solve_stats_on;
+__device__ unsigned long long d_solve_cyc[2][6];
+constexpr int kSolveThreads = 256;
+
+struct SolvePlan {
+  std::vector<SUnit> units;
+  std::vector<SStep> steps;
+  int slots = 0, stride = 0;
+};
+
+static SolvePlan build_solve_plan(const Factor& F, const std::vector<SolveBlk>& flat,
+                                  const std::vector<int>& off, bool trans) {
+  SolvePlan P;
+  const int nd = (int)F.diag_leaf.size();
+  for (const SolveBlk& b : flat) {
+    const LeafDev& l = F.leaf[b.leaf];
+    if (l.kind != DENSE) P.stride = std::max(P.stride, l.cap);
+  }
+  P.stride = std::max(P.stride, 1);
+  std::vector<SUnit> u3;
+  for (int t = 0; t < nd; ++t) {
+    SStep s{};
+    s.dleaf = F.diag_leaf[t];
+    s.base = F.diag_base[t];
+    s.u2b = (int)P.units.size();
+    u3.clear();
+    for (int k = off[t]; k < off[t + 1]; ++k) {
+      const SolveBlk& b = flat[k];
+      const LeafDev& l = F.leaf[b.leaf];
+      const int in0 = trans ? b.r0 : b.c0, out0 = trans ? b.c0 : b.r0;
+      const int nin = trans ? l.m : l.n, nout = trans ? l.n : l.m;
+      if (l.kind == DENSE) {
+        P.units.push_back(SUnit{b.leaf, 0, in0, out0, 0, 0, 0, 0});
+      } else if (std::max(nin, nout) <= kSolveChunk) {
+        P.units.push_back(SUnit{b.leaf, 1, in0, out0, 0, 0, 0, 0});
+      } else {
+        const int p0 = P.slots;
+        for (int a = 0; a < nin; a += kSolveChunk)
+          P.units.push_back(SUnit{b.leaf, 2, in0, out0, a, std::min(nin, a + kSolveChunk), P.slots++, 0});
+        for (int a = 0; a < nout; a += kSolveChunk)
+          u3.push_back(SUnit{b.leaf, 3, in0, out0, a, std::min(nout, a + kSolveChunk), p0, P.slots});
+      }
+    }
+    s.u2e = (int)P.units.size();
+    s.u3b = s.u2e;
+    P.units.insert(P.units.end(), u3.begin(), u3.end());
+    s.u3e = (int)P.units.size();
+    P.steps.push_back(s);
+  }
+  return P;
+}
+
+__device__ void solve_unit(const SUnit& u, const LeafDev* __restrict__ lf, const int* __restrict__ rank,
+                           double* __restrict__ v, double* __restrict__ part, int stride, int trans,
+                           double* sT) {
+  const LeafDev L = lf[u.leaf];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (u.kind == 0) {
+    if (!trans && L.n <= 1024 - (int)blockDim.x) {  // y[out0 + i] -= sum_j D(i, j) x[in0 + j]
+      for (int j = threadIdx.x; j < L.n; j += blockDim.x) sT[j] = v[u.in0 + j];
+      __syncthreads();
+      const int split = (2 * L.m <= (int)blockDim.x) ? 2 : 1;
+      const int half = (L.n + split - 1) / split;
+      double* red = sT + 1024 - blockDim.x;  // scratch behind the x segment (n <= 1024 - blockDim)
+      for (int i0 = 0; i0 < L.m; i0 += blockDim.x / split) {
+        const int i = i0 + (int)threadIdx.x % (blockDim.x / split), h = (int)threadIdx.x / (blockDim.x / split);
+        double s = 0.0;
+        if (i < L.m) {
+          const int j1 = min(L.n, (h + 1) * half);
+#pragma unroll 8
+          for (int j = h * half; j < j1; ++j) s += L.a[(size_t)j * L.m + i] * sT[j];
+        }
+        if (split == 2) {
+          if (h == 1) red[threadIdx.x] = s;
+          __syncthreads();
+          if (h == 0 && i < L.m) v[u.out0 + i] -= s + red[threadIdx.x + blockDim.x / 2];
+          __syncthreads();
+        } else if (i < L.m) {
+          v[u.out0 + i] -= s;
+        }
+      }
+    } else if (!trans) {
+      for (int i = threadIdx.x; i < L.m; i += blockDim.x) {
+        double s = 0.0;
+        for (int j = 0; j < L.n; ++j) s += L.a[(size_t)j * L.m + i] * v[u.in0 + j];
+        v[u.out0 + i] -= s;
+      }
+    } else {  // y[out0 + j] -= sum_i D(i, j) x[in0 + i]
+      for (int j = w; j < L.n; j += nw) {
+        double s = 0.0;
+        for (int i = lane; i < L.m; i += 32) s += L.a[(size_t)j * L.m + i] * v[u.in0 + i];
+        s = warp_sum(s);
+        if (lane == 0) v[u.out0 + j] -= s;
+      }
+    }
+    return;
+  }
+  const int r = rank[u.leaf];
+  if (r <= 0) return;
+  const double* A = trans ? L.a : L.b;  // contracted with the input
+  const double* Bm = trans ? L.b : L.a;
+  const int nin = trans ? L.m : L.n, nout = trans ? L.n : L.m;
+  if (u.kind == 1 || u.kind == 2) {
+    const int j0 = u.kind == 1 ? 0 : u.a0, j1 = u.kind == 1 ? nin : u.a1;
+    for (int l = w; l < r; l += nw) {
+      double s = 0.0;
+#pragma unroll 4
+      for (int j = j0 + lane; j < j1; j += 32) s += A[(size_t)l * nin + j] * v[u.in0 + j];
+      s = warp_sum(s);
+      if (lane == 0) {
+        if (u.kind == 1)
+          sT[l] = s;
+        else
+          part[(size_t)u.p0 * stride + l] = s;
+      }
+    }
+    if (u.kind == 2) return;
+    __syncthreads();
+    for (int i = threadIdx.x; i < nout; i += blockDim.x) {
+      double s = 0.0;
+#pragma unroll 4
+      for (int l = 0; l < r; ++l) s += Bm[(size_t)l * nout + i] * sT[l];
+      v[u.out0 + i] -= s;
+    }
+    return;
+  }
+  // kind 3: T = sum of the block's partials (fixed order), then its output chunk
+  for (int l = threadIdx.x; l < r; l += blockDim.x) {
+    double s = 0.0;
+    for (int p = u.p0; p < u.p1; ++p) s += part[(size_t)p * stride + l];
+    sT[l] = s;
+  }
+  __syncthreads();
+  for (int i = u.a0 + threadIdx.x; i < u.a1; i += blockDim.x) {
+    double s = 0.0;
+    for (int l = 0; l < r; ++l) s += Bm[(size_t)l * nout + i] * sT[l];
+    v[u.out0 + i] -= s;
+  }
+}
+
+// Diagonal-leaf substitution by one CTA (L staged in shared memory when it
+// fits).  Blocked by 32: warp 0 solves a 32-row diagonal block with the values
+// in registers (one shuffle broadcast per column, reciprocal diagonal), then all
+// threads apply the block to the remaining rows (a small mat-vec).
+__device__ void solve_trsv_cta(const double* __restrict__ Lg, int b, double* __restrict__ xg, int trans,
+                               double* sm, bool staged) {
+  const double* L = Lg;
+  double* x = sm + (staged ? (size_t)b * b : 0);
+  double* inv = x + b;
+  if (staged) {  // 16-byte loads, eight in flight per thread
+    double* Ls = sm;
+    const int n2 = (b * b) / 2;
+    const double2* src = reinterpret_cast<const double2*>(Lg);
+    double2* dst = reinterpret_cast<double2*>(Ls);
+    if ((reinterpret_cast<uintptr_t>(Lg) & 15) == 0) {
+#pragma unroll 8
+      for (int e = threadIdx.x; e < n2; e += blockDim.x) dst[e] = src[e];
+      if ((b * b) & 1)
+        if (threadIdx.x == 0) Ls[b * b - 1] = Lg[b * b - 1];
+    } else {
+      for (int e = threadIdx.x; e < b * b; e += blockDim.x) Ls[e] = Lg[e];
+    }
+    L = Ls;
+  }
+  for (int e = threadIdx.x; e < b; e += blockDim.x) {
+    x[e] = xg[e];
+    inv[e] = 1.0 / Lg[(size_t)e * b + e];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  if (!trans) {
+    for (int jb = 0; jb < b; jb += 32) {
+      const int nb = min(32, b - jb);
+      if (threadIdx.x < 32) {
+        double xi = lane < nb ? x[jb + lane] : 0.0;
+        for (int j = 0; j < nb; ++j) {
+          if (lane == j) xi *= inv[jb + j];
+          const double xj = __shfl_sync(0xffffffffu, xi, j);
+          if (lane > j && lane < nb) xi -= L[(size_t)(jb + j) * b + jb + lane] * xj;
+        }
+        if (lane < nb) x[jb + lane] = xi;
+      }
+      __syncthreads();
+      for (int i = jb + nb + threadIdx.x; i < b; i += blockDim.x) {
+        double s = 0.0;
+#pragma unroll 8
+        for (int j = 0; j < nb; ++j) s += L[(size_t)(jb + j) * b + i] * x[jb + j];
+        x[i] -= s;
+      }
+      __syncthreads();
+    }
+  } else {
+    const int nblk = (b + 31) / 32;
+    for (int q = nblk - 1; q >= 0; --q) {
+      const int jb = q * 32, nb = min(32, b - jb);
+      // x_J -= L(I, J)^T x_I for the rows I below the block (already solved)
+      for (int j = jb + threadIdx.x; j < jb + nb; j += blockDim.x) {
+        double s = 0.0;
+#pragma unroll 8
+        for (int i = jb + nb; i < b; ++i) s += L[(size_t)j * b + i] * x[i];
+        x[j] -= s;
+      }
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        double xi = lane < nb ? x[jb + lane] : 0.0;
+        for (int j = nb - 1; j >= 0; --j) {
+          if (lane == j) xi *= inv[jb + j];
+          const double xj = __shfl_sync(0xffffffffu, xi, j);
+          if (lane < j) xi -= L[(size_t)(jb + lane) * b + jb + j] * xj;
+        }
+        if (lane < nb) x[jb + lane] = xi;
+      }
+      __syncthreads();
+    }
+  }
+  for (int e = threadIdx.x; e < b; e += blockDim.x) xg[e] = x[e];
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kSolveThreads) k_solve_sweep(const SStep* __restrict__ steps, int nsteps,
+                                                              const SUnit* __restrict__ units,
+                                                              const LeafDev* __restrict__ lf,
+                                                              const int* __restrict__ rank, double* v,
+                                                              double* part, int stride, int trans,
+                                                              int smem_b) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double ssm[];
+  __shared__ double sT[1024];
+  long long tc = clock64(), acc[6] = {0, 0, 0, 0, 0, 0};
+  auto tick = [&](int i) {
+    const long long now = clock64();
+    acc[i] += now - tc;
+    tc = now;
+  };
+  for (int s = 0; s < nsteps; ++s) {
+    const SStep st = steps[trans ? nsteps - 1 - s : s];
+    if (blockIdx.x == 0) {
+      const LeafDev d = lf[st.dleaf];
+      solve_trsv_cta(d.a, d.m, v + st.base, trans, ssm, d.m <= smem_b);
+    }
+    tick(0);
+    grid.sync();
+    tick(1);
+    for (int k = st.u2b + blockIdx.x; k < st.u2e; k += gridDim.x) {
+      solve_unit(units[k], lf, rank, v, part, stride, trans, sT);
+      __syncthreads();
+    }
+    tick(2);
+    if (st.u3e > st.u3b) {
+      grid.sync();
+      tick(3);
+      for (int k = st.u3b + blockIdx.x; k < st.u3e; k += gridDim.x) {
+        solve_unit(units[k], lf, rank, v, part, stride, trans, sT);
+        __syncthreads();
+      }
+      tick(4);
+    }
+    if (blockIdx.x == 0 && s + 1 < nsteps) {  // warm L2 with the next diagonal leaf
+      const LeafDev d = lf[steps[trans ? nsteps - 2 - s : s + 1].dleaf];
+      const char* p = reinterpret_cast<const char*>(d.a);
+      const size_t bytes = (size_t)d.m * d.m * 8;
+      for (size_t o = (size_t)threadIdx.x * 128; o < bytes; o += (size_t)blockDim.x * 128)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(p + o));
+    }
+    grid.sync();
+    tick(5);
+  }
+  if (d_solve_stats_on && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == 1))
+    for (int i = 0; i < 6; ++i) atomicAdd(&d_solve_cyc[blockIdx.x][i], (unsigned long long)acc[i]);
+}
+
+static void solve_sweep(const Factor& F, double* v, bool trans, cudaStream_t st) {
+  const int nsteps = (int)F.diag_leaf.size();
+  if (nsteps == 0) return;
+  static int grid = 0, smem_b = 0;
+  static size_t smem = 0;
+  if (!grid) {
+    int dev = 0, sms = 0, optin = 0;
+    HMGP_CUDA(cudaGetDevice(&dev));
+    HMGP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    HMGP_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    smem = std::min<size_t>((size_t)optin - 8192 - 1024, (size_t)200 * 1024);
+    int b = 1;
+    while ((size_t)(b + 1) * (b + 1) * 8 + 2 * (size_t)(b + 1) * 8 <= smem) ++b;
+    smem_b = b;
+    HMGP_CUDA(cudaFuncSetAttribute(k_solve_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per = 0;
+    HMGP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_solve_sweep, kSolveThreads, smem));
+    grid = std::max(1, per) * sms;
+  }
+  const SStep* d_steps = static_cast<const SStep*>(trans ? F.d_bsteps : F.d_fsteps);
+  const SUnit* d_units = static_cast<const SUnit*>(trans ? F.d_bunits : F.d_funits);
+  int ns = nsteps, tr = trans ? 1 : 0, stride = F.solve_stride, sb = smem_b;
+  double* part = F.d_part;
+  const LeafDev* lf = F.d_leaf;
+  const int* rk = F.d_rank;
+  void* args[] = {(void*)&d_steps, &ns, (void*)&d_units, (void*)&lf, (void*)&rk, &v, &part, &stride, &tr, &sb};
+  const bool stats = getenv("HMGP_SOLVE_STATS") != nullptr;
+  if (stats) {
+    const int one = 1;
+    static unsigned long long z[2][6] = {};
+    HMGP_CUDA(cudaMemcpyToSymbol(d_solve_stats_on, &one, 4));
+    HMGP_CUDA(cudaMemcpyToSymbol(d_solve_cyc, z, sizeof(z)));
+  }
+  HMGP_CUDA(cudaLaunchCooperativeKernel((const void*)k_solve_sweep, dim3(grid), dim3(kSolveThreads), args, smem, st));
+  if (stats) {
+    unsigned long long c[2][6];
+    HMGP_CUDA(cudaStreamSynchronize(st));
+    HMGP_CUDA(cudaMemcpyFromSymbol(c, d_solve_cyc, sizeof(c)));
+    for (int b = 0; b < 2; ++b)
+      fprintf(stderr,
+              "[hmgp] solve sweep (%s, CTA %d of %d, ms @1.965GHz): trsv %.2f sync %.2f units %.2f sync %.2f "
+              "units-B %.2f sync %.2f\n",
+              trans ? "bwd" : "fwd", b, grid, c[b][0] / 1.965e6, c[b][1] / 1.965e6, c[b][2] / 1.965e6,
+              c[b][3] / 1.965e6, c[b][4] / 1.965e6, c[b][5] / 1.965e6);
+  }
+}
+
 // ------------------------------------------------------------ Factor API --
 Factor::~Factor() {
   cudaFree(pool);
@@ -1952,6 +2296,11 @@ Factor::~Factor() {
   cudaFree(d_fwd);
   cudaFree(d_bwd);
   cudaFree(d_work);
+  cudaFree(d_fsteps);
+  cudaFree(d_funits);
+  cudaFree(d_bsteps);
+  cudaFree(d_bunits);
+  cudaFree(d_part);
 }
 
 void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size_t arena_bytes) {
@@ -2165,12 +2514,33 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
   HMGP_CUDA(cudaMemcpyAsync(F.d_fwd, flat_f.data(), sizeof(SolveBlk) * flat_f.size(), cudaMemcpyHostToDevice, st));
   HMGP_CUDA(cudaMemcpyAsync(F.d_bwd, flat_b.data(), sizeof(SolveBlk) * flat_b.size(), cudaMemcpyHostToDevice, st));
   HMGP_CUDA(cudaMalloc(&F.d_work, 8ull * (2 * G.n + 1024)));
+  {  // persistent-sweep plans (K10)
+    const SolvePlan pf = build_solve_plan(F, flat_f, F.fwd_off, false);
+    const SolvePlan pb = build_solve_plan(F, flat_b, F.bwd_off, true);
+    auto up = [&](const void* src, size_t bytes) {
+      void* d = nullptr;
+      HMGP_CUDA(cudaMalloc(&d, std::max<size_t>(bytes, 16)));
+      if (bytes) HMGP_CUDA(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, st));
+      return d;
+    };
+    F.d_fsteps = up(pf.steps.data(), pf.steps.size() * sizeof(SStep));
+    F.d_funits = up(pf.units.data(), pf.units.size() * sizeof(SUnit));
+    F.d_bsteps = up(pb.steps.data(), pb.steps.size() * sizeof(SStep));
+    F.d_bunits = up(pb.units.data(), pb.units.size() * sizeof(SUnit));
+    F.solve_stride = std::max(pf.stride, pb.stride);
+    const size_t pd = (size_t)std::max(pf.slots, pb.slots) * F.solve_stride;
+    HMGP_CUDA(cudaMalloc(&F.d_part, std::max<size_t>(pd, 1) * 8));
+  }
   phase_mark(PH_LAYOUT);
   HMGP_CUDA(cudaStreamSynchronize(st));
 }
 
 // v (tree order, device) <- L^{-1} v
 void forward_solve(const Factor& F, double* v, cudaStream_t st) {
+  if (F.d_fsteps && !getenv("HMGP_SOLVE_LEGACY")) {
+    solve_sweep(F, v, false, st);
+    return;
+  }
   const int nd = (int)F.diag_leaf.size();
   for (int t = 0; t < nd; ++t) {
     const LeafDev& l = F.leaf[F.diag_leaf[t]];
@@ -2186,6 +2556,10 @@ void forward_solve(const Factor& F, double* v, cudaStream_t st) {
 }
 // v <- L^{-T} v
 void backward_solve(const Factor& F, double* v, cudaStream_t st) {
+  if (F.d_bsteps && !getenv("HMGP_SOLVE_LEGACY")) {
+    solve_sweep(F, v, true, st);
+    return;
+  }
   const int nd = (int)F.diag_leaf.size();
   for (int t = nd - 1; t >= 0; --t) {
     const LeafDev& l = F.leaf[F.diag_leaf[t]];

@@ -35,6 +35,13 @@ struct Factor {
   void* d_fwd = nullptr;
   void* d_bwd = nullptr;
   double* d_work = nullptr;
+  // persistent-sweep solve plans (factor.cu, K10)
+  void* d_fsteps = nullptr;
+  void* d_funits = nullptr;
+  void* d_bsteps = nullptr;
+  void* d_bunits = nullptr;
+  double* d_part = nullptr;
+  int solve_stride = 1;
   size_t arena_peak = 0;
   ~Factor();
 };

@@ -23,8 +23,12 @@ void linalg_counters_read_reset(double* g, double* t, double* l) {
 }
 
 // ----------------------------------------------------------------- GEMM ---
-// 64x64 output tile per CTA iteration, k-slabs of 16 staged in shared memory,
-// 256 threads x (4 x 4) register micro-tile.  Dimensions may live on device.
+// FP64 tensor cores (DMMA.8x8x4, mma.sync.m8n8k4.f64).  64x64 output tile per
+// CTA iteration, k-slabs of 16 staged in shared memory, 8 warps as 2 x 4, each
+// warp a 32x16 sub-tile = 4 x 2 DMMA accumulators (16 doubles per thread).
+// Fragments (PTX m8n8k4 .f64): A a0 at (row lane/4, k lane%4); B b0 at
+// (k lane%4, col lane/4); C c0,c1 at (row lane/4, col 2*(lane%4) + {0,1}).
+// Dimensions may live on device.
 constexpr int GT = 64, GK = 16;
 
 __device__ void gemm_item(const GemmItem& it, int tile0, int tstride, bool count);
@@ -48,6 +52,12 @@ void launch_gemm_seq(const GemmItem* d_items, const int* d_off, int targets, cud
   HMGP_LAUNCH_CHECK();
 }
 
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
 __device__ void gemm_item(const GemmItem& it, int tile0, int tstride, bool count) {
   const int M = it.M.get(), N = it.N.get(), K = it.K.get();
   if (M <= 0 || N <= 0) return;
@@ -55,14 +65,16 @@ __device__ void gemm_item(const GemmItem& it, int tile0, int tstride, bool count
   const int tm = (M + GT - 1) / GT, tn = (N + GT - 1) / GT;
   __shared__ double sA[GK][GT + 1];
   __shared__ double sB[GK][GT + 1];
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int wr = (w >> 2) * 32, wc = (w & 3) * 16;  // warp sub-tile origin
+  const int fr = lane >> 2, fk = lane & 3;           // fragment row / k index
   for (int tile = tile0; tile < tm * tn; tile += tstride) {
     const int i0 = (tile % tm) * GT, j0 = (tile / tm) * GT;
-    double acc[4][4];
+    double acc[4][2][2];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+      for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
     for (int k0 = 0; k0 < K; k0 += GK) {
       __syncthreads();
       for (int e = threadIdx.x; e < GK * GT; e += 256) {
@@ -90,43 +102,44 @@ __device__ void gemm_item(const GemmItem& it, int tile0, int tstride, bool count
           kk = e / GT;
         }
         const int gj = j0 + jj, gk2 = k0 + kk;
-        double w = 0.0;
+        double wv = 0.0;
         if (gj < N && gk2 < K)
-          w = it.tb ? it.B[(size_t)gk2 * it.ldb + gj] : it.B[(size_t)gj * it.ldb + gk2];
-        sB[kk][jj] = w;
+          wv = it.tb ? it.B[(size_t)gk2 * it.ldb + gj] : it.B[(size_t)gj * it.ldb + gk2];
+        sB[kk][jj] = wv;
       }
       __syncthreads();
 #pragma unroll
-      for (int kk = 0; kk < GK; ++kk) {
-        double a[4], b[4];
+      for (int ks = 0; ks < GK; ks += 4) {
+        double af[4], bf[2];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          a[q] = sA[kk][tx + 16 * q];
-          b[q] = sB[kk][ty + 16 * q];
-        }
+        for (int rb = 0; rb < 4; ++rb) af[rb] = sA[ks + fk][wr + rb * 8 + fr];
 #pragma unroll
-        for (int p = 0; p < 4; ++p)
+        for (int cb = 0; cb < 2; ++cb) bf[cb] = sB[ks + fk][wc + cb * 8 + fr];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) acc[p][q] += a[p] * b[q];
+        for (int rb = 0; rb < 4; ++rb)
+#pragma unroll
+          for (int cb = 0; cb < 2; ++cb) dmma884(acc[rb][cb], af[rb], bf[cb]);
       }
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int gj = j0 + ty + 16 * q;
-      if (gj >= N) continue;
+    for (int cb = 0; cb < 2; ++cb)
 #pragma unroll
-      for (int p = 0; p < 4; ++p) {
-        const int gi = i0 + tx + 16 * p;
-        if (gi < M) {
+      for (int h = 0; h < 2; ++h) {
+        const int gj = j0 + wc + cb * 8 + 2 * fk + h;
+        if (gj >= N) continue;
+#pragma unroll
+        for (int rb = 0; rb < 4; ++rb) {
+          const int gi = i0 + wr + rb * 8 + fr;
+          if (gi >= M) continue;
+          const double v = acc[rb][cb][h];
           if (it.atomic == 1)
-            atomicAdd(&it.C[(size_t)gj * it.ldc + gi], it.alpha * acc[p][q]);
+            atomicAdd(&it.C[(size_t)gj * it.ldc + gi], it.alpha * v);
           else if (it.atomic == 2)
-            it.C[(size_t)gj * it.ldc + gi] = it.alpha * acc[p][q];
+            it.C[(size_t)gj * it.ldc + gi] = it.alpha * v;
           else
-            it.C[(size_t)gj * it.ldc + gi] += it.alpha * acc[p][q];
+            it.C[(size_t)gj * it.ldc + gi] += it.alpha * v;
         }
       }
-    }
   }
 }
 

@@ -183,14 +183,87 @@ __device__ void cta_apply_q_map(const double* QR, int m, int ldq, int kq, const 
   }
 }
 
-// One-sided Jacobi with the rotations and stopping rule of cta_jacobi; the
-// three dot products of a pair are reduced together, one barrier per round.
+// One-sided Jacobi with the rotations and stopping rule of cta_jacobi, one
+// barrier per round.  A pair is handled by a group of G lanes (G sized to the
+// column length p: 8 lanes for p <= 64, ...), so a warp works on 32/G pairs at
+// once and the three dot products of a pair reduce over log2(G) shuffle levels
+// -- the round is bound by instruction issue, not by latency, and this cuts
+// the instructions per pair by ~32/G.
 // tol: rotate a pair while |w_a . w_b| > tol * |w_a| |w_b|.  R = J G^T holds
 // exactly whatever the convergence state, so the truncation error is bounded by
 // the norms of the dropped columns in any case; a tolerance tied to the cut
 // (tol <= 1e-4 eps) only spares the final sweeps.
-__device__ double cta_jacobi2(double* W, int p, int q, double* J, int* sweeps_out, double tol) {
+template <int G>
+__device__ bool jacobi_round(double* W, int p, int q, double* J, int qq, int m1, int round, double tol2,
+                             unsigned& nrot) {
+  constexpr int kGpw = 32 / G;  // pairs per warp at once
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int gi = lane / G, gl = lane % G;
+  bool rot = false;
+  for (int base = w * kGpw; base < qq / 2; base += nw * kGpw) {
+    const int t = base + gi;
+    bool act = t < qq / 2;
+    int a = 0, b = 0;
+    if (act) {
+      if (t == 0) {
+        a = qq - 1;
+        b = round;
+      } else {  // (round + t) mod m1 and (round - t) mod m1 without divisions
+        a = round + t;
+        if (a >= m1) a -= m1;
+        b = round - t;
+        if (b < 0) b += m1;
+      }
+      if (a > b) {
+        const int tmp = a;
+        a = b;
+        b = tmp;
+      }
+      if (b >= q) act = false;
+    }
+    double sa = 0.0, sb = 0.0, sc = 0.0;
+    double* wj = W + (size_t)a * p;
+    double* wk = W + (size_t)b * p;
+    if (act)
+      for (int i = gl; i < p; i += G) {
+        const double x = wj[i], y = wk[i];
+        sa += x * x;
+        sb += y * y;
+        sc += x * y;
+      }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+      sa += __shfl_xor_sync(0xffffffffu, sa, o);
+      sb += __shfl_xor_sync(0xffffffffu, sb, o);
+      sc += __shfl_xor_sync(0xffffffffu, sc, o);
+    }
+    // |sc| <= tol sqrt(sa sb), squared (sa, sb >= 0)
+    if (!act || sc * sc <= tol2 * (sa * sb) || sc == 0.0) continue;
+    rot = true;
+    if (gl == 0) ++nrot;
+    // tan of the rotation angle, zeta = (sb - sa) / (2 sc):
+    // tt = 2 sc sign(sb - sa) / (|sb - sa| + sqrt((sb - sa)^2 + 4 sc^2))
+    const double dd = sb - sa;
+    const double tt = (dd >= 0.0 ? 2.0 * sc : -2.0 * sc) / (fabs(dd) + sqrt(dd * dd + 4.0 * sc * sc));
+    const double cs = rsqrt(1.0 + tt * tt), sn = cs * tt;
+    for (int i = gl; i < p; i += G) {
+      const double x = wj[i], y = wk[i];
+      wj[i] = cs * x - sn * y;
+      wk[i] = sn * x + cs * y;
+    }
+    double* jj = J + (size_t)a * q;
+    double* jk = J + (size_t)b * q;
+    for (int i = gl; i < q; i += G) {
+      const double x = jj[i], y = jk[i];
+      jj[i] = cs * x - sn * y;
+      jk[i] = sn * x + cs * y;
+    }
+  }
+  return rot;
+}
+
+__device__ double cta_jacobi2(double* W, int p, int q, double* J, int* sweeps_out, double tol) {
+  const int lane = threadIdx.x & 31;
   for (int idx = threadIdx.x; idx < q * q; idx += blockDim.x) J[idx] = (idx % (q + 1) == 0) ? 1.0 : 0.0;
   __shared__ unsigned s_nrot2;
   if (threadIdx.x == 0) s_nrot2 = 0;
@@ -206,102 +279,25 @@ __device__ double cta_jacobi2(double* W, int p, int q, double* J, int* sweeps_ou
   int sweeps = 0;
   for (int sweep = 0; sweep < 60; ++sweep) {
     ++sweeps;
-    int rot = 0;
+    bool rot = false;
     for (int round = 0; round < m1; ++round) {
-      // two pairs per warp at once: their dot products share one interleaved
-      // reduction and their rotation scalars overlap (per pair the arithmetic
-      // is exactly the single-pair sequence)
-      for (int t0 = w; t0 < qq / 2; t0 += 2 * nw) {
-        int a[2], b[2];
-        bool act[2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int t = t0 + u * nw;
-          act[u] = t < qq / 2;
-          int aa, bb;
-          if (t == 0) {
-            aa = qq - 1;
-            bb = round;
-          } else {  // (round + t) mod m1 and (round - t) mod m1 without divisions
-            aa = round + t;
-            if (aa >= m1) aa -= m1;
-            bb = round - t;
-            if (bb < 0) bb += m1;
-          }
-          if (aa > bb) {
-            const int tmp = aa;
-            aa = bb;
-            bb = tmp;
-          }
-          if (bb >= q) act[u] = false;
-          a[u] = act[u] ? aa : 0;
-          b[u] = act[u] ? bb : 0;
-        }
-        if (!act[0] && !act[1]) continue;
-        double sv[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-        const double* w0 = W + (size_t)a[0] * p;
-        const double* k0 = W + (size_t)b[0] * p;
-        const double* w1 = W + (size_t)a[1] * p;
-        const double* k1 = W + (size_t)b[1] * p;
-        for (int i = lane; i < p; i += 32) {
-          if (act[0]) {
-            const double x = w0[i], y = k0[i];
-            sv[0] += x * x;
-            sv[1] += y * y;
-            sv[2] += x * y;
-          }
-          if (act[1]) {
-            const double x = w1[i], y = k1[i];
-            sv[3] += x * x;
-            sv[4] += y * y;
-            sv[5] += x * y;
-          }
-        }
-        warp_sum_n<6>(sv);
-        double cs[2], sn[2];
-        bool go[2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const double sa = sv[3 * u], sb = sv[3 * u + 1], sc = sv[3 * u + 2];
-          // |sc| <= 1e-15 sqrt(sa sb), squared (sa, sb >= 0)
-          go[u] = act[u] && !(sc * sc <= tol2 * (sa * sb) || sc == 0.0);
-          cs[u] = 1.0;
-          sn[u] = 0.0;
-          if (go[u]) {
-            // tan of the rotation angle, zeta = (sb - sa) / (2 sc):
-            // tt = 2 sc sign(sb - sa) / (|sb - sa| + sqrt((sb - sa)^2 + 4 sc^2))
-            const double dd = sb - sa;
-            const double tt = (dd >= 0.0 ? 2.0 * sc : -2.0 * sc) / (fabs(dd) + sqrt(dd * dd + 4.0 * sc * sc));
-            cs[u] = rsqrt(1.0 + tt * tt);
-            sn[u] = cs[u] * tt;
-          }
-        }
-        if (!go[0] && !go[1]) continue;
-        rot = 1;
-        nrot += (unsigned)go[0] + (unsigned)go[1];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          if (!go[u]) continue;
-          double* wj = W + (size_t)a[u] * p;
-          double* wk = W + (size_t)b[u] * p;
-          for (int i = lane; i < p; i += 32) {
-            const double x = wj[i], y = wk[i];
-            wj[i] = cs[u] * x - sn[u] * y;
-            wk[i] = sn[u] * x + cs[u] * y;
-          }
-          double* jj = J + (size_t)a[u] * q;
-          double* jk = J + (size_t)b[u] * q;
-          for (int i = lane; i < q; i += 32) {
-            const double x = jj[i], y = jk[i];
-            jj[i] = cs[u] * x - sn[u] * y;
-            jk[i] = sn[u] * x + cs[u] * y;
-          }
-        }
-      }
+      if (p <= 32)
+        rot |= jacobi_round<4>(W, p, q, J, qq, m1, round, tol2, nrot);
+      else if (p <= 64)
+        rot |= jacobi_round<8>(W, p, q, J, qq, m1, round, tol2, nrot);
+      else if (p <= 128)
+        rot |= jacobi_round<16>(W, p, q, J, qq, m1, round, tol2, nrot);
+      else
+        rot |= jacobi_round<32>(W, p, q, J, qq, m1, round, tol2, nrot);
       __syncthreads();
     }
     if (!__syncthreads_or(rot)) break;
   }
+  nrot += __shfl_xor_sync(0xffffffffu, nrot, 16);
+  nrot += __shfl_xor_sync(0xffffffffu, nrot, 8);
+  nrot += __shfl_xor_sync(0xffffffffu, nrot, 4);
+  nrot += __shfl_xor_sync(0xffffffffu, nrot, 2);
+  nrot += __shfl_xor_sync(0xffffffffu, nrot, 1);
   if (lane == 0 && nrot) atomicAdd(&s_nrot2, nrot);
   __syncthreads();
   if (threadIdx.x == 0) *sweeps_out = sweeps;
