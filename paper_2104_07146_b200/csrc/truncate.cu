@@ -68,6 +68,8 @@ __device__ __forceinline__ void hist_add(int path, int m, int n, int r, long lon
 // stages: 0 stage-in / W formation, 1 Householder QR of the factors, 2 RRQR of
 // the core, 3 Jacobi, 4 Q application / write-back; d_stage_sweeps counts sweeps
 __device__ unsigned long long d_stage_cyc[3][5], d_stage_sweeps[3], d_stage_jac[3];
+// (stats mode) global cluster path stages: stage-in, QR U, QR V, core SVD, write, apply U, apply V
+__device__ unsigned long long d_clu_cyc[7];
 __device__ __forceinline__ void stage_add(int path, int st, long long& t) {
   if (!d_hist_on || threadIdx.x != 0) return;
   const long long now = clock64();
@@ -92,6 +94,15 @@ void truncate_hist_print() {
             " jacobi calls %llu, sweeps/call %.2f\n",
             p == 2 ? "pair" : p ? "large" : "small", sc[p][0] / 1.9e9, sc[p][1] / 1.9e9, sc[p][2] / 1.9e9, sc[p][3] / 1.9e9,
             sc[p][4] / 1.9e9, sj[p], sj[p] ? (double)sw[p] / sj[p] : 0.0);
+  {
+    static unsigned long long cc[7];
+    HMGP_CUDA(cudaMemcpyFromSymbol(cc, d_clu_cyc, sizeof(cc)));
+    fprintf(stderr,
+            "[hmgp]   trunc cluster(global) stages (s): stage-in %.3f qrU %.3f qrV %.3f core %.3f write %.3f "
+            "applyU %.3f applyV %.3f\n",
+            cc[0] / 1.9e9, cc[1] / 1.9e9, cc[2] / 1.9e9, cc[3] / 1.9e9, cc[4] / 1.9e9, cc[5] / 1.9e9,
+            cc[6] / 1.9e9);
+  }
   static const char* nm[4] = {"small", "large", "cluster", "pair"};
   for (int p = 0; p < 4; ++p)
     for (int a = 0; a < kHM; ++a)
@@ -799,109 +810,140 @@ constexpr int kCluMaxR = 1024;
 
 namespace cg = cooperative_groups;
 
+constexpr int kGather = 64;  // remote partials fetched per chunk (per rank)
+
 struct CluShared {
   double part[2][kCluMaxR + 2];  // per column step: [0] tail norm^2, [1] row-k value, [2..] dots
+  double gb[kClu][kGather];      // local copy of the ranks' partials being summed
 };
 
-// Distributed Householder QR of A (m x r, ld m) over the cluster's row slices.
-__device__ void clu_qr(cg::cluster_group& cl, CluShared& sh, double* A, int m, int r, double* tau) {
+// Distributed Householder QR of A (m x r, ld m) over the row slices of a group
+// of gs ranks starting at rank g0 (the U and V factors run at once on the two
+// halves of the cluster).  Every rank executes the same barrier sequence: kit
+// column steps (the larger of the two groups' min(m, r)), two cluster barriers
+// each, whether or not its group has work at that step.
+__device__ void clu_qr(cg::cluster_group& cl, CluShared& sh, double* A, int m, int r, double* tau, int g0,
+                       int gs, int kit) {
+  double (*gb)[kGather] = sh.gb;
   const int rank = cl.block_rank();
-  const int ms = (m + kClu - 1) / kClu, lo = rank * ms, hi = min(m, lo + ms);
+  const int ms = (m + gs - 1) / gs, lo = (rank - g0) * ms, hi = min(m, lo + ms);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   __shared__ double red[32];
   const int kmax = min(m, r);
-  for (int k = 0; k < kmax; ++k) {
+  for (int k = 0; k < kit; ++k) {
+    const bool act = k < kmax;
     double* P = sh.part[k & 1];
     double* col = A + (size_t)k * m;
     // (a) partial tail norm^2 over own rows > k; owner of row k publishes A(k,k)
     double part = 0.0;
-    for (int i = max(lo, k + 1) + threadIdx.x; i < hi; i += blockDim.x) part += col[i] * col[i];
+    if (act)
+      for (int i = max(lo, k + 1) + threadIdx.x; i < hi; i += blockDim.x) part += col[i] * col[i];
     part = block_sum(part, red);
     if (threadIdx.x == 0) {
       P[0] = part;
-      P[1] = (k >= lo && k < hi) ? col[k] : 0.0;
+      P[1] = (act && k >= lo && k < hi) ? col[k] : 0.0;
     }
     cl.sync();
-    // (b) every CTA forms the same reflector from the cluster-wide sums
+    // (b) every rank of the group forms the same reflector from the group sums
+    // (remote values fetched once, in parallel, summed in rank order)
+    if (threadIdx.x < 2 * gs) gb[0][threadIdx.x] = cl.map_shared_rank(P, g0 + threadIdx.x % gs)[threadIdx.x / gs];
+    __syncthreads();
     double tail2 = 0.0, c0 = 0.0;
-    for (int c = 0; c < kClu; ++c) {
-      const double* Q = cl.map_shared_rank(P, c);
-      tail2 += Q[0];
-      c0 += Q[1];
+    for (int c = 0; c < gs; ++c) {
+      tail2 += gb[0][c];
+      c0 += gb[0][gs + c];
     }
-    double t, beta, inv;
-    if (tail2 <= 2.2250738585072014e-308) {
-      t = 0.0;
-      beta = c0;
-      inv = 0.0;
-    } else {
+    double t = 0.0, beta = c0, inv = 0.0;
+    if (tail2 > 2.2250738585072014e-308) {
       beta = sqrt(c0 * c0 + tail2);
       if (c0 >= 0.0) beta = -beta;
       inv = 1.0 / (c0 - beta);
       t = (beta - c0) / beta;
     }
-    for (int i = max(lo, k + 1) + threadIdx.x; i < hi; i += blockDim.x) col[i] = (t == 0.0) ? 0.0 : col[i] * inv;
+    if (act)
+      for (int i = max(lo, k + 1) + threadIdx.x; i < hi; i += blockDim.x) col[i] = (t == 0.0) ? 0.0 : col[i] * inv;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (act && threadIdx.x == 0) {
       if (k >= lo && k < hi) col[k] = beta;
-      if (rank == 0) tau[k] = t;
+      if (rank == g0) tau[k] = t;
     }
-    if (t == 0.0) {
-      cl.sync();
-      continue;
-    }
+    const bool up = act && t != 0.0;
     // (c) partial dots v^T A(:, j) over own rows for the trailing columns
-    for (int j = k + 1 + w; j < r; j += nw) {
-      const double* cj = A + (size_t)j * m;
-      double s = 0.0;
-      for (int i = max(lo, k + 1) + lane; i < hi; i += 32) s += col[i] * cj[i];
-      s = warp_sum(s);
-      if (lane == 0) P[2 + j] = s + ((k >= lo && k < hi) ? cj[k] : 0.0);
-    }
+    if (up)
+      for (int j = k + 1 + w; j < r; j += nw) {
+        const double* cj = A + (size_t)j * m;
+        double s = 0.0;
+        for (int i = max(lo, k + 1) + lane; i < hi; i += 32) s += col[i] * cj[i];
+        s = warp_sum(s);
+        if (lane == 0) P[2 + j] = s + ((k >= lo && k < hi) ? cj[k] : 0.0);
+      }
     cl.sync();
-    // (d) full dots from every CTA, update own rows
-    for (int j = k + 1 + w; j < r; j += nw) {
-      double s = 0.0;
-      for (int c = 0; c < kClu; ++c) s += cl.map_shared_rank(P, c)[2 + j];
-      s *= t;
-      double* cj = A + (size_t)j * m;
-      for (int i = max(lo, k + 1) + lane; i < hi; i += 32) cj[i] -= s * col[i];
-      if (lane == 0 && k >= lo && k < hi) cj[k] -= s;
-    }
-    __syncthreads();
+    // (d) full dots from the group (remote partials gathered in chunks of
+    // kGather columns, summed in rank order), update own rows
+    if (up)
+      for (int jc = k + 1; jc < r; jc += kGather) {
+        const int nj = min(kGather, r - jc);
+        if (threadIdx.x < gs * kGather) {
+          const int cc = threadIdx.x / kGather, jj = threadIdx.x % kGather;
+          if (jj < nj) gb[cc][jj] = cl.map_shared_rank(P, g0 + cc)[2 + jc + jj];
+        }
+        __syncthreads();
+        for (int j = jc + w; j < jc + nj; j += nw) {
+          double s = 0.0;
+          for (int c = 0; c < gs; ++c) s += gb[c][j - jc];
+          s *= t;
+          double* cj = A + (size_t)j * m;
+          for (int i = max(lo, k + 1) + lane; i < hi; i += 32) cj[i] -= s * col[i];
+          if (lane == 0 && k >= lo && k < hi) cj[k] -= s;
+        }
+        __syncthreads();
+      }
   }
   cl.sync();
 }
 
-// E <- Q E over the cluster's row slices (Q from clu_qr), E m x c (ld m).
+// E <- Q E over a group's row slices (Q from clu_qr with the same group), E m x c
+// (ld m); kit reflector steps for every rank (uniform barrier sequence).
 __device__ void clu_apply_q(cg::cluster_group& cl, CluShared& sh, const double* A, int m, int kq,
-                            const double* tau, double* E, int c) {
+                            const double* tau, double* E, int c, int g0, int gs, int kit) {
+  double (*gb)[kGather] = sh.gb;
   const int rank = cl.block_rank();
-  const int ms = (m + kClu - 1) / kClu, lo = rank * ms, hi = min(m, lo + ms);
+  const int ms = (m + gs - 1) / gs, lo = (rank - g0) * ms, hi = min(m, lo + ms);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  int step = 0;  // buffer parity per EXECUTED step (skipped reflectors do not sync)
-  for (int k = kq - 1; k >= 0; --k) {
-    const double t = tau[k];
-    if (t == 0.0) continue;
-    double* P = sh.part[(step++) & 1];
+  for (int k = kit - 1; k >= 0; --k) {
+    const double t = k < kq ? tau[k] : 0.0;
+    const bool up = t != 0.0;
+    double* P = sh.part[k & 1];
     const double* v = A + (size_t)k * m;
-    for (int j = w; j < c; j += nw) {
-      const double* e = E + (size_t)j * m;
-      double s = 0.0;
-      for (int i = max(lo, k + 1) + lane; i < hi; i += 32) s += v[i] * e[i];
-      s = warp_sum(s);
-      if (lane == 0) P[2 + j] = s + ((k >= lo && k < hi) ? e[k] : 0.0);
-    }
+    if (up)
+      for (int j = w; j < c; j += nw) {
+        const double* e = E + (size_t)j * m;
+        double s = 0.0;
+        for (int i = max(lo, k + 1) + lane; i < hi; i += 32) s += v[i] * e[i];
+        s = warp_sum(s);
+        if (lane == 0) P[2 + j] = s + ((k >= lo && k < hi) ? e[k] : 0.0);
+      }
     cl.sync();
-    for (int j = w; j < c; j += nw) {
-      double s = 0.0;
-      for (int q = 0; q < kClu; ++q) s += cl.map_shared_rank(P, q)[2 + j];
-      s *= t;
-      double* e = E + (size_t)j * m;
-      for (int i = max(lo, k + 1) + lane; i < hi; i += 32) e[i] -= s * v[i];
-      if (lane == 0 && k >= lo && k < hi) e[k] -= s;
-    }
-    __syncthreads();
+    if (up)
+      for (int jc = 0; jc < c; jc += kGather) {
+        const int nj = min(kGather, c - jc);
+        if (threadIdx.x < gs * kGather) {
+          const int cc = threadIdx.x / kGather, jj = threadIdx.x % kGather;
+          if (jj < nj) gb[cc][jj] = cl.map_shared_rank(P, g0 + cc)[2 + jc + jj];
+        }
+        __syncthreads();
+        for (int j = jc + w; j < jc + nj; j += nw) {
+          double s = 0.0;
+          for (int q = 0; q < gs; ++q) s += gb[q][j - jc];
+          s *= t;
+          double* e = E + (size_t)j * m;
+          for (int i = max(lo, k + 1) + lane; i < hi; i += 32) e[i] -= s * v[i];
+          if (lane == 0 && k >= lo && k < hi) e[k] -= s;
+        }
+        __syncthreads();
+      }
+    // the next step overwrites the other parity buffer only after every rank
+    // passed this step's first barrier, so one barrier per step suffices here
   }
   cl.sync();
 }
@@ -956,6 +998,13 @@ __device__ void lr_update_cluster(cg::cluster_group& cl, CluShared& sh, const Tr
     return;
   }
   const long long t0 = clock64();
+  long long tcl = t0;
+  auto cstage = [&](int i) {
+    if (!d_hist_on || rank != 0 || threadIdx.x != 0) return;
+    const long long now = clock64();
+    atomicAdd(&d_clu_cyc[i], (unsigned long long)(now - tcl));
+    tcl = now;
+  };
   double* WU = it.ws;
   double* WV = WU + (size_t)m * it.rcap;
   double* tu = WV + (size_t)n * it.rcap;
@@ -985,14 +1034,23 @@ __device__ void lr_update_cluster(cg::cluster_group& cl, CluShared& sh, const Tr
     }
   }
   cl.sync();
-  clu_qr(cl, sh, WU, m, r, tu);
-  clu_qr(cl, sh, WV, n, r, tv);
+  cstage(0);
+  {  // U on ranks 0-3, V on ranks 4-7, at once
+    const int kit = max(min(m, r), min(n, r));
+    if (rank < kClu / 2)
+      clu_qr(cl, sh, WU, m, r, tu, 0, kClu / 2, kit);
+    else
+      clu_qr(cl, sh, WV, n, r, tv, kClu / 2, kClu / 2, kit);
+  }
+  cstage(1);
+  cstage(2);
   const int ku = min(m, r), kv = min(n, r);
   const int kqmax = min(ku, kv);
   double* tau = C + (size_t)ku * kv;
-  double* cn = tau + kv;
-  int* piv = reinterpret_cast<int*>(cn + kv);
-  double* G = cn + 2 * kv;
+  double* cn = tau + kv;                                // 2 kv (double-buffered norms)
+  int* phys = reinterpret_cast<int*>(cn + 2 * kv);      // kv ints
+  int* stepof = phys + kv;                              // kv ints
+  double* G = cn + 3 * kv;
   double* J = G + (size_t)kv * kqmax;
   double* Uc = J + (size_t)kqmax * kqmax;
   double* gsig = Uc + (size_t)ku * kqmax;  // exported sigma / order for the other CTAs
@@ -1006,13 +1064,21 @@ __device__ void lr_update_cluster(cg::cluster_group& cl, CluShared& sh, const Tr
       C[(size_t)j * ku + i] = s;
     }
     __syncthreads();
-    rs = cta_rrqr_svd(C, ku, kv, eps, tau, piv, cn, G, J, s_sig, s_ord, red);
+    // lean rank-revealing SVD (virtual pivoting, one barrier per step)
+    const bool lean = kv <= 128;  // the lean variant's pivot bitmask covers 128 columns
+    if (lean) {
+      rs = cta_rrqr_svd2(C, ku, kv, eps, tau, phys, cn, stepof, G, J, s_sig, s_ord, 1, nullptr);
+    } else {
+      rs = cta_rrqr_svd(C, ku, kv, eps, tau, phys, cn, G, J, s_sig, s_ord, red);
+      for (int j = threadIdx.x; j < kv; j += blockDim.x) phys[j] = j;  // explicit swaps: identity map
+      __syncthreads();
+    }
     for (int idx = threadIdx.x; idx < ku * rs.keep; idx += blockDim.x) {
       const int i = idx % ku, c = idx / ku, src = s_ord[c];
       Uc[idx] = i < rs.kq ? J[(size_t)src * rs.kq + i] * s_sig[src] : 0.0;
     }
     __syncthreads();
-    cta_apply_q(C, ku, rs.kq, tau, Uc, rs.keep);
+    cta_apply_q_map(C, ku, ku, rs.kq, tau, phys, Uc, rs.keep);
     for (int c = threadIdx.x; c < rs.keep; c += blockDim.x) {
       gsig[c] = s_sig[s_ord[c]];
       gord[c] = s_ord[c];
@@ -1024,6 +1090,7 @@ __device__ void lr_update_cluster(cg::cluster_group& cl, CluShared& sh, const Tr
     __syncthreads();
   }
   cl.sync();
+  cstage(3);
   const int keep = gord[kqmax];
   if (keep > it.cap) {
     if (rank == 0 && threadIdx.x == 0) atomicOr(err, 4);
@@ -1040,8 +1107,16 @@ __device__ void lr_update_cluster(cg::cluster_group& cl, CluShared& sh, const Tr
       it.V[(size_t)c * n + i] = i < kv ? G[(size_t)src * kv + i] / sg : 0.0;
   }
   cl.sync();
-  clu_apply_q(cl, sh, WU, m, ku, tu, it.U, keep);
-  clu_apply_q(cl, sh, WV, n, kv, tv, it.V, keep);
+  cstage(4);
+  {
+    const int kit = max(ku, kv);
+    if (rank < kClu / 2)
+      clu_apply_q(cl, sh, WU, m, ku, tu, it.U, keep, 0, kClu / 2, kit);
+    else
+      clu_apply_q(cl, sh, WV, n, kv, tv, it.V, keep, kClu / 2, kClu / 2, kit);
+  }
+  cstage(5);
+  cstage(6);
   if (rank == 0 && threadIdx.x == 0) {
     *it.rank = keep;
     if (it.compact) *it.compact = keep;
