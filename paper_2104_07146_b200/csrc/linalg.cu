@@ -217,9 +217,147 @@ __global__ void __launch_bounds__(512) k_trsm_left_smem(const TrsmLItem* __restr
   }
 }
 
+// Register-resident substitutions for diagonal leaves of up to 32*NB rows:
+// L staged in shared memory once per CTA (padded ld, 16-byte loads), the
+// reciprocal diagonal precomputed, and each warp solves one right-hand side
+// held in registers (lane l owns rows l, l+32, ...): one shuffle broadcast and
+// NB FMAs per column instead of a division and two warp barriers.
+template <int NB>
+__device__ __forceinline__ void stage_tri(const double* __restrict__ Lg, int ldl, int b, double* L, double* inv) {
+  constexpr int S = 32 * NB, LD = S + 1;
+#pragma unroll 4
+  for (int e = threadIdx.x; e < S * S; e += blockDim.x) {
+    const int c = e / S, r = e % S;
+    L[c * LD + r] = (c < b && r < b) ? Lg[(size_t)c * ldl + r] : 0.0;
+  }
+  for (int j = threadIdx.x; j < S; j += blockDim.x) inv[j] = j < b ? 1.0 / Lg[(size_t)j * ldl + j] : 0.0;
+}
+// x <- L^{-1} x (forward) for one warp's register vector
+template <int NB>
+__device__ __forceinline__ void warp_fwd(double (&xr)[NB], const double* L, const double* inv, int lane) {
+  constexpr int LD = 32 * NB + 1;
+#pragma unroll
+  for (int kb = 0; kb < NB; ++kb)
+    for (int jj = 0; jj < 32; ++jj) {
+      const int j = kb * 32 + jj;
+      if (lane == jj) xr[kb] *= inv[j];
+      const double xj = __shfl_sync(0xffffffffu, xr[kb], jj);
+      const double* Lc = L + (size_t)j * LD;
+      if (lane > jj) xr[kb] -= Lc[kb * 32 + lane] * xj;
+#pragma unroll
+      for (int k = kb + 1; k < NB; ++k) xr[k] -= Lc[k * 32 + lane] * xj;
+    }
+}
+// x <- L^{-T} x (backward)
+template <int NB>
+__device__ __forceinline__ void warp_bwd(double (&xr)[NB], const double* L, const double* inv, int lane) {
+  constexpr int LD = 32 * NB + 1;
+#pragma unroll
+  for (int kb = NB - 1; kb >= 0; --kb)
+    for (int jj = 31; jj >= 0; --jj) {
+      const int j = kb * 32 + jj;
+      if (lane == jj) xr[kb] *= inv[j];
+      const double xj = __shfl_sync(0xffffffffu, xr[kb], jj);
+      if (lane < jj) xr[kb] -= L[(size_t)(kb * 32 + lane) * LD + j] * xj;
+#pragma unroll
+      for (int k = 0; k < kb; ++k) xr[k] -= L[(size_t)(k * 32 + lane) * LD + j] * xj;
+    }
+}
+
+template <int NB>
+__global__ void __launch_bounds__(512) k_trsm_left_reg(const TrsmLItem* __restrict__ items) {
+  const TrsmLItem it = items[blockIdx.x];
+  const int cols = it.cols.get();
+  const int b = it.b;
+  const int nw = blockDim.x >> 5;
+  if (cols <= 0 || (int)blockIdx.y * nw >= cols) return;
+  extern __shared__ double sm[];
+  constexpr int S = 32 * NB;
+  double* L = sm;
+  double* inv = sm + (size_t)S * (S + 1);
+  stage_tri<NB>(it.L, it.ldl, b, L, inv);
+  if (blockIdx.y == 0 && threadIdx.x == 0) atomicAdd(&d_cnt_trsm, (double)b * b * cols);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int c = blockIdx.y * nw + w; c < cols; c += gridDim.y * nw) {
+    double* x = it.M + (size_t)c * it.ldm;
+    double xr[NB];
+#pragma unroll
+    for (int k = 0; k < NB; ++k) xr[k] = (k * 32 + lane < b) ? x[k * 32 + lane] : 0.0;
+    if (!it.trans)
+      warp_fwd<NB>(xr, L, inv, lane);
+    else
+      warp_bwd<NB>(xr, L, inv, lane);
+#pragma unroll
+    for (int k = 0; k < NB; ++k)
+      if (k * 32 + lane < b) x[k * 32 + lane] = xr[k];
+  }
+}
+
+// X (s x t) <- X L^{-T} (D^{-1}): every row of X is a forward substitution
+// with L; rows are staged 32 at a time through shared memory (coalesced) and
+// solved one per warp in registers.
+template <int NB>
+__global__ void __launch_bounds__(512) k_trsm_right_reg(const TrsmRItem* __restrict__ items) {
+  const TrsmRItem it = items[blockIdx.x];
+  const int t = it.t;
+  extern __shared__ double sm[];
+  constexpr int S = 32 * NB;
+  double* L = sm;
+  double* inv = sm + (size_t)S * (S + 1);
+  double* X = inv + S;  // 32 rows x S, ld 33 (row r, column c at c * 33 + r)
+  stage_tri<NB>(it.L, it.ldl, t, L, inv);
+  if (blockIdx.y == 0 && threadIdx.x == 0) atomicAdd(&d_cnt_trsm, (double)t * t * it.s);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int r0 = blockIdx.y * 32; r0 < it.s; r0 += gridDim.y * 32) {
+    const int rows = min(32, it.s - r0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < 32 * S; e += blockDim.x) {
+      const int r = e & 31, c = e >> 5;
+      X[c * 33 + r] = (r < rows && c < t) ? it.X[(size_t)c * it.ldx + r0 + r] : 0.0;
+    }
+    __syncthreads();
+    for (int r = w; r < rows; r += nw) {
+      double xr[NB];
+#pragma unroll
+      for (int k = 0; k < NB; ++k) xr[k] = X[(k * 32 + lane) * 33 + r];
+      warp_fwd<NB>(xr, L, inv, lane);
+#pragma unroll
+      for (int k = 0; k < NB; ++k) X[(k * 32 + lane) * 33 + r] = xr[k];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < 32 * S; e += blockDim.x) {
+      const int r = e & 31, c = e >> 5;
+      if (r < rows && c < t) it.X[(size_t)c * it.ldx + r0 + r] = it.d ? X[c * 33 + r] / it.d[c] : X[c * 33 + r];
+    }
+  }
+}
+
+template <class K>
+static void set_smem_once(K kern, size_t bytes, bool& done) {
+  if (!done) {
+    HMGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    done = true;
+  }
+}
+
 void launch_trsm_left(const TrsmLItem* d_items, int count, int max_cols, cudaStream_t st,
                       int max_b) {
   if (count <= 0) return;
+  if (max_b > 0 && max_b <= 128) {
+    const int gy = max(1, min((max_cols + 15) / 16, 32));
+    const int nb = (max_b + 31) / 32;
+    const size_t by = ((size_t)32 * nb * (32 * nb + 1) + 32 * nb) * 8;
+    static bool c1 = false, c2 = false, c3 = false, c4 = false;
+    switch (nb) {
+      case 1: set_smem_once(k_trsm_left_reg<1>, by, c1); k_trsm_left_reg<1><<<dim3(count, gy), 512, by, st>>>(d_items); break;
+      case 2: set_smem_once(k_trsm_left_reg<2>, by, c2); k_trsm_left_reg<2><<<dim3(count, gy), 512, by, st>>>(d_items); break;
+      case 3: set_smem_once(k_trsm_left_reg<3>, by, c3); k_trsm_left_reg<3><<<dim3(count, gy), 512, by, st>>>(d_items); break;
+      default: set_smem_once(k_trsm_left_reg<4>, by, c4); k_trsm_left_reg<4><<<dim3(count, gy), 512, by, st>>>(d_items); break;
+    }
+    HMGP_LAUNCH_CHECK();
+    return;
+  }
   const size_t bytes = (size_t)max_b * max_b * 8;
   if (max_b > 0 && bytes <= 200 * 1024) {
     static bool configured = false;
@@ -292,6 +430,20 @@ __global__ void __launch_bounds__(256) k_trsm_right_smem(const TrsmRItem* __rest
 void launch_trsm_right(const TrsmRItem* d_items, int count, int max_rows, cudaStream_t st,
                        int max_t) {
   if (count <= 0) return;
+  if (max_t > 0 && max_t <= 128) {
+    const int gy = max(1, min((max_rows + 31) / 32, 32));
+    const int nb = (max_t + 31) / 32;
+    const size_t by = ((size_t)32 * nb * (32 * nb + 1) + 32 * nb + (size_t)33 * 32 * nb) * 8;
+    static bool c1 = false, c2 = false, c3 = false, c4 = false;
+    switch (nb) {
+      case 1: set_smem_once(k_trsm_right_reg<1>, by, c1); k_trsm_right_reg<1><<<dim3(count, gy), 512, by, st>>>(d_items); break;
+      case 2: set_smem_once(k_trsm_right_reg<2>, by, c2); k_trsm_right_reg<2><<<dim3(count, gy), 512, by, st>>>(d_items); break;
+      case 3: set_smem_once(k_trsm_right_reg<3>, by, c3); k_trsm_right_reg<3><<<dim3(count, gy), 512, by, st>>>(d_items); break;
+      default: set_smem_once(k_trsm_right_reg<4>, by, c4); k_trsm_right_reg<4><<<dim3(count, gy), 512, by, st>>>(d_items); break;
+    }
+    HMGP_LAUNCH_CHECK();
+    return;
+  }
   const size_t bytes = ((size_t)max_t * max_t + (size_t)kTrsmRTile * max_t) * 8;
   if (bytes <= 200 * 1024) {
     static bool configured = false;
@@ -483,7 +635,13 @@ __global__ void k_leaf_factor(double* __restrict__ Dg, int b, int base, int ldl,
 // Cholesky (l = c/sqrt(s)).  Two barriers per column.
 // BMAX (32, 64 or 128) is a compile-time bound on b so every register slot and
 // shared-memory offset is static.
-constexpr int kLeafRegThreads = 1024;
+constexpr int kLeafRegThreads = 512;
+// Register-resident leaf LDL / Cholesky (dense_ldl_leaf / dense_cholesky_leaf,
+// hfactor.cpp:22-73): thread (i, g) holds row i of the columns g, g + G, ...;
+// column j is published to a double-buffered shared vector and every thread
+// derives the (clamped) pivot from it redundantly, so each column costs one
+// barrier.  Pivot bookkeeping (min pivot, clamps, negatives, first failure)
+// is kept by thread 0 and committed with one set of atomics at the end.
 template <int BMAX>
 __global__ void __launch_bounds__(kLeafRegThreads) k_leaf_factor_reg(double* __restrict__ Dg, int b,
                                                                      int base, int ldl,
@@ -492,22 +650,20 @@ __global__ void __launch_bounds__(kLeafRegThreads) k_leaf_factor_reg(double* __r
                                                                      LeafFactorStatus* st) {
   constexpr int G = kLeafRegThreads / BMAX;
   constexpr int kLeafRegMaxK = BMAX / G;  // columns per thread
-  __shared__ double col[BMAX];
-  __shared__ double s_piv;
+  __shared__ double col[2][BMAX];
   const int t = threadIdx.x;
   const int i = t % BMAX, g = t / BMAX;
   const bool active = i < b;
-  constexpr int nk = kLeafRegMaxK;
   double a[kLeafRegMaxK];
 #pragma unroll
   for (int q = 0; q < kLeafRegMaxK; ++q) {
     const int k = g + q * G;
-    a[q] = (active && q < nk && k < b) ? Dg[(size_t)k * b + i] : 0.0;
+    a[q] = (active && k < b) ? Dg[(size_t)k * b + i] : 0.0;
   }
-  // pivot bookkeeping stays in thread 0's registers; one set of atomics at the end
   double minp = INFINITY, failv = 0.0;
   int nclamp = 0, nneg = 0, failpos = INT_MAX;
   for (int j = 0; j < b; ++j) {
+    double* cj = col[j & 1];
     // owners of column j (group g = j % G, slot qj = j / G) publish it
     const int qj = j / G;
     const bool own = active && g == j % G;
@@ -515,42 +671,43 @@ __global__ void __launch_bounds__(kLeafRegThreads) k_leaf_factor_reg(double* __r
 #pragma unroll
     for (int q = 0; q < kLeafRegMaxK; ++q)
       if (q == qj) aj = a[q];
-    if (own) col[i] = aj;
+    if (own) cj[i] = aj;
     __syncthreads();
-    if (t == 0) {
-      double s = col[j];
-      minp = fmin(minp, s);
-      bool failed;
-      if (ldl) {
-        failed = (s == 0.0);
-        if (s < 0.0) {
-          if (-s <= clamp_tol) {
-            s = clamp_tol;
-            ++nclamp;
-          } else {
-            ++nneg;
-          }
+    double s = cj[j];
+    const double s_raw = s;
+    bool failed;
+    bool clamped = false, negative = false;
+    if (ldl) {
+      failed = (s == 0.0);
+      if (s < 0.0) {
+        if (-s <= clamp_tol) {
+          s = clamp_tol;
+          clamped = true;
+        } else {
+          negative = true;
         }
-      } else {
-        failed = !(s > 0.0);
       }
+    } else {
+      failed = !(s > 0.0);
+    }
+    if (t == 0) {
+      minp = fmin(minp, s_raw);
+      nclamp += clamped;
+      nneg += negative;
       if (failed && failpos == INT_MAX) {
         failpos = base + j;
         failv = s;
       }
-      s_piv = s;
+      if (ldl) d[base + j] = s;
     }
-    __syncthreads();
-    if (ldl && t == 32) d[base + j] = s_piv;
-    const double s = s_piv;
     // trailing update of the columns k > j this thread owns (rows i > j only are
     // ever read again, so the strict upper part may hold stale values)
     if (active && i > j) {
-      const double ci = col[i] / s;
+      const double ci = cj[i] / s;
       const int qmin = j >= g ? (j - g) / G + 1 : 0;  // first q with g + q*G > j
 #pragma unroll
       for (int q = 0; q < kLeafRegMaxK; ++q)
-        if (q >= qmin) a[q] -= ci * col[g + q * G];
+        if (q >= qmin) a[q] -= ci * cj[g + q * G];
     }
     // finalize column j in its owners' registers
     if (own) {
@@ -560,12 +717,11 @@ __global__ void __launch_bounds__(kLeafRegThreads) k_leaf_factor_reg(double* __r
       for (int q = 0; q < kLeafRegMaxK; ++q)
         if (q == qj) a[q] = v;
     }
-    __syncthreads();
   }
 #pragma unroll
   for (int q = 0; q < kLeafRegMaxK; ++q) {
     const int k = g + q * G;
-    if (active && q < nk && k < b) Dg[(size_t)k * b + i] = (i < k) ? 0.0 : a[q];
+    if (active && k < b) Dg[(size_t)k * b + i] = (i < k) ? 0.0 : a[q];
   }
   if (t == 0) {
     atomicAdd(&d_cnt_leaf, (double)b * b * b / 3.0);

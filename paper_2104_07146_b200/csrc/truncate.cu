@@ -507,7 +507,50 @@ __device__ void lr_update(const TruncItem& it, double eps, int* err, int smem_w,
 
 // Fused trsm_lower_t post-op (hfactor.cpp:198-202): V <- L^{-1} V, V /= d.
 // One warp per column, lanes over rows; L read through L1/L2.
+// n <= 32*NB: the column is held in registers (lane l owns rows l, l+32, ...),
+// one shuffle broadcast per step, reciprocal diagonal precomputed, L columns
+// read through L1 (every warp walks the same L).
+template <int NB>
+__device__ void lr_post_solve_reg(const TruncItem& it, double* s_inv) {
+  const int cols = *it.rank, n = it.n, ld = it.post_ldl_ld;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const double* L = it.post_L;
+  for (int j = threadIdx.x; j < 32 * NB; j += blockDim.x) s_inv[j] = j < n ? 1.0 / L[(size_t)j * ld + j] : 0.0;
+  __syncthreads();
+  for (int c = w; c < cols; c += nw) {
+    double* x = it.V + (size_t)c * n;
+    double xr[NB];
+#pragma unroll
+    for (int k = 0; k < NB; ++k) xr[k] = (k * 32 + lane < n) ? x[k * 32 + lane] : 0.0;
+#pragma unroll
+    for (int kb = 0; kb < NB; ++kb)
+#pragma unroll 4
+      for (int jj = 0; jj < 32; ++jj) {
+        const int j = kb * 32 + jj;
+        if (j >= n) break;
+        const double* lc = L + (size_t)j * ld;
+        double lv[NB];
+#pragma unroll
+        for (int k = kb; k < NB; ++k) lv[k] = (k * 32 + lane < n) ? lc[k * 32 + lane] : 0.0;
+        if (lane == jj) xr[kb] *= s_inv[j];
+        const double xj = __shfl_sync(0xffffffffu, xr[kb], jj);
+        if (lane > jj) xr[kb] -= lv[kb] * xj;
+#pragma unroll
+        for (int k = kb + 1; k < NB; ++k) xr[k] -= lv[k] * xj;
+      }
+#pragma unroll
+    for (int k = 0; k < NB; ++k)
+      if (k * 32 + lane < n) x[k * 32 + lane] = it.post_d ? xr[k] / it.post_d[k * 32 + lane] : xr[k];
+  }
+  __syncthreads();
+}
+
 __device__ void lr_post_solve(const TruncItem& it) {
+  __shared__ double s_inv[128];
+  if (it.n <= 32) return lr_post_solve_reg<1>(it, s_inv);
+  if (it.n <= 64) return lr_post_solve_reg<2>(it, s_inv);
+  if (it.n <= 96) return lr_post_solve_reg<3>(it, s_inv);
+  if (it.n <= 128) return lr_post_solve_reg<4>(it, s_inv);
   const int cols = *it.rank, n = it.n, ld = it.post_ldl_ld;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const double* L = it.post_L;
