@@ -415,9 +415,28 @@ struct Engine {
   void gemm(std::vector<GemmItem>& v) {
     if (v.empty()) return;
     int tiles = 1;
-    for (auto& g : v) tiles = std::max(tiles, ((g.M.v + 63) / 64) * ((g.N.v + 63) / 64));
+    for (auto& g : v) {
+      const int t = ((g.M.v + 63) / 64) * ((g.N.v + 63) / 64);
+      // accumulate-mode items with a long K get split-K CTAs (linalg.cu)
+      const int ks = g.atomic != 2 ? std::min(32, std::max(1, (g.K.v + 511) / 512)) : 1;
+      tiles = std::max(tiles, std::min(128, t * ks));
+    }
     acc_all(v);
-    run("gemm", [&](cudaStream_t s) { launch_gemm(sg.put(v), (int)v.size(), tiles, s); });
+    const char* lab = "gemm";
+    if (dag && dag->serial) {  // (diagnostics) size class of the launch
+      static std::set<std::string> pool;
+      int mm = 0, nn = 0, kk = 0;
+      for (auto& g : v) {
+        mm = std::max(mm, g.M.v);
+        nn = std::max(nn, g.N.v);
+        kk = std::max(kk, g.K.v);
+      }
+      auto p2 = [](int x) { int p = 1; while (p < x) p <<= 1; return p; };
+      char buf[96];
+      snprintf(buf, sizeof buf, "gemm:%s M<=%d N<=%d K<=%d n<=%d", site, p2(mm), p2(nn), p2(kk), p2((int)v.size()));
+      lab = pool.insert(buf).first->c_str();
+    }
+    run(lab, [&](cudaStream_t s) { launch_gemm(sg.put(v), (int)v.size(), tiles, s); });
     stat(S_GEMM, v.size());
     v.clear();
   }
@@ -888,6 +907,7 @@ struct Engine {
   // low-rank stages.  Leaves of one block may share y rows -> FP64 atomics.
   void apply(const std::vector<Ap>& its0) {
     if (its0.empty()) return;
+    site = "apply";
     std::vector<Ap> its;
     std::vector<int> shared;
     for (const Ap& a : its0) {
@@ -931,9 +951,14 @@ struct Engine {
         const LeafDev& l = LF(a.b);
         T.push_back(temp(l.cap, a.x.cols));
       }
+      std::vector<CopyScaleItem> zf;
       for (size_t i = 0; i < lr.size(); ++i) {  // T = (trans ? U : V)^T x   (rank x c)
         const Ap& a = lr[i];
         const LeafDev& l = LF(a.b);
+        const int kk = a.trans ? l.m : l.n;
+        // long contractions are split over CTAs (accumulate into a zeroed T)
+        const bool split = kk >= 2048;
+        if (split) zf.push_back(cpy(nullptr, 0, T[i], a.x.cols, 0, 0.0, nullptr, 0));
         GemmItem gi{};
         gi.A = a.trans ? l.a : l.b;
         gi.lda = a.trans ? l.m : l.n;
@@ -946,9 +971,11 @@ struct Engine {
         gi.N = a.x.cols;
         gi.K = dimv(a.trans ? l.m : l.n);
         gi.alpha = 1.0;
-        gi.atomic = 2;  // T is this item's own: overwrite (no zero fill)
+        gi.atomic = split ? 1 : 2;  // T is this item's own: overwrite (no zero fill) unless split
         g.push_back(gi);
       }
+      for (CopyScaleItem& z : zf) z.mode = 0;
+      copy(zf);
       gemm(g);
       for (size_t i = 0; i < lr.size(); ++i) {  // y += alpha (trans ? V : U) T
         const Ap& a = lr[i];
@@ -1324,6 +1351,7 @@ struct Engine {
   // distinct leaf targets, one add each
   void add_leaves(const std::vector<Add>& its) {
     if (its.empty()) return;
+    site = "add-leaves";
     std::vector<GemmItem> g;
     std::vector<TruncItem> t;
     std::vector<Add> br;

@@ -68,14 +68,30 @@ __device__ void gemm_item(const GemmItem& it, int tile0, int tstride, bool count
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int wr = (w >> 2) * 32, wc = (w & 3) * 16;  // warp sub-tile origin
   const int fr = lane >> 2, fk = lane & 3;           // fragment row / k index
-  for (int tile = tile0; tile < tm * tn; tile += tstride) {
+  // split-K when the item has fewer output tiles than CTAs (long, thin
+  // products such as V^T x over a big block): the partial products are added
+  // with FP64 atomics, so it needs an accumulate mode (C pre-zeroed by the
+  // caller for temporaries)
+  const int T = tm * tn;
+  int nsplit = 1, tbeg = tile0, tstep = tstride, kbeg = 0, kend = K;
+  if (it.atomic != 2 && tstride > T) nsplit = min(tstride / T, max(1, (K + 255) / 256));
+  if (nsplit > 1) {
+    if (tile0 >= T * nsplit) return;
+    const int kc = ((K + nsplit - 1) / nsplit + GK - 1) / GK * GK;
+    tbeg = tile0 % T;
+    tstep = T;
+    kbeg = (tile0 / T) * kc;
+    kend = min(K, kbeg + kc);
+    if (kbeg >= kend) return;
+  }
+  for (int tile = tbeg; tile < T; tile += tstep) {
     const int i0 = (tile % tm) * GT, j0 = (tile / tm) * GT;
     double acc[4][2][2];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-    for (int k0 = 0; k0 < K; k0 += GK) {
+    for (int k0 = kbeg; k0 < kend; k0 += GK) {
       __syncthreads();
       for (int e = threadIdx.x; e < GK * GT; e += 256) {
         int kk, ii;
@@ -89,7 +105,7 @@ __device__ void gemm_item(const GemmItem& it, int tile0, int tstride, bool count
         }
         const int gi = i0 + ii, gk = k0 + kk;
         double v = 0.0;
-        if (gi < M && gk < K)
+        if (gi < M && gk < kend)
           v = it.ta ? it.A[(size_t)gi * it.lda + gk] : it.A[(size_t)gk * it.lda + gi];
         sA[kk][ii] = v;
         // B tile: op(B)[k0+kk, j0+jj]
@@ -103,7 +119,7 @@ __device__ void gemm_item(const GemmItem& it, int tile0, int tstride, bool count
         }
         const int gj = j0 + jj, gk2 = k0 + kk;
         double wv = 0.0;
-        if (gj < N && gk2 < K)
+        if (gj < N && gk2 < kend)
           wv = it.tb ? it.B[(size_t)gk2 * it.ldb + gj] : it.B[(size_t)gj * it.ldb + gk2];
         sB[kk][jj] = wv;
       }
@@ -132,7 +148,7 @@ __device__ void gemm_item(const GemmItem& it, int tile0, int tstride, bool count
           const int gi = i0 + wr + rb * 8 + fr;
           if (gi >= M) continue;
           const double v = acc[rb][cb][h];
-          if (it.atomic == 1)
+          if (it.atomic == 1 || nsplit > 1)
             atomicAdd(&it.C[(size_t)gj * it.ldc + gi], it.alpha * v);
           else if (it.atomic == 2)
             it.C[(size_t)gj * it.ldc + gi] = it.alpha * v;
@@ -145,7 +161,7 @@ __device__ void gemm_item(const GemmItem& it, int tile0, int tstride, bool count
 
 void launch_gemm(const GemmItem* d_items, int count, int max_tiles, cudaStream_t st) {
   if (count <= 0) return;
-  const int ty = max(1, min(max_tiles, 64));
+  const int ty = max(1, min(max_tiles, 128));
   k_gemm<<<dim3(count, ty), 256, 0, st>>>(d_items);
   HMGP_LAUNCH_CHECK();
 }
