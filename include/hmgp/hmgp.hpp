@@ -385,4 +385,28 @@ inline PredictionResult predict(std::span<const Location> train, const Vector& z
   return res;
 }
 
+// simgen.hpp data utilities over the C ABI
+inline std::vector<Location> random_locations(int n, std::uint64_t seed) {  // simgen.cpp:114-123
+  if (n < 1) throw std::invalid_argument("random_locations: n must be >= 1");
+  std::vector<double> xy(2 * static_cast<size_t>(n));
+  detail::check(hmgp_random_locations(n, 2, seed, xy.data()));
+  std::vector<Location> out(n);
+  for (int i = 0; i < n; ++i) out[i] = Location{xy[2 * i], xy[2 * i + 1]};
+  return out;
+}
+
+// simgen.cpp:125-141 on the GPU (dense FP64 Cholesky; n <= 65536 instead of
+// the reference's 16384).  std::runtime_error if the covariance is not SPD.
+inline Vector sample_grf(std::span<const Location> locations, const MaternParams& params,
+                         std::uint64_t seed) {
+  params.validate();
+  if (locations.empty()) throw std::invalid_argument("sample_grf: empty dataset");
+  const auto xy = detail::flat(locations);
+  const hmgp_matern m = params.c();
+  Vector z(locations.size());
+  detail::check(hmgp_sample_grf(detail::context(), xy.data(), static_cast<int>(locations.size()), 2, &m,
+                                seed, z.data()));
+  return z;
+}
+
 }  // namespace hmgp

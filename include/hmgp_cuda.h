@@ -30,7 +30,8 @@ enum {
   HMGP_ERANGE = 3,    /* std::out_of_range (cov_block indices) */
   HMGP_ENOTSPD = 4,   /* hmgp::FactorError (pivot_index / pivot_value set) */
   HMGP_ECUDA = 5,     /* CUDA runtime failure */
-  HMGP_ECAPACITY = 6  /* a device workspace bound was exceeded */
+  HMGP_ECAPACITY = 6, /* a device workspace bound was exceeded */
+  HMGP_ERUNTIME = 7   /* std::runtime_error (sample_grf: covariance not SPD) */
 };
 
 typedef struct hmgp_ctx hmgp_ctx;
@@ -192,6 +193,11 @@ int hmgp_random_locations(int n, int dim, uint64_t seed, double* out);
 int hmgp_jittered_grid(int g, uint64_t seed, double* out);
 /* iid standard normals via AS241 (simgen.cpp:9-112) */
 int hmgp_normals(int n, uint64_t seed, double* out);
+/* sample_grf(locations, params, seed) (simgen.cpp:125-141): z = chol(cov_dense) w,
+   w = AS241 normals of `seed`; dense on device, n <= 65536 (the reference caps at
+   16384); HMGP_ERUNTIME when the covariance is not SPD.  Host buffers. */
+int hmgp_sample_grf(hmgp_ctx* ctx, const double* coords, int n, int dim, const hmgp_matern* theta,
+                    uint64_t seed, double* out);
 
 #ifdef __cplusplus
 }

@@ -46,7 +46,7 @@ _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int32)
 _vp = C.c_void_p
 
-HMGP_OK, HMGP_EINVAL, HMGP_EDOMAIN, HMGP_ERANGE, HMGP_ENOTSPD, HMGP_ECUDA, HMGP_ECAPACITY = range(7)
+HMGP_OK, HMGP_EINVAL, HMGP_EDOMAIN, HMGP_ERANGE, HMGP_ENOTSPD, HMGP_ECUDA, HMGP_ECAPACITY, HMGP_ERUNTIME = range(8)
 
 
 class DomainError(ValueError):
@@ -152,6 +152,7 @@ _sig("hmgp_cross_apply_device", C.c_int, [_vp, C.c_void_p, C.c_int, C.c_int, C.c
 _sig("hmgp_random_locations", C.c_int, [C.c_int, C.c_int, C.c_uint64, _dp])
 _sig("hmgp_jittered_grid", C.c_int, [C.c_int, C.c_uint64, _dp])
 _sig("hmgp_normals", C.c_int, [C.c_int, C.c_uint64, _dp])
+_sig("hmgp_sample_grf", C.c_int, [_vp, _dp, C.c_int, C.c_int, C.POINTER(Matern), C.c_uint64, _dp])
 
 
 def _chk(rc):
@@ -168,6 +169,8 @@ def _chk(rc):
         raise FactorError(msg, _lib.hmgp_last_pivot_index(), _lib.hmgp_last_pivot_value())
     if rc == HMGP_ECAPACITY:
         raise CapacityError(msg)
+    if rc == HMGP_ERUNTIME:
+        raise RuntimeError(msg)
     raise CudaError(msg)
 
 
@@ -224,6 +227,11 @@ class MaternParams:
     ell: float = 0.1
     nu: float = 0.5
     tau2: float = 0.0
+
+    def valid(self):  # covkernel.cpp:9-13
+        v = (self.sigma2, self.ell, self.nu, self.tau2)
+        return (all(np.isfinite(v)) and self.sigma2 > 0.0 and self.ell > 0.0 and self.nu > 0.0
+                and self.tau2 >= 0.0)
 
     def c(self):
         return Matern(self.sigma2, self.ell, self.nu, self.tau2)
@@ -571,6 +579,17 @@ def jittered_grid(g, seed):
 def normals(n, seed):
     out = np.empty(n)
     _chk(_lib.hmgp_normals(n, seed, _d(out)))
+    return out
+
+
+def sample_grf(locations, params, seed, ctx=None):
+    """sample_grf (simgen.cpp:125-141): exact Gaussian-field sample z = chol(C) w on
+    the GPU (dense FP64 covariance + POTRF), w = AS241 normals of `seed`; n <= 65536."""
+    ctx = ctx or default_context()
+    x = _pts(locations)
+    out = np.empty(x.shape[0])
+    m = _mp(params)
+    _chk(_lib.hmgp_sample_grf(ctx.h, _d(x), x.shape[0], x.shape[1], C.byref(m), seed, _d(out)))
     return out
 
 

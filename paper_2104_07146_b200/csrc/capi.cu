@@ -50,6 +50,8 @@ void hmgp_set_pivot(int idx, double v) {
     return fail(HMGP_ERANGE, e.what());                     \
   } catch (const std::bad_alloc& e) {                       \
     return fail(HMGP_ECUDA, "host allocation failed");      \
+  } catch (const std::runtime_error& e) {                   \
+    return fail(HMGP_ERUNTIME, e.what());                   \
   } catch (const std::exception& e) {                       \
     return fail(HMGP_ECUDA, e.what());                      \
   }
@@ -365,6 +367,23 @@ int hmgp_normals(int n, uint64_t seed, double* out) {
   API_GUARD({
     std::mt19937_64 g(seed);
     for (int i = 0; i < n; ++i) out[i] = normal_quantile_host(u01(g));
+  })
+}
+
+/* sample_grf(locations, params, seed) (simgen.cpp:125-141), dense, on device */
+int hmgp_sample_grf(hmgp_ctx* ctx, const double* coords, int n, int dim, const hmgp_matern* theta,
+                    uint64_t seed, double* out) {
+  API_GUARD({
+    hmgp_validate_matern(theta);
+    if (dim != 2 && dim != 3) throw std::invalid_argument("dim must be 2 or 3");
+    if (n < 1) throw std::invalid_argument("sample_grf: empty dataset");
+    if (n > 65536) throw std::invalid_argument("sample_grf: dense sampling capped at n = 65536");
+    std::vector<double> w(n);
+    std::mt19937_64 g(seed);
+    for (int i = 0; i < n; ++i) w[i] = normal_quantile_host(u01(g));
+    HMGP_CUDA(cudaSetDevice(ctx->device));
+    sample_grf_dense(ctx->stream, coords, n, dim,
+                     make_matern(theta->sigma2, theta->ell, theta->nu, theta->tau2), w.data(), out);
   })
 }
 

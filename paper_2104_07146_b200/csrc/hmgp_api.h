@@ -54,6 +54,9 @@ bool device_all_finite(const double* d_x, size_t count, cudaStream_t st);
 void kernel_pairs(cudaStream_t st, const double* coords, int n, int dim, const MaternDev& p,
                   const int32_t* ii, const int32_t* jj, int64_t count, double* out);
 void at_distance(cudaStream_t st, const MaternDev& p, const double* h, int64_t count, double* out);
+// sample_grf (simgen.cpp:125-141): z = chol(cov_dense) w, host buffers
+void sample_grf_dense(cudaStream_t st, const double* coords, int n, int dim, const MaternDev& p,
+                      const double* w, double* out);
 void bessel_batch(cudaStream_t st, const double* nu, const double* x, int64_t count, int generic,
                   double* out);
 void hmat_matvec(cudaStream_t st, const HMat& h, const double* x, double* y);

@@ -1,5 +1,8 @@
 // Entry-level kernels (parity hooks), H-matvec, K12 kriging cross-covariance,
 // and host-side input utilities.
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+
 #include <cmath>
 #include <stdexcept>
 #include <vector>
@@ -246,6 +249,81 @@ double normal_quantile_host(double p) {
     x = horner(e, r) / horner(f, r);
   }
   return q < 0.0 ? -x : x;
+}
+
+}  // namespace hmgp_gpu
+
+// ------------------------------------------------- exact GRF sample (dense) --
+// sample_grf (simgen.cpp:125-141) on device, beyond the reference's n <= 16384
+// guard: dense covariance (cov_dense, covkernel.cpp:262-275:
+// diagonal sigma2 + tau2, off-diagonal at_distance), lower Cholesky, z = L w with
+// w the AS241 normals of `seed` drawn on the host exactly as the reference does.
+// A data-generation utility, not the measured path: the factorization is the
+// library dense POTRF (cuSOLVER 64-bit API), the triangular product cuBLAS TRMV.
+namespace hmgp_gpu {
+
+__global__ void k_cov_dense_lower(const double* __restrict__ x, int n, int dim, MaternDev p,
+                                  double* __restrict__ C, int j0) {
+  // column-major n x n, lower triangle (j <= i); one thread per (i, j), i fastest
+  const int j = j0 + blockIdx.y;
+  for (int i = j + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double v;
+    if (i == j) {
+      v = p.sigma2 + p.tau2;
+    } else {
+      const double* pa = x + (size_t)i * dim;
+      const double* pb = x + (size_t)j * dim;
+      const double h = dim == 2 ? dist2d(pa[0], pa[1], pb[0], pb[1])
+                                : dist3d(pa[0], pa[1], pa[2], pb[0], pb[1], pb[2]);
+      v = matern_at(p, h);
+    }
+    C[(size_t)j * n + i] = v;
+  }
+}
+
+void sample_grf_dense(cudaStream_t st, const double* coords, int n, int dim, const MaternDev& p,
+                      const double* w, double* out) {
+  DBuf<double> dx((size_t)n * dim), dC((size_t)n * n), dw(n);
+  HMGP_CUDA(cudaMemcpyAsync(dx.p, coords, 8ull * n * dim, cudaMemcpyHostToDevice, st));
+  HMGP_CUDA(cudaMemcpyAsync(dw.p, w, 8ull * n, cudaMemcpyHostToDevice, st));
+  for (int j0 = 0; j0 < n; j0 += 65535) {  // grid.y limit
+    const int nj = std::min(65535, n - j0);
+    const int gx = std::min((n - j0 + 255) / 256, 64);
+    dim3 grid(gx, nj);  // block (x, y) handles column j0 + y
+    k_cov_dense_lower<<<grid, 256, 0, st>>>(dx.p, n, dim, p, dC.p, j0);
+    HMGP_LAUNCH_CHECK();
+  }
+  cusolverDnHandle_t sh = nullptr;
+  cusolverDnParams_t prm = nullptr;
+  if (cusolverDnCreate(&sh) != CUSOLVER_STATUS_SUCCESS) throw Error(HMGP_ECUDA, "cusolverDnCreate failed");
+  cusolverDnSetStream(sh, st);
+  cusolverDnCreateParams(&prm);
+  size_t dbytes = 0, hbytes = 0;
+  cusolverStatus_t cs = cusolverDnXpotrf_bufferSize(sh, prm, CUBLAS_FILL_MODE_LOWER, n, CUDA_R_64F, dC.p, n,
+                                                    CUDA_R_64F, &dbytes, &hbytes);
+  int info = 0;
+  if (cs == CUSOLVER_STATUS_SUCCESS) {
+    DBuf<char> dwork(dbytes);
+    std::vector<char> hwork(std::max<size_t>(hbytes, 1));
+    DBuf<int> dinfo(1);
+    cs = cusolverDnXpotrf(sh, prm, CUBLAS_FILL_MODE_LOWER, n, CUDA_R_64F, dC.p, n, CUDA_R_64F, dwork.p,
+                          dbytes, hwork.data(), hbytes, dinfo.p);
+    HMGP_CUDA(cudaMemcpyAsync(&info, dinfo.p, 4, cudaMemcpyDeviceToHost, st));
+    HMGP_CUDA(cudaStreamSynchronize(st));
+  }
+  cusolverDnDestroyParams(prm);
+  cusolverDnDestroy(sh);
+  if (cs != CUSOLVER_STATUS_SUCCESS) throw Error(HMGP_ECUDA, "cusolverDnXpotrf failed");
+  if (info != 0) throw std::runtime_error("sample_grf: covariance not SPD; increase nugget tau2");
+  cublasHandle_t bh = nullptr;
+  if (cublasCreate(&bh) != CUBLAS_STATUS_SUCCESS) throw Error(HMGP_ECUDA, "cublasCreate failed");
+  cublasSetStream(bh, st);
+  const cublasStatus_t bs =
+      cublasDtrmv_64(bh, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, n, dC.p, n, dw.p, 1);
+  HMGP_CUDA(cudaMemcpyAsync(out, dw.p, 8ull * n, cudaMemcpyDeviceToHost, st));
+  HMGP_CUDA(cudaStreamSynchronize(st));
+  cublasDestroy(bh);
+  if (bs != CUBLAS_STATUS_SUCCESS) throw Error(HMGP_ECUDA, "cublasDtrmv failed");
 }
 
 }  // namespace hmgp_gpu

@@ -32,15 +32,7 @@ static int g_fail = 0;
     CHECK(ok_);                  \
   } while (0)
 
-static std::vector<Location> random_locations(int n, uint64_t seed) {
-  std::mt19937_64 g(seed);
-  std::vector<Location> p(n);
-  for (auto& l : p) {
-    l.x = ((g() >> 11) + 0.5) * 0x1.0p-53;
-    l.y = ((g() >> 11) + 0.5) * 0x1.0p-53;
-  }
-  return p;
-}
+// random_locations (simgen.cpp:114-123) comes from hmgp/hmgp.hpp
 
 int main() {
   {  // single point tree (test_geometry.cpp:20-27)
