@@ -293,10 +293,14 @@ def extras(hm, _lib, ctx, stream):
                           "dense_entries": w[0], "aca_entries": w[1], "max_rank": h.stats()["max_rank"]}
         del h
     out["C2_assembly"] = c2
-    # C4-shaped kriging: n = 65536 training (jittered), m = 10000 uniform test points,
-    # θ = (1, 0.1, 0.5, 0.01); Z iid normals (exact-sample Z needs a 34 GB dense
-    # Cholesky — a data utility outside the timed path, not built yet)
-    z = hm.normals(65536, Z_SEED)
+    # C4: n = 65536 training (jittered), Z ~ N(0, C(θ₀)) exact sample, θ₀ = (1, 0.1,
+    # 0.5, 0.01) (BASELINE configs[3]) via the device dense sampler (34 GB FP64
+    # covariance + POTRF; a data utility, outside every timed region); kriging at
+    # m = 10000 uniform test points
+    t0 = time.time()
+    z = hm.sample_grf(x, [1.0, 0.1, 0.5, 0.01], Z_SEED, ctx=ctx)
+    out["C4_data"] = {"z": "sample_grf(theta0=(1,0.1,0.5,0.01), seed 1^0x517cc1b727220a95)",
+                      "sample_grf_s": time.time() - t0}
     te = hm.random_locations(10000, SEED + 1)
     cfg = hm.HConfig(leaf_size=64, rank=hm.RankControl.fixed_accuracy(1e-7))
     hm.predict(x, z, te[:100], [1.0, 0.1, 0.5, 0.01], cfg, ctx=ctx)  # warm-up

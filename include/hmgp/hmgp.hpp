@@ -22,6 +22,19 @@ namespace hmgp {
 
 using Vector = std::vector<double>;
 
+// Dense column-major matrix for the n <= 4096 diagnostics (stands in for
+// Eigen::MatrixXd in to_dense / lower_dense / reconstruct).
+struct Matrix {
+  int n_rows = 0, n_cols = 0;
+  std::vector<double> data;
+  Matrix() = default;
+  Matrix(int r, int c) : n_rows(r), n_cols(c), data(static_cast<size_t>(r) * c) {}
+  int rows() const { return n_rows; }
+  int cols() const { return n_cols; }
+  double operator()(int i, int j) const { return data[static_cast<size_t>(j) * n_rows + i]; }
+  double& operator()(int i, int j) { return data[static_cast<size_t>(j) * n_rows + i]; }
+};
+
 struct Location {  // geometry.hpp:11-14
   double x = 0.0;
   double y = 0.0;
@@ -252,6 +265,13 @@ class HMatrix {  // hmatrix.hpp:44-83
     detail::check(hmgp_hmat_stats(h_.get(), &b, &r, &md));
     return r;
   }
+  // hmatrix.cpp:274-297 (original index order; refused beyond n = 4096)
+  Matrix to_dense() const {
+    if (n_ > 4096) throw std::invalid_argument("to_dense: refused beyond n = 4096");
+    Matrix out(n_, n_);
+    detail::check(hmgp_hmat_to_dense(detail::context(), h_.get(), out.data.data()));
+    return out;
+  }
   hmgp_hmat* handle() const { return h_.get(); }
 
  private:
@@ -307,6 +327,19 @@ class HFactor {  // hfactor.hpp:34-68
     return d;
   }
   std::size_t storage_bytes() const { return bytes_; }
+  // hfactor.cpp:421-434 (tree order) and 436-449 (L D L^T or L L^T, original order)
+  Matrix lower_dense() const {
+    if (n_ > 4096) throw std::invalid_argument("lower_dense: refused beyond n = 4096");
+    Matrix out(n_, n_);
+    detail::check(hmgp_factor_lower_dense(detail::context(), f_.get(), out.data.data()));
+    return out;
+  }
+  Matrix reconstruct() const {
+    if (n_ > 4096) throw std::invalid_argument("lower_dense: refused beyond n = 4096");
+    Matrix out(n_, n_);
+    detail::check(hmgp_factor_reconstruct(detail::context(), f_.get(), out.data.data()));
+    return out;
+  }
 
  private:
   using SolveFn = int (*)(hmgp_ctx*, const hmgp_factor*, const double*, double*);

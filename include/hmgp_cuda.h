@@ -149,6 +149,13 @@ int hmgp_quad_form(hmgp_ctx* ctx, const hmgp_factor* f, const double* b, double*
 int hmgp_solve_factored(hmgp_ctx* ctx, const hmgp_factor* f, const double* b, double* x);
 int hmgp_solve_lower(hmgp_ctx* ctx, const hmgp_factor* f, const double* b, double* x);
 int hmgp_factor_diagonal(hmgp_ctx* ctx, const hmgp_factor* f, double* out);
+/* Dense diagnostics, n <= 4096 (HMGP_EINVAL beyond), out n x n column-major:
+   HMatrix::to_dense (hmatrix.cpp:274-297, original order),
+   HFactor::lower_dense (hfactor.cpp:421-434, tree order),
+   HFactor::reconstruct (hfactor.cpp:436-449, L D L^T / L L^T, original order) */
+int hmgp_hmat_to_dense(hmgp_ctx* ctx, const hmgp_hmat* h, double* out);
+int hmgp_factor_lower_dense(hmgp_ctx* ctx, const hmgp_factor* f, double* out);
+int hmgp_factor_reconstruct(hmgp_ctx* ctx, const hmgp_factor* f, double* out);
 void hmgp_factor_destroy(hmgp_factor* f);
 
 /* ------------------------------------------------------------ pipeline --- */

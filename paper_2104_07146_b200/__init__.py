@@ -139,6 +139,9 @@ _sig("hmgp_solve_factored", C.c_int, [_vp, _vp, _dp, _dp])
 _sig("hmgp_solve_lower", C.c_int, [_vp, _vp, _dp, _dp])
 _sig("hmgp_factor_diagonal", C.c_int, [_vp, _vp, _dp])
 _sig("hmgp_factor_destroy", None, [_vp])
+_sig("hmgp_hmat_to_dense", C.c_int, [_vp, _vp, _dp])
+_sig("hmgp_factor_lower_dense", C.c_int, [_vp, _vp, _dp])
+_sig("hmgp_factor_reconstruct", C.c_int, [_vp, _vp, _dp])
 _sig("hmgp_loglik", C.c_int, [_vp, _dp, C.c_int, C.c_int, _dp, C.POINTER(Matern), C.POINTER(_Config),
                               C.POINTER(_LogLik)])
 _sig("hmgp_loglik_geom", C.c_int, [_vp, _vp, C.c_void_p, C.POINTER(Matern), C.POINTER(_Config),
@@ -434,6 +437,13 @@ class HMatrix:
         _chk(_lib.hmgp_hmat_matvec(self.ctx.h, self.h, _d(x), _d(y)))
         return y
 
+    def to_dense(self):
+        """hmatrix.cpp:274-297: entry-wise reconstruction, original order (n <= 4096)."""
+        n = self.g.n
+        out = np.empty((n, n), order="F")
+        _chk(_lib.hmgp_hmat_to_dense(self.ctx.h, self.h, out.ctypes.data_as(_dp)))
+        return out
+
 
 def assemble(geom, params, rc=None):
     """hmatrix.hpp:88-89"""
@@ -492,6 +502,20 @@ class HFactor:
         x = np.empty(self.hm.g.n)
         _chk(_lib.hmgp_factor_diagonal(self.ctx.h, self.h, _d(x)))
         return x
+
+    def lower_dense(self):
+        """hfactor.cpp:421-434: dense L in tree order (n <= 4096)."""
+        n = self.hm.g.n
+        out = np.empty((n, n), order="F")
+        _chk(_lib.hmgp_factor_lower_dense(self.ctx.h, self.h, out.ctypes.data_as(_dp)))
+        return out
+
+    def reconstruct(self):
+        """hfactor.cpp:436-449: L D L^T (or L L^T) in original order (n <= 4096)."""
+        n = self.hm.g.n
+        out = np.empty((n, n), order="F")
+        _chk(_lib.hmgp_factor_reconstruct(self.ctx.h, self.h, out.ctypes.data_as(_dp)))
+        return out
 
 
 def factorize(hm, eps_f, form="ldl"):

@@ -64,7 +64,16 @@ struct Arena {
       if (base) cudaFree(base);
       base = nullptr;
       cap = bytes;
-      HMGP_CUDA(cudaMalloc(&base, cap));
+      if (cudaMalloc(&base, cap) != cudaSuccess) {
+        // less free memory than planned (e.g. after a pool regrowth): take what
+        // is there minus 1 GiB; device-detected overflow still reports cleanly
+        cudaGetLastError();
+        base = nullptr;
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        cap = fr > ((size_t)2 << 30) ? fr - ((size_t)1 << 30) : fr / 2;
+        HMGP_CUDA(cudaMalloc(&base, cap));
+      }
     }
     sub_cap = (cap / K) & ~size_t(255);
     for (int i = 0; i < K; ++i) tops[i] = i * sub_cap;
@@ -2380,7 +2389,14 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
     if (total != pool_doubles) {
       cudaFree(F.pool);
       F.pool = nullptr;
-      HMGP_CUDA(cudaMalloc(&F.pool, std::max<size_t>(1, total) * 8));
+      if (cudaMalloc(&F.pool, std::max<size_t>(1, total) * 8) != cudaSuccess) {
+        // a regrown pool (doubled capacities) may not fit next to the persistent
+        // temporary arena: drop the arena (re-sized to what is left below) first
+        cudaGetLastError();
+        F.pool = nullptr;
+        release_thread_workspace();
+        HMGP_CUDA(cudaMalloc(&F.pool, std::max<size_t>(1, total) * 8));
+      }
       pool_doubles = total;
     }
     std::vector<CloneItem> ci;

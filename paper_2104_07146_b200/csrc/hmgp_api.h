@@ -60,6 +60,10 @@ void sample_grf_dense(cudaStream_t st, const double* coords, int n, int dim, con
 void bessel_batch(cudaStream_t st, const double* nu, const double* x, int64_t count, int generic,
                   double* out);
 void hmat_matvec(cudaStream_t st, const HMat& h, const double* x, double* y);
+// dense diagnostics, n <= 4096 (hmatrix.cpp:274-297, hfactor.cpp:421-449), host out
+void hmat_to_dense(cudaStream_t st, const HMat& h, double* out);              // original order
+void factor_lower_dense(cudaStream_t st, const Factor& F, double* out);       // tree order
+void factor_reconstruct(cudaStream_t st, const Factor& F, double* out);       // original order
 // K12: d_out[i] = sum_j at_distance(|test_i - train_j|) d_w[j] (all device, AoS coords)
 void cross_apply(cudaStream_t st, const double* d_train, int n, int dim, const double* d_w,
                  const double* d_test, int m, const MaternDev& p, double* d_out);

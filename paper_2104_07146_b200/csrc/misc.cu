@@ -327,3 +327,127 @@ void sample_grf_dense(cudaStream_t st, const double* coords, int n, int dim, con
 }
 
 }  // namespace hmgp_gpu
+
+// ------------------------------------------------ dense diagnostics (n <= 4096)
+// HMatrix::to_dense (hmatrix.cpp:274-297), HFactor::lower_dense / reconstruct
+// (hfactor.cpp:421-449): leaves expanded on the device into a dense tree-order
+// matrix (one CTA per stored leaf; low-rank leaves as U V^T), then permuted to
+// the original order.  SURVEY.md §8f row 3.
+#include "factor.h"
+namespace hmgp_gpu {
+
+// mode bit 0: symmetric H-matrix (also write the mirror of off-diagonal leaves);
+// bit 1: factor (diagonal leaves: strict upper triangle zero, diagonal = 1 for
+// LDL or the stored L_ii (diag != nullptr) for Cholesky)
+__global__ void k_expand_leaves(const LeafDev* __restrict__ leaf, const int* __restrict__ rank,
+                                const int* __restrict__ r0, const int* __restrict__ c0, int n, int mode,
+                                const double* __restrict__ diag, double* __restrict__ T) {
+  const int k = blockIdx.x;
+  const LeafDev L = leaf[k];
+  const int rb = r0[k], cb = c0[k];
+  const bool on_diag = rb == cb;
+  const int r = L.kind == DENSE ? 0 : rank[k];
+  for (int e = threadIdx.x; e < L.m * L.n; e += blockDim.x) {
+    const int i = e % L.m, j = e / L.m;
+    double v;
+    if (L.kind == DENSE) {
+      v = L.a[(size_t)j * L.m + i];
+    } else {
+      v = 0.0;
+      for (int q = 0; q < r; ++q) v += L.a[(size_t)q * L.m + i] * L.b[(size_t)q * L.n + j];
+    }
+    if ((mode & 2) && on_diag) {
+      if (i < j) v = 0.0;
+      if (i == j) v = diag ? diag[rb + i] : 1.0;
+    }
+    T[(size_t)(cb + j) * n + rb + i] = v;
+    if ((mode & 1) && !on_diag) T[(size_t)(rb + i) * n + cb + j] = v;
+  }
+}
+
+__global__ void k_permute_dense(const double* __restrict__ T, const int* __restrict__ perm, int n,
+                                double* __restrict__ out) {
+  // out(perm[i], perm[j]) = T(i, j), column-major
+  const int j = blockIdx.y;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[(size_t)perm[j] * n + perm[i]] = T[(size_t)j * n + i];
+}
+
+__global__ void k_scale_cols(const double* __restrict__ A, const double* __restrict__ d, int n,
+                             double* __restrict__ W) {
+  const int j = blockIdx.y;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    W[(size_t)j * n + i] = A[(size_t)j * n + i] * d[j];
+}
+
+static void expand(cudaStream_t st, const Geometry& G, const std::vector<HNode>& nodes,
+                   const std::vector<int>& leaf_node, const LeafDev* d_leaf, const int* d_rank, int mode,
+                   const double* d_diag, double* d_T) {
+  const int n = G.n, L = (int)leaf_node.size();
+  std::vector<int> r0(L), c0(L);
+  for (int k = 0; k < L; ++k) {
+    r0[k] = G.nbeg[nodes[leaf_node[k]].row];
+    c0[k] = G.nbeg[nodes[leaf_node[k]].col];
+  }
+  DBuf<int> dr0(L), dc0(L);
+  HMGP_CUDA(cudaMemcpyAsync(dr0.p, r0.data(), 4ull * L, cudaMemcpyHostToDevice, st));
+  HMGP_CUDA(cudaMemcpyAsync(dc0.p, c0.data(), 4ull * L, cudaMemcpyHostToDevice, st));
+  HMGP_CUDA(cudaMemsetAsync(d_T, 0, 8ull * n * n, st));
+  if (L > 0) {
+    k_expand_leaves<<<L, 256, 0, st>>>(d_leaf, d_rank, dr0.p, dc0.p, n, mode, d_diag, d_T);
+    HMGP_LAUNCH_CHECK();
+  }
+  HMGP_CUDA(cudaStreamSynchronize(st));
+}
+
+static void check_dense_n(int n, const char* what) {
+  if (n > 4096) throw std::invalid_argument(std::string(what) + ": refused beyond n = 4096");
+}
+
+void hmat_to_dense(cudaStream_t st, const HMat& h, double* out) {
+  const Geometry& G = *h.g;
+  const int n = G.n;
+  check_dense_n(n, "to_dense");
+  DBuf<double> T((size_t)n * n), O((size_t)n * n);
+  expand(st, G, h.nodes, h.leaf_node, h.d_leaf, h.d_rank, 1, nullptr, T.p);
+  k_permute_dense<<<dim3((n + 255) / 256, n), 256, 0, st>>>(T.p, G.d_perm, n, O.p);
+  HMGP_LAUNCH_CHECK();
+  HMGP_CUDA(cudaMemcpyAsync(out, O.p, 8ull * n * n, cudaMemcpyDeviceToHost, st));
+  HMGP_CUDA(cudaStreamSynchronize(st));
+}
+
+void factor_lower_dense(cudaStream_t st, const Factor& F, double* out) {
+  const int n = F.g->n;
+  check_dense_n(n, "lower_dense");
+  DBuf<double> T((size_t)n * n);
+  expand(st, *F.g, F.nodes, F.leaf_node, F.d_leaf, F.d_rank, 2, F.ldl ? nullptr : F.d_d, T.p);
+  HMGP_CUDA(cudaMemcpyAsync(out, T.p, 8ull * n * n, cudaMemcpyDeviceToHost, st));
+  HMGP_CUDA(cudaStreamSynchronize(st));
+}
+
+void factor_reconstruct(cudaStream_t st, const Factor& F, double* out) {
+  const int n = F.g->n;
+  check_dense_n(n, "reconstruct");
+  DBuf<double> T((size_t)n * n), W((size_t)n * n), M((size_t)n * n);
+  expand(st, *F.g, F.nodes, F.leaf_node, F.d_leaf, F.d_rank, 2, F.ldl ? nullptr : F.d_d, T.p);
+  const double* Lw = T.p;
+  if (F.ldl) {  // W = L diag(d)
+    k_scale_cols<<<dim3((n + 255) / 256, n), 256, 0, st>>>(T.p, F.d_d, n, W.p);
+    HMGP_LAUNCH_CHECK();
+    Lw = W.p;
+  }
+  cublasHandle_t bh = nullptr;
+  if (cublasCreate(&bh) != CUBLAS_STATUS_SUCCESS) throw Error(HMGP_ECUDA, "cublasCreate failed");
+  cublasSetStream(bh, st);
+  const double one = 1.0, zero = 0.0;  // M = Lw L^T (tree order)
+  const cublasStatus_t bs =
+      cublasDgemm(bh, CUBLAS_OP_N, CUBLAS_OP_T, n, n, n, &one, Lw, n, T.p, n, &zero, M.p, n);
+  cublasDestroy(bh);
+  if (bs != CUBLAS_STATUS_SUCCESS) throw Error(HMGP_ECUDA, "cublasDgemm failed");
+  k_permute_dense<<<dim3((n + 255) / 256, n), 256, 0, st>>>(M.p, F.g->d_perm, n, W.p);
+  HMGP_LAUNCH_CHECK();
+  HMGP_CUDA(cudaMemcpyAsync(out, W.p, 8ull * n * n, cudaMemcpyDeviceToHost, st));
+  HMGP_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace hmgp_gpu

@@ -233,6 +233,27 @@ int hmgp_factor_diagonal(hmgp_ctx* ctx, const hmgp_factor* f, double* out) {
   })
 }
 
+int hmgp_hmat_to_dense(hmgp_ctx* ctx, const hmgp_hmat* h, double* out) {
+  API_GUARD2({
+    HMGP_CUDA(cudaSetDevice(ctx->device));
+    hmat_to_dense(ctx->stream, h->h, out);
+  })
+}
+
+int hmgp_factor_lower_dense(hmgp_ctx* ctx, const hmgp_factor* f, double* out) {
+  API_GUARD2({
+    HMGP_CUDA(cudaSetDevice(ctx->device));
+    factor_lower_dense(ctx->stream, *f->f, out);
+  })
+}
+
+int hmgp_factor_reconstruct(hmgp_ctx* ctx, const hmgp_factor* f, double* out) {
+  API_GUARD2({
+    HMGP_CUDA(cudaSetDevice(ctx->device));
+    factor_reconstruct(ctx->stream, *f->f, out);
+  })
+}
+
 void hmgp_factor_destroy(hmgp_factor* f) { delete f; }
 
 int hmgp_loglik(hmgp_ctx* ctx, const double* coords, int n, int dim, const double* z,

@@ -98,7 +98,7 @@ void truncate_hist_print() {
     static unsigned long long cc[7];
     HMGP_CUDA(cudaMemcpyFromSymbol(cc, d_clu_cyc, sizeof(cc)));
     fprintf(stderr,
-            "[hmgp]   trunc cluster(global) stages (s): stage-in %.3f qrU %.3f qrV %.3f core %.3f write %.3f "
+            "[hmgp]   trunc cluster(global) stages (s): stage-in %.3f qr %.3f core-form %.3f core-svd %.3f write %.3f "
             "applyU %.3f applyV %.3f\n",
             cc[0] / 1.9e9, cc[1] / 1.9e9, cc[2] / 1.9e9, cc[3] / 1.9e9, cc[4] / 1.9e9, cc[5] / 1.9e9,
             cc[6] / 1.9e9);
@@ -1086,7 +1086,6 @@ __device__ void lr_update_cluster(cg::cluster_group& cl, CluShared& sh, const Tr
       clu_qr(cl, sh, WV, n, r, tv, kClu / 2, kClu / 2, kit);
   }
   cstage(1);
-  cstage(2);
   const int ku = min(m, r), kv = min(n, r);
   const int kqmax = min(ku, kv);
   double* tau = C + (size_t)ku * kv;
@@ -1099,18 +1098,48 @@ __device__ void lr_update_cluster(cg::cluster_group& cl, CluShared& sh, const Tr
   double* gsig = Uc + (size_t)ku * kqmax;  // exported sigma / order for the other CTAs
   int* gord = reinterpret_cast<int*>(gsig + kqmax);
   RS rs{0, 0, 0.0};
-  if (rank == 0) {
-    for (int idx = threadIdx.x; idx < ku * kv; idx += blockDim.x) {
-      const int i = idx % ku, j = idx / ku;
-      double s = 0.0;
-      for (int l = max(i, j); l < r; ++l) s += WU[(size_t)l * m + i] * WV[(size_t)l * n + j];
-      C[(size_t)j * ku + i] = s;
+  {  // core(i,j) = sum_{l >= max(i,j)} Ru(i,l) Rv(j,l), 32x32 tiles spread over all
+     // ranks of the cluster and staged through shared memory (sh.part is free
+     // between the QR and the Q application).  Every entry accumulates l in
+     // ascending order from a start <= max(i,j); the masked entries below the
+     // diagonals contribute exact zeros, so C is bit-identical to the
+     // one-rank formula it replaces.
+    double* As = &sh.part[0][0];  // [l][i], 32 x 32
+    double* Bs = As + 1024;       // [l][j]
+    const int ti = (ku + 31) / 32, tj = (kv + 31) / 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, nty = blockDim.x >> 5;
+    for (int t = rank; t < ti * tj; t += kClu) {
+      const int i0 = (t % ti) * 32, j0 = (t / ti) * 32;
+      double acc[2] = {0.0, 0.0};
+      for (int l0 = max(i0, j0); l0 < r; l0 += 32) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < 1024; e += blockDim.x) {
+          const int a = e & 31, gl = l0 + (e >> 5), gi = i0 + a, gj = j0 + a;
+          As[e] = (gl < r && gi < ku && gi <= gl) ? WU[(size_t)gl * m + gi] : 0.0;
+          Bs[e] = (gl < r && gj < kv && gj <= gl) ? WV[(size_t)gl * n + gj] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int l = 0; l < 32; ++l) {
+          const double a = As[l * 32 + tx];
+          for (int q = 0; q < 2; ++q)
+            if (ty + q * nty < 32) acc[q] += a * Bs[l * 32 + ty + q * nty];
+        }
+      }
+      for (int q = 0; q < 2; ++q) {
+        const int i = i0 + tx, j = j0 + ty + q * nty;
+        if (ty + q * nty < 32 && i < ku && j < kv) C[(size_t)j * ku + i] = acc[q];
+      }
     }
-    __syncthreads();
+    cl.sync();
+  }
+  cstage(2);
+  if (rank == 0) {
     // lean rank-revealing SVD (virtual pivoting, one barrier per step)
     const bool lean = kv <= 128;  // the lean variant's pivot bitmask covers 128 columns
+    long long tcs = clock64();    // HMGP_STATS: rrqr / jacobi / core-Q split in path 1's slots
     if (lean) {
-      rs = cta_rrqr_svd2(C, ku, kv, eps, tau, phys, cn, stepof, G, J, s_sig, s_ord, 1, nullptr);
+      rs = cta_rrqr_svd2(C, ku, kv, eps, tau, phys, cn, stepof, G, J, s_sig, s_ord, 1, &tcs);
     } else {
       rs = cta_rrqr_svd(C, ku, kv, eps, tau, phys, cn, G, J, s_sig, s_ord, red);
       for (int j = threadIdx.x; j < kv; j += blockDim.x) phys[j] = j;  // explicit swaps: identity map
@@ -1122,6 +1151,7 @@ __device__ void lr_update_cluster(cg::cluster_group& cl, CluShared& sh, const Tr
     }
     __syncthreads();
     cta_apply_q_map(C, ku, ku, rs.kq, tau, phys, Uc, rs.keep);
+    stage_add(1, 4, tcs);
     for (int c = threadIdx.x; c < rs.keep; c += blockDim.x) {
       gsig[c] = s_sig[s_ord[c]];
       gord[c] = s_ord[c];

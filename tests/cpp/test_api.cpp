@@ -126,6 +126,29 @@ int main() {
     for (size_t i = 0; i < c.size(); ++i) worst = std::max(worst, std::abs(c[i] - (1.7 * a[i] - 0.4 * b[i])));
     CHECK(worst <= 1e-10);
   }
+  {  // dense diagnostics (test_hmatrix.cpp:91-98, test_hfactor.cpp:71-99)
+    std::vector<Location> one{{0.4, 0.6}};
+    ClusterTree t1(one, 32);
+    BlockClusterTree b1(t1, t1, 2.0);
+    const HMatrix h1 = assemble(b1, one, MaternParams{1.2, 0.1, 0.5, 0.3}, RankControl::fixed_accuracy(1e-6));
+    CHECK(std::abs(h1.to_dense()(0, 0) - 1.5) <= 1.5e-14);
+    const auto pts = random_locations(512, 31);
+    ClusterTree t(pts, 32);
+    BlockClusterTree b(t, t, 2.0);
+    const MaternParams p{1.0, 0.1, 0.5, 0.01};
+    const HMatrix h = assemble(b, pts, p, RankControl::fixed_accuracy(1e-6));
+    const Matrix d = h.to_dense();
+    const HFactor fc = h_cholesky(h, 1e-6);
+    const Matrix rc = fc.reconstruct();
+    double num = 0, den = 0;
+    for (size_t e = 0; e < d.data.size(); ++e) {
+      num += (rc.data[e] - d.data[e]) * (rc.data[e] - d.data[e]);
+      den += d.data[e] * d.data[e];
+    }
+    CHECK(std::sqrt(num / den) <= 1e-4);
+    const Matrix l = h_ldl(h, 1e-6).lower_dense();
+    CHECK(l(0, 0) == 1.0 && l(0, 1) == 0.0);
+  }
   std::printf("%s (%d failures)\n", g_fail ? "FAILED" : "ALL PASSED", g_fail);
   return g_fail ? 1 : 0;
 }
