@@ -293,31 +293,62 @@ void sample_grf_dense(cudaStream_t st, const double* coords, int n, int dim, con
     k_cov_dense_lower<<<grid, 256, 0, st>>>(dx.p, n, dim, p, dC.p, j0);
     HMGP_LAUNCH_CHECK();
   }
+  // blocked right-looking Cholesky, nb = 4096: POTRF of each diagonal block
+  // (cuSOLVER), TRSM of the panel below it and SYRK of the trailing matrix
+  // (cuBLAS 64-bit API) -- every library call stays far below 2^31 elements
+  // per operand dimension product except the GEMM-like updates, which take
+  // 64-bit sizes
   cusolverDnHandle_t sh = nullptr;
   cusolverDnParams_t prm = nullptr;
+  cublasHandle_t bh = nullptr;
   if (cusolverDnCreate(&sh) != CUSOLVER_STATUS_SUCCESS) throw Error(HMGP_ECUDA, "cusolverDnCreate failed");
+  if (cublasCreate(&bh) != CUBLAS_STATUS_SUCCESS) {
+    cusolverDnDestroy(sh);
+    throw Error(HMGP_ECUDA, "cublasCreate failed");
+  }
   cusolverDnSetStream(sh, st);
+  cublasSetStream(bh, st);
   cusolverDnCreateParams(&prm);
-  size_t dbytes = 0, hbytes = 0;
-  cusolverStatus_t cs = cusolverDnXpotrf_bufferSize(sh, prm, CUBLAS_FILL_MODE_LOWER, n, CUDA_R_64F, dC.p, n,
-                                                    CUDA_R_64F, &dbytes, &hbytes);
+  const int64_t nb = 4096, ld = n;
+  bool lib_ok = true;
   int info = 0;
-  if (cs == CUSOLVER_STATUS_SUCCESS) {
-    DBuf<char> dwork(dbytes);
+  {
+    size_t dbytes = 0, hbytes = 0;
+    const int64_t b0 = std::min<int64_t>(nb, n);
+    lib_ok = cusolverDnXpotrf_bufferSize(sh, prm, CUBLAS_FILL_MODE_LOWER, b0, CUDA_R_64F, dC.p, ld, CUDA_R_64F,
+                                         &dbytes, &hbytes) == CUSOLVER_STATUS_SUCCESS;
+    DBuf<char> dwork(std::max<size_t>(dbytes, 1));
     std::vector<char> hwork(std::max<size_t>(hbytes, 1));
     DBuf<int> dinfo(1);
-    cs = cusolverDnXpotrf(sh, prm, CUBLAS_FILL_MODE_LOWER, n, CUDA_R_64F, dC.p, n, CUDA_R_64F, dwork.p,
-                          dbytes, hwork.data(), hbytes, dinfo.p);
-    HMGP_CUDA(cudaMemcpyAsync(&info, dinfo.p, 4, cudaMemcpyDeviceToHost, st));
-    HMGP_CUDA(cudaStreamSynchronize(st));
+    for (int64_t k0 = 0; lib_ok && k0 < n; k0 += nb) {
+      const int64_t kb = std::min<int64_t>(nb, n - k0), rest = n - k0 - kb;
+      double* A11 = dC.p + (size_t)k0 * ld + k0;
+      lib_ok = cusolverDnXpotrf(sh, prm, CUBLAS_FILL_MODE_LOWER, kb, CUDA_R_64F, A11, ld, CUDA_R_64F, dwork.p,
+                                dbytes, hwork.data(), hbytes, dinfo.p) == CUSOLVER_STATUS_SUCCESS;
+      HMGP_CUDA(cudaMemcpyAsync(&info, dinfo.p, 4, cudaMemcpyDeviceToHost, st));
+      HMGP_CUDA(cudaStreamSynchronize(st));
+      if (!lib_ok || info != 0) break;
+      if (rest > 0) {
+        double* A21 = A11 + kb;
+        double* A22 = A21 + (size_t)kb * ld;
+        const double one = 1.0, mone = -1.0;
+        lib_ok = cublasDtrsm_64(bh, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT,
+                                rest, kb, &one, A11, ld, A21, ld) == CUBLAS_STATUS_SUCCESS &&
+                 cublasDsyrk_64(bh, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, rest, kb, &mone, A21, ld, &one, A22,
+                                ld) == CUBLAS_STATUS_SUCCESS;
+      }
+    }
   }
   cusolverDnDestroyParams(prm);
   cusolverDnDestroy(sh);
-  if (cs != CUSOLVER_STATUS_SUCCESS) throw Error(HMGP_ECUDA, "cusolverDnXpotrf failed");
-  if (info != 0) throw std::runtime_error("sample_grf: covariance not SPD; increase nugget tau2");
-  cublasHandle_t bh = nullptr;
-  if (cublasCreate(&bh) != CUBLAS_STATUS_SUCCESS) throw Error(HMGP_ECUDA, "cublasCreate failed");
-  cublasSetStream(bh, st);
+  if (!lib_ok) {
+    cublasDestroy(bh);
+    throw Error(HMGP_ECUDA, "sample_grf: cuSOLVER/cuBLAS call failed");
+  }
+  if (info != 0) {
+    cublasDestroy(bh);
+    throw std::runtime_error("sample_grf: covariance not SPD; increase nugget tau2");
+  }
   const cublasStatus_t bs =
       cublasDtrmv_64(bh, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, n, dC.p, n, dw.p, 1);
   HMGP_CUDA(cudaMemcpyAsync(out, dw.p, 8ull * n, cudaMemcpyDeviceToHost, st));
