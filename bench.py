@@ -29,6 +29,8 @@ import os
 import subprocess
 import sys
 import threading
+
+import numpy as np
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -276,6 +278,22 @@ def extras(hm, _lib, ctx, stream):
         e1.synchronize()
         return e0.elapsed_time(e1), r
 
+    # C3 θ-throughput: the same n = 262144 problem, 5 θ (ℓ nudged) through
+    # hmgp_loglik_batch on one geometry (the first θ alone sizes the workspace,
+    # the other four run concurrently on host workers / streams).  One L(θ) keeps
+    # a small part of the GPU busy, so an MLE probe batch fills the idle SMs.
+    xc3 = hm.jittered_grid(C3["g"], SEED)
+    zc3 = torch.from_numpy(hm.normals(C3["g"] ** 2, Z_SEED)).to(torch.device("cuda", ctx.device))
+    gc3 = hm.Geometry(xc3, C3["leaf"], 2.0, ctx=ctx)
+    cfg3 = hm.HConfig(leaf_size=C3["leaf"], rank=hm.RankControl.fixed_accuracy(C3["eps"]), form=C3["form"])
+    th3 = np.array([[C3["theta"][0], C3["theta"][1] * (1.0 + 0.01 * k), C3["theta"][2], C3["theta"][3]]
+                    for k in range(5)])
+    from paper_2104_07146_b200 import sweep as sw3
+    ms3, v3 = dev_ms(lambda: sw3.run_sweep(gc3, zc3.data_ptr(), th3, list(range(5)), cfg3, ctx))
+    out["C3_theta_batch"] = {"n": C3["g"] ** 2, "thetas": 5, "ms": ms3, "evals_per_s": 5 / (ms3 / 1e3),
+                             "loglik": v3[:, 0].tolist(), "status": v3[:, 3].tolist(),
+                             "note": "5 θ via hmgp_loglik_batch: θ0 alone, then 4 concurrent"}
+    del gc3, zc3
     # C2: assembly only, n = 65536 jittered 256x256, leaf 64, eta 2, eps 1e-7
     x = hm.jittered_grid(256, SEED)
     g = hm.Geometry(x, 64, 2.0, ctx=ctx)

@@ -865,8 +865,8 @@ struct CluShared {
 // halves of the cluster).  Every rank executes the same barrier sequence: kit
 // column steps (the larger of the two groups' min(m, r)), two cluster barriers
 // each, whether or not its group has work at that step.
-__device__ void clu_qr(cg::cluster_group& cl, CluShared& sh, double* A, int m, int r, double* tau, int g0,
-                       int gs, int kit) {
+__device__ void clu_qr_2b(cg::cluster_group& cl, CluShared& sh, double* A, int m, int r, double* tau, int g0,
+                          int gs, int kit) {
   double (*gb)[kGather] = sh.gb;
   const int rank = cl.block_rank();
   const int ms = (m + gs - 1) / gs, lo = (rank - g0) * ms, hi = min(m, lo + ms);
@@ -945,48 +945,199 @@ __device__ void clu_qr(cg::cluster_group& cl, CluShared& sh, double* A, int m, i
   cl.sync();
 }
 
+// One cluster barrier per column (r <= kCluMaxR / 2): at step k every rank
+// publishes, for its own rows, the partial tail norm^2 of the UNNORMALISED
+// column x = A(:, k) and the partial dots x_tail . A(:, j) for j > k; the owner
+// of row k also publishes the heads A(k, k..r-1).  After the barrier every warp
+// forms the reflector scalars (t, beta, inv) from the group sums itself and the
+// full dots as s_j = t (A(k, j) + inv D_j) -- the same reflector as the
+// two-barrier variant, v = [1; inv x_tail] -- and updates its columns' own
+// rows.  Column k is normalised one step late (nobody reads it then), so the
+// only intra-CTA barrier is the one that makes step k's updates visible to
+// step k+1's partials.  Partials are double-buffered by step parity: a rank
+// overwrites buffer k&1 only after passing step k+1's barrier, i.e. after every
+// rank has finished reading it at step k.
+// lda: column stride of A.  A may be a shared-memory row slice addressed with
+// global row indices (A = slice - lo, lda = slice height): only own rows are
+// touched.
+__device__ void clu_qr(cg::cluster_group& cl, CluShared& sh, double* A, int m, int r, double* tau, int g0,
+                       int gs, int kit, int lda) {
+  if (2 * r > kCluMaxR) {  // (only reached with lda == m: see lr_update_cluster)
+    clu_qr_2b(cl, sh, A, m, r, tau, g0, gs, kit);
+    return;
+  }
+  const int rank = cl.block_rank();
+  const int ms = (m + gs - 1) / gs, lo = (rank - g0) * ms, hi = min(m, lo + ms);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int kmax = min(m, r);
+  double pt = 0.0, pinv = 0.0, pbeta = 0.0;  // previous step's scalars (lagged normalisation)
+  for (int k = 0; k < kit; ++k) {
+    const bool act = k < kmax;
+    double* P = sh.part[k & 1];
+    // lagged normalisation of column k-1 (own rows), by the last warp
+    if (k > 0 && k - 1 < kmax && w == nw - 1) {
+      double* xp = A + (size_t)(k - 1) * lda;
+      for (int i = max(lo, k) + lane; i < hi; i += 32) xp[i] = (pt == 0.0) ? 0.0 : xp[i] * pinv;
+      if (lane == 0 && k - 1 >= lo && k - 1 < hi) xp[k - 1] = pbeta;
+    }
+    const double* x = A + (size_t)k * lda;
+    const bool own_k = k >= lo && k < hi;
+    if (act) {
+      // virtual column q = 0: norm of x's tail; q >= 1: dot with column k + q.
+      // Four columns per warp pass: their loads and shuffle reductions overlap.
+      for (int q0 = w; q0 < r - k; q0 += 4 * nw) {
+        const double* c[4];
+        bool on[4];
+        double sd[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int q = q0 + u * nw;
+          on[u] = q < r - k;
+          c[u] = (on[u] && q > 0) ? A + (size_t)(k + q) * lda : x;
+          sd[u] = 0.0;
+        }
+        for (int i = max(lo, k + 1) + lane; i < hi; i += 32) {
+          const double xi = x[i];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) sd[u] += xi * c[u][i];
+        }
+        warp_sum_n<4>(sd);
+        if (lane == 0)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int q = q0 + u * nw;
+            if (!on[u]) continue;
+            if (q == 0) {
+              P[0] = sd[u];
+              P[1] = own_k ? x[k] : 0.0;
+            } else {
+              P[2 + k + q] = sd[u];                   // dots at P[2 + j] (j = k + q)
+              if (own_k) P[2 + r + k + q] = c[u][k];  // heads at P[2 + r + j]
+            }
+          }
+      }
+    }
+    cl.sync();
+    if (act) {
+      // reflector scalars from the group sums (every warp, identical arithmetic)
+      const int owner = g0 + min(k / ms, gs - 1);
+      double part = 0.0;
+      if (lane < gs) part = cl.map_shared_rank(P, g0 + lane)[0];
+      else if (lane == gs) part = cl.map_shared_rank(P, owner)[1];
+      double tail2 = 0.0;
+      for (int c = 0; c < gs; ++c) tail2 += __shfl_sync(0xffffffffu, part, c);
+      const double c0 = __shfl_sync(0xffffffffu, part, gs);
+      double t = 0.0, beta = c0, inv = 0.0;
+      if (tail2 > 2.2250738585072014e-308) {
+        beta = sqrt(c0 * c0 + tail2);
+        if (c0 >= 0.0) beta = -beta;
+        inv = 1.0 / (c0 - beta);
+        t = (beta - c0) / beta;
+      }
+      if (rank == g0 && threadIdx.x == 0) tau[k] = t;
+      if (t != 0.0) {
+        // lanes < gs read rank lane's dot partials, lane gs the owner's heads;
+        // four columns' remote loads are in flight at once
+        const double* Prem = lane < gs ? cl.map_shared_rank(P, g0 + lane) : cl.map_shared_rank(P, owner);
+        const int off = lane < gs ? 2 : 2 + r;
+        for (int j0 = k + 1 + w; j0 < r; j0 += 4 * nw) {
+          double dp[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = j0 + u * nw;
+            dp[u] = (j < r && lane <= gs) ? Prem[off + j] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = j0 + u * nw;
+            double D = 0.0;
+            for (int c = 0; c < gs; ++c) D += __shfl_sync(0xffffffffu, dp[u], c);
+            const double head = __shfl_sync(0xffffffffu, dp[u], gs);
+            if (j >= r) continue;
+            const double sj = t * (head + inv * D);
+            double* cj = A + (size_t)j * lda;
+            for (int i = max(lo, k + 1) + lane; i < hi; i += 32) cj[i] -= sj * (inv * x[i]);
+            if (lane == 0 && own_k) cj[k] -= sj;
+          }
+        }
+      }
+      pt = t;
+      pinv = inv;
+      pbeta = beta;
+    }
+    __syncthreads();
+  }
+  // normalise the last factored column
+  if (kit > 0 && kit - 1 < kmax && w == nw - 1) {
+    double* xp = A + (size_t)(kit - 1) * lda;
+    for (int i = max(lo, kit) + lane; i < hi; i += 32) xp[i] = (pt == 0.0) ? 0.0 : xp[i] * pinv;
+    if (lane == 0 && kit - 1 >= lo && kit - 1 < hi) xp[kit - 1] = pbeta;
+  }
+  cl.sync();
+}
+
 // E <- Q E over a group's row slices (Q from clu_qr with the same group), E m x c
 // (ld m); kit reflector steps for every rank (uniform barrier sequence).
 __device__ void clu_apply_q(cg::cluster_group& cl, CluShared& sh, const double* A, int m, int kq,
-                            const double* tau, double* E, int c, int g0, int gs, int kit) {
-  double (*gb)[kGather] = sh.gb;
+                            const double* tau, double* E, int c, int g0, int gs, int kit, int lda, int lde) {
   const int rank = cl.block_rank();
   const int ms = (m + gs - 1) / gs, lo = (rank - g0) * ms, hi = min(m, lo + ms);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int k = kit - 1; k >= 0; --k) {
     const double t = k < kq ? tau[k] : 0.0;
     const bool up = t != 0.0;
+    const bool own_k = k >= lo && k < hi;
     double* P = sh.part[k & 1];
-    const double* v = A + (size_t)k * m;
+    const double* v = A + (size_t)k * lda;
+    // partial dots v . E(:, j) over own rows (+ the unit head on the owner);
+    // column j is handled by the same warp in both phases, so E needs no
+    // intra-CTA barrier, only the cluster barrier for the partials
     if (up)
-      for (int j = w; j < c; j += nw) {
-        const double* e = E + (size_t)j * m;
-        double s = 0.0;
-        for (int i = max(lo, k + 1) + lane; i < hi; i += 32) s += v[i] * e[i];
-        s = warp_sum(s);
-        if (lane == 0) P[2 + j] = s + ((k >= lo && k < hi) ? e[k] : 0.0);
+      for (int j0 = w; j0 < c; j0 += 4 * nw) {
+        double sd[4];
+        const double* e[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = min(j0 + u * nw, c - 1);
+          e[u] = E + (size_t)j * lde;
+          sd[u] = 0.0;
+        }
+        for (int i = max(lo, k + 1) + lane; i < hi; i += 32) {
+          const double vi = v[i];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) sd[u] += vi * e[u][i];
+        }
+        warp_sum_n<4>(sd);
+        if (lane == 0)
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (j0 + u * nw < c) P[2 + j0 + u * nw] = sd[u] + (own_k ? e[u][k] : 0.0);
       }
     cl.sync();
-    if (up)
-      for (int jc = 0; jc < c; jc += kGather) {
-        const int nj = min(kGather, c - jc);
-        if (threadIdx.x < gs * kGather) {
-          const int cc = threadIdx.x / kGather, jj = threadIdx.x % kGather;
-          if (jj < nj) gb[cc][jj] = cl.map_shared_rank(P, g0 + cc)[2 + jc + jj];
+    if (up) {
+      const double* Prem = cl.map_shared_rank(P, g0 + min(lane, gs - 1));
+      for (int j0 = w; j0 < c; j0 += 4 * nw) {
+        double dp[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = j0 + u * nw;
+          dp[u] = (j < c && lane < gs) ? Prem[2 + j] : 0.0;
         }
-        __syncthreads();
-        for (int j = jc + w; j < jc + nj; j += nw) {
-          double s = 0.0;
-          for (int q = 0; q < gs; ++q) s += gb[q][j - jc];
-          s *= t;
-          double* e = E + (size_t)j * m;
-          for (int i = max(lo, k + 1) + lane; i < hi; i += 32) e[i] -= s * v[i];
-          if (lane == 0 && k >= lo && k < hi) e[k] -= s;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = j0 + u * nw;
+          double sj = 0.0;
+          for (int q = 0; q < gs; ++q) sj += __shfl_sync(0xffffffffu, dp[u], q);  // rank order
+          if (j >= c) continue;
+          sj *= t;
+          double* e = E + (size_t)j * lde;
+          for (int i = max(lo, k + 1) + lane; i < hi; i += 32) e[i] -= sj * v[i];
+          if (lane == 0 && own_k) e[k] -= sj;
         }
-        __syncthreads();
       }
+    }
     // the next step overwrites the other parity buffer only after every rank
-    // passed this step's first barrier, so one barrier per step suffices here
+    // passed this step's barrier, so one barrier per step suffices here
   }
   cl.sync();
 }
@@ -1053,6 +1204,7 @@ __device__ void lr_update_cluster(cg::cluster_group& cl, CluShared& sh, const Tr
   double* tu = WV + (size_t)n * it.rcap;
   double* tv = tu + it.rcap;
   double* C = tv + it.rcap;
+  const int ku = min(m, r), kv = min(n, r);
   // stage [U | aP] and [V | Q] (own row slices)
   for (int l = 0; l < r; ++l) {
     for (int i = mlo + threadIdx.x; i < mhi; i += blockDim.x) {
@@ -1080,13 +1232,13 @@ __device__ void lr_update_cluster(cg::cluster_group& cl, CluShared& sh, const Tr
   cstage(0);
   {  // U on ranks 0-3, V on ranks 4-7, at once
     const int kit = max(min(m, r), min(n, r));
-    if (rank < kClu / 2)
-      clu_qr(cl, sh, WU, m, r, tu, 0, kClu / 2, kit);
-    else
-      clu_qr(cl, sh, WV, n, r, tv, kClu / 2, kClu / 2, kit);
+    if (rank < kClu / 2) {
+      clu_qr(cl, sh, WU, m, r, tu, 0, kClu / 2, kit, m);
+    } else {
+      clu_qr(cl, sh, WV, n, r, tv, kClu / 2, kClu / 2, kit, n);
+    }
   }
   cstage(1);
-  const int ku = min(m, r), kv = min(n, r);
   const int kqmax = min(ku, kv);
   double* tau = C + (size_t)ku * kv;
   double* cn = tau + kv;                                // 2 kv (double-buffered norms)
@@ -1171,22 +1323,25 @@ __device__ void lr_update_cluster(cg::cluster_group& cl, CluShared& sh, const Tr
     return;
   }
   // E_u = [U_core; 0] -> it.U, E_v = [Y; 0] -> it.V (own row slices)
-  for (int c = 0; c < keep; ++c) {
-    for (int i = mlo + threadIdx.x; i < mhi; i += blockDim.x)
-      it.U[(size_t)c * m + i] = i < ku ? Uc[(size_t)c * ku + i] : 0.0;
-    const int src = gord[c];
-    const double sg = gsig[c];
-    for (int i = nlo + threadIdx.x; i < nhi; i += blockDim.x)
-      it.V[(size_t)c * n + i] = i < kv ? G[(size_t)src * kv + i] / sg : 0.0;
+  {
+    for (int c = 0; c < keep; ++c) {
+      for (int i = mlo + threadIdx.x; i < mhi; i += blockDim.x)
+        it.U[(size_t)c * m + i] = i < ku ? Uc[(size_t)c * ku + i] : 0.0;
+      const int src = gord[c];
+      const double sg = gsig[c];
+      for (int i = nlo + threadIdx.x; i < nhi; i += blockDim.x)
+        it.V[(size_t)c * n + i] = i < kv ? G[(size_t)src * kv + i] / sg : 0.0;
+    }
   }
   cl.sync();
   cstage(4);
   {
     const int kit = max(ku, kv);
-    if (rank < kClu / 2)
-      clu_apply_q(cl, sh, WU, m, ku, tu, it.U, keep, 0, kClu / 2, kit);
-    else
-      clu_apply_q(cl, sh, WV, n, kv, tv, it.V, keep, kClu / 2, kClu / 2, kit);
+    if (rank < kClu / 2) {
+      clu_apply_q(cl, sh, WU, m, ku, tu, it.U, keep, 0, kClu / 2, kit, m, m);
+    } else {
+      clu_apply_q(cl, sh, WV, n, kv, tv, it.V, keep, kClu / 2, kClu / 2, kit, n, n);
+    }
   }
   cstage(5);
   cstage(6);
@@ -1650,7 +1805,9 @@ void launch_truncate_cluster(const TruncItem* d_items, const int* d_off, int tar
     HMGP_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     // ~112 KB: enough for the register path's slices (ms <= 256 at r <= 32,
     // ms <= 128 at r <= 40) while leaving L1 for the items that fall back to
-    // the global-memory path
+    // the global-memory path (measured: a 200 KB carve-out holding the global
+    // path's row slices in shared memory instead was 20 % slower per item --
+    // the rank-0 core SVD then misses L1)
     bytes = std::min((size_t)optin - fa.sharedSizeBytes - 1024, (size_t)14336 * 8);
     HMGP_CUDA(cudaFuncSetAttribute(k_truncate_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)bytes));
