@@ -70,6 +70,7 @@ __device__ __forceinline__ void hist_add(int path, int m, int n, int r, long lon
 __device__ unsigned long long d_stage_cyc[3][5], d_stage_sweeps[3], d_stage_jac[3];
 // (stats mode) global cluster path stages: stage-in, QR U, QR V, core SVD, write, apply U, apply V
 __device__ unsigned long long d_clu_cyc[7];
+__device__ unsigned long long d_qr_cyc[5];  // clu_qr phases (rank 0, thread 0): partials, barrier, gather+update, syncthreads, steps
 __device__ __forceinline__ void stage_add(int path, int st, long long& t) {
   if (!d_hist_on || threadIdx.x != 0) return;
   const long long now = clock64();
@@ -97,6 +98,12 @@ void truncate_hist_print() {
   {
     static unsigned long long cc[7];
     HMGP_CUDA(cudaMemcpyFromSymbol(cc, d_clu_cyc, sizeof(cc)));
+    unsigned long long qc[5];
+    HMGP_CUDA(cudaMemcpyFromSymbol(qc, d_qr_cyc, sizeof(qc)));
+    if (qc[4])
+      fprintf(stderr, "[hmgp]   cluster QR per column step (cycles, rank 0 thread 0): partials %.0f barrier %.0f "
+              "gather+update %.0f syncthreads %.0f (%llu steps)\n", (double)qc[0] / qc[4], (double)qc[1] / qc[4],
+              (double)qc[2] / qc[4], (double)qc[3] / qc[4], qc[4]);
     fprintf(stderr,
             "[hmgp]   trunc cluster(global) stages (s): stage-in %.3f qr %.3f core-form %.3f core-svd %.3f write %.3f "
             "applyU %.3f applyV %.3f\n",
@@ -960,17 +967,24 @@ __device__ void clu_qr_2b(cg::cluster_group& cl, CluShared& sh, double* A, int m
 // lda: column stride of A.  A may be a shared-memory row slice addressed with
 // global row indices (A = slice - lo, lda = slice height): only own rows are
 // touched.
-__device__ void clu_qr(cg::cluster_group& cl, CluShared& sh, double* A, int m, int r, double* tau, int g0,
-                       int gs, int kit, int lda) {
-  if (2 * r > kCluMaxR) {  // (only reached with lda == m: see lr_update_cluster)
-    clu_qr_2b(cl, sh, A, m, r, tau, g0, gs, kit);
-    return;
-  }
+// kQrRows: rows per lane held in registers (the slice height / 32, rounded up
+// to 2, 4 or 8; taller slices fall back to row loops).
+template <int kQrRows>
+__device__ void clu_qr_t(cg::cluster_group& cl, CluShared& sh, double* A, int m, int r, double* tau, int g0,
+                         int gs, int kit, int lda) {
   const int rank = cl.block_rank();
   const int ms = (m + gs - 1) / gs, lo = (rank - g0) * ms, hi = min(m, lo + ms);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int kmax = min(m, r);
   double pt = 0.0, pinv = 0.0, pbeta = 0.0;  // previous step's scalars (lagged normalisation)
+  const bool prof = d_hist_on && rank == 0 && threadIdx.x == 0;
+  long long tq = prof ? clock64() : 0;
+  auto qmark = [&](int i) {
+    if (!prof) return;
+    const long long now = clock64();
+    atomicAdd(&d_qr_cyc[i], (unsigned long long)(now - tq));
+    tq = now;
+  };
   for (int k = 0; k < kit; ++k) {
     const bool act = k < kmax;
     double* P = sh.part[k & 1];
@@ -982,6 +996,16 @@ __device__ void clu_qr(cg::cluster_group& cl, CluShared& sh, double* A, int m, i
     }
     const double* x = A + (size_t)k * lda;
     const bool own_k = k >= lo && k < hi;
+    // this lane's rows of the step (i0 + 32 t, t < nrow); with at most kQrRows
+    // per lane (slices <= 256 rows) x's tail stays in registers for the step and
+    // each four-column group issues all its loads before any arithmetic / store
+    // (one memory round trip per group instead of one per row)
+    const int i0 = max(lo, k + 1) + lane;
+    const int nrow = i0 < hi ? (hi - i0 + 31) / 32 : 0;
+    const bool regs = (hi - lo + 31) / 32 <= kQrRows;
+    double xv[kQrRows];
+#pragma unroll
+    for (int t = 0; t < kQrRows; ++t) xv[t] = (regs && act && t < nrow) ? x[i0 + 32 * t] : 0.0;
     if (act) {
       // virtual column q = 0: norm of x's tail; q >= 1: dot with column k + q.
       // Four columns per warp pass: their loads and shuffle reductions overlap.
@@ -996,10 +1020,22 @@ __device__ void clu_qr(cg::cluster_group& cl, CluShared& sh, double* A, int m, i
           c[u] = (on[u] && q > 0) ? A + (size_t)(k + q) * lda : x;
           sd[u] = 0.0;
         }
-        for (int i = max(lo, k + 1) + lane; i < hi; i += 32) {
-          const double xi = x[i];
+        if (regs) {
+          double cv[4][kQrRows];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) sd[u] += xi * c[u][i];
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int t = 0; t < kQrRows; ++t) cv[u][t] = t < nrow ? c[u][i0 + 32 * t] : 0.0;
+#pragma unroll
+          for (int t = 0; t < kQrRows; ++t)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) sd[u] += xv[t] * cv[u][t];
+        } else {
+          for (int i = i0; i < hi; i += 32) {
+            const double xi = x[i];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) sd[u] += xi * c[u][i];
+          }
         }
         warp_sum_n<4>(sd);
         if (lane == 0)
@@ -1017,7 +1053,9 @@ __device__ void clu_qr(cg::cluster_group& cl, CluShared& sh, double* A, int m, i
           }
       }
     }
+    qmark(0);
     cl.sync();
+    qmark(1);
     if (act) {
       // reflector scalars from the group sums (every warp, identical arithmetic)
       const int owner = g0 + min(k / ms, gs - 1);
@@ -1047,17 +1085,41 @@ __device__ void clu_qr(cg::cluster_group& cl, CluShared& sh, double* A, int m, i
             const int j = j0 + u * nw;
             dp[u] = (j < r && lane <= gs) ? Prem[off + j] : 0.0;
           }
+          double sj[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const int j = j0 + u * nw;
             double D = 0.0;
             for (int c = 0; c < gs; ++c) D += __shfl_sync(0xffffffffu, dp[u], c);
             const double head = __shfl_sync(0xffffffffu, dp[u], gs);
-            if (j >= r) continue;
-            const double sj = t * (head + inv * D);
-            double* cj = A + (size_t)j * lda;
-            for (int i = max(lo, k + 1) + lane; i < hi; i += 32) cj[i] -= sj * (inv * x[i]);
-            if (lane == 0 && own_k) cj[k] -= sj;
+            sj[u] = t * (head + inv * D);
+          }
+          if (regs) {
+            double* cjp[4];
+            double cv[4][kQrRows];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              cjp[u] = A + (size_t)min(j0 + u * nw, r - 1) * lda;
+#pragma unroll
+              for (int t2 = 0; t2 < kQrRows; ++t2)
+                cv[u][t2] = (j0 + u * nw < r && t2 < nrow) ? cjp[u][i0 + 32 * t2] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (j0 + u * nw >= r) continue;
+#pragma unroll
+              for (int t2 = 0; t2 < kQrRows; ++t2)
+                if (t2 < nrow) cjp[u][i0 + 32 * t2] = cv[u][t2] - sj[u] * (inv * xv[t2]);
+              if (lane == 0 && own_k) cjp[u][k] -= sj[u];
+            }
+          } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int j = j0 + u * nw;
+              if (j >= r) continue;
+              double* cj = A + (size_t)j * lda;
+              for (int i = i0; i < hi; i += 32) cj[i] -= sj[u] * (inv * x[i]);
+              if (lane == 0 && own_k) cj[k] -= sj[u];
+            }
           }
         }
       }
@@ -1065,7 +1127,10 @@ __device__ void clu_qr(cg::cluster_group& cl, CluShared& sh, double* A, int m, i
       pinv = inv;
       pbeta = beta;
     }
+    qmark(2);
     __syncthreads();
+    qmark(3);
+    if (prof) atomicAdd(&d_qr_cyc[4], 1ull);
   }
   // normalise the last factored column
   if (kit > 0 && kit - 1 < kmax && w == nw - 1) {
@@ -1078,8 +1143,9 @@ __device__ void clu_qr(cg::cluster_group& cl, CluShared& sh, double* A, int m, i
 
 // E <- Q E over a group's row slices (Q from clu_qr with the same group), E m x c
 // (ld m); kit reflector steps for every rank (uniform barrier sequence).
-__device__ void clu_apply_q(cg::cluster_group& cl, CluShared& sh, const double* A, int m, int kq,
-                            const double* tau, double* E, int c, int g0, int gs, int kit, int lda, int lde) {
+template <int kQrRows>
+__device__ void clu_apply_q_t(cg::cluster_group& cl, CluShared& sh, const double* A, int m, int kq,
+                              const double* tau, double* E, int c, int g0, int gs, int kit, int lda, int lde) {
   const int rank = cl.block_rank();
   const int ms = (m + gs - 1) / gs, lo = (rank - g0) * ms, hi = min(m, lo + ms);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -1089,6 +1155,14 @@ __device__ void clu_apply_q(cg::cluster_group& cl, CluShared& sh, const double* 
     const bool own_k = k >= lo && k < hi;
     double* P = sh.part[k & 1];
     const double* v = A + (size_t)k * lda;
+    // register-held rows as in clu_qr: v's tail once per step, all loads of a
+    // four-column group issued before its arithmetic / stores
+    const int i0 = max(lo, k + 1) + lane;
+    const int nrow = i0 < hi ? (hi - i0 + 31) / 32 : 0;
+    const bool regs = (hi - lo + 31) / 32 <= kQrRows;
+    double vv[kQrRows];
+#pragma unroll
+    for (int q = 0; q < kQrRows; ++q) vv[q] = (regs && up && q < nrow) ? v[i0 + 32 * q] : 0.0;
     // partial dots v . E(:, j) over own rows (+ the unit head on the owner);
     // column j is handled by the same warp in both phases, so E needs no
     // intra-CTA barrier, only the cluster barrier for the partials
@@ -1102,10 +1176,22 @@ __device__ void clu_apply_q(cg::cluster_group& cl, CluShared& sh, const double* 
           e[u] = E + (size_t)j * lde;
           sd[u] = 0.0;
         }
-        for (int i = max(lo, k + 1) + lane; i < hi; i += 32) {
-          const double vi = v[i];
+        if (regs) {
+          double ev[4][kQrRows];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) sd[u] += vi * e[u][i];
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int q = 0; q < kQrRows; ++q) ev[u][q] = q < nrow ? e[u][i0 + 32 * q] : 0.0;
+#pragma unroll
+          for (int q = 0; q < kQrRows; ++q)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) sd[u] += vv[q] * ev[u][q];
+        } else {
+          for (int i = i0; i < hi; i += 32) {
+            const double vi = v[i];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) sd[u] += vi * e[u][i];
+          }
         }
         warp_sum_n<4>(sd);
         if (lane == 0)
@@ -1123,16 +1209,39 @@ __device__ void clu_apply_q(cg::cluster_group& cl, CluShared& sh, const double* 
           const int j = j0 + u * nw;
           dp[u] = (j < c && lane < gs) ? Prem[2 + j] : 0.0;
         }
+        double sj[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int j = j0 + u * nw;
-          double sj = 0.0;
-          for (int q = 0; q < gs; ++q) sj += __shfl_sync(0xffffffffu, dp[u], q);  // rank order
-          if (j >= c) continue;
-          sj *= t;
-          double* e = E + (size_t)j * lde;
-          for (int i = max(lo, k + 1) + lane; i < hi; i += 32) e[i] -= sj * v[i];
-          if (lane == 0 && own_k) e[k] -= sj;
+          double su = 0.0;
+          for (int q = 0; q < gs; ++q) su += __shfl_sync(0xffffffffu, dp[u], q);  // rank order
+          sj[u] = su * t;
+        }
+        if (regs) {
+          double* ep[4];
+          double ev[4][kQrRows];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            ep[u] = E + (size_t)min(j0 + u * nw, c - 1) * lde;
+#pragma unroll
+            for (int q = 0; q < kQrRows; ++q) ev[u][q] = (j0 + u * nw < c && q < nrow) ? ep[u][i0 + 32 * q] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (j0 + u * nw >= c) continue;
+#pragma unroll
+            for (int q = 0; q < kQrRows; ++q)
+              if (q < nrow) ep[u][i0 + 32 * q] = ev[u][q] - sj[u] * vv[q];
+            if (lane == 0 && own_k) ep[u][k] -= sj[u];
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = j0 + u * nw;
+            if (j >= c) continue;
+            double* e = E + (size_t)j * lde;
+            for (int i = i0; i < hi; i += 32) e[i] -= sj[u] * v[i];
+            if (lane == 0 && own_k) e[k] -= sj[u];
+          }
         }
       }
     }
@@ -1140,6 +1249,32 @@ __device__ void clu_apply_q(cg::cluster_group& cl, CluShared& sh, const double* 
     // passed this step's barrier, so one barrier per step suffices here
   }
   cl.sync();
+}
+
+__device__ void clu_qr(cg::cluster_group& cl, CluShared& sh, double* A, int m, int r, double* tau, int g0,
+                       int gs, int kit, int lda) {
+  if (2 * r > kCluMaxR) {  // (only reached with lda == m: see lr_update_cluster)
+    clu_qr_2b(cl, sh, A, m, r, tau, g0, gs, kit);
+    return;
+  }
+  const int rpl = ((m + gs - 1) / gs + 31) / 32;
+  if (rpl <= 2)
+    clu_qr_t<2>(cl, sh, A, m, r, tau, g0, gs, kit, lda);
+  else if (rpl <= 4)
+    clu_qr_t<4>(cl, sh, A, m, r, tau, g0, gs, kit, lda);
+  else
+    clu_qr_t<8>(cl, sh, A, m, r, tau, g0, gs, kit, lda);
+}
+
+__device__ void clu_apply_q(cg::cluster_group& cl, CluShared& sh, const double* A, int m, int kq,
+                            const double* tau, double* E, int c, int g0, int gs, int kit, int lda, int lde) {
+  const int rpl = ((m + gs - 1) / gs + 31) / 32;
+  if (rpl <= 2)
+    clu_apply_q_t<2>(cl, sh, A, m, kq, tau, E, c, g0, gs, kit, lda, lde);
+  else if (rpl <= 4)
+    clu_apply_q_t<4>(cl, sh, A, m, kq, tau, E, c, g0, gs, kit, lda, lde);
+  else
+    clu_apply_q_t<8>(cl, sh, A, m, kq, tau, E, c, g0, gs, kit, lda, lde);
 }
 
 __device__ void lr_update_cluster(cg::cluster_group& cl, CluShared& sh, const TruncItem& it,
