@@ -418,6 +418,53 @@ inline PredictionResult predict(std::span<const Location> train, const Vector& z
   return res;
 }
 
+// krige.hpp kriging_variance_dense (krige.cpp:46-74) on the GPU, dense, n <= 4096
+inline Vector kriging_variance_dense(std::span<const Location> train,
+                                     std::span<const Location> new_locations,
+                                     const MaternParams& params) {
+  params.validate();
+  const auto tr = detail::flat(train);
+  const auto te = detail::flat(new_locations);
+  const hmgp_matern m = params.c();
+  Vector out(new_locations.size());
+  detail::check(hmgp_kriging_variance_dense(detail::context(), tr.data(), static_cast<int>(train.size()), 2,
+                                            te.data(), static_cast<int>(new_locations.size()), &m,
+                                            out.data()));
+  return out;
+}
+
+// metrics.hpp (metrics.cpp:11-69): rmse on the host, mloe_mmom dense on the GPU
+inline double rmse(const Vector& z_hat, const Vector& z_true) {
+  if (z_hat.size() != z_true.size()) throw std::invalid_argument("rmse: length mismatch");
+  if (z_hat.size() == 0) throw std::invalid_argument("rmse: empty input");
+  double s = 0.0;
+  for (size_t i = 0; i < z_hat.size(); ++i) s += (z_hat[i] - z_true[i]) * (z_hat[i] - z_true[i]);
+  return std::sqrt(s / static_cast<double>(z_hat.size()));
+}
+
+struct MetricConfig {
+  int M = 1000;  // evaluation locations, clamped to n
+  std::uint64_t seed = 0;
+  int dense_guard = 4096;
+};
+
+struct MloeMmom {
+  double mloe = 0.0;
+  double mmom = 0.0;
+};
+
+inline MloeMmom mloe_mmom(std::span<const Location> locations, const MaternParams& theta_true,
+                          const MaternParams& theta_approx, const MetricConfig& cfg = {}) {
+  theta_true.validate();
+  theta_approx.validate();
+  const auto xy = detail::flat(locations);
+  const hmgp_matern mt = theta_true.c(), ma = theta_approx.c();
+  MloeMmom r;
+  detail::check(hmgp_mloe_mmom(detail::context(), xy.data(), static_cast<int>(locations.size()), 2, &mt, &ma,
+                               cfg.M, cfg.seed, cfg.dense_guard, &r.mloe, &r.mmom));
+  return r;
+}
+
 // simgen.hpp data utilities over the C ABI
 inline std::vector<Location> random_locations(int n, std::uint64_t seed) {  // simgen.cpp:114-123
   if (n < 1) throw std::invalid_argument("random_locations: n must be >= 1");

@@ -206,6 +206,19 @@ int hmgp_normals(int n, uint64_t seed, double* out);
 int hmgp_sample_grf(hmgp_ctx* ctx, const double* coords, int n, int dim, const hmgp_matern* theta,
                     uint64_t seed, double* out);
 
+/* ------------------------------------------- dense diagnostics */
+/* kriging_variance_dense(train, new_locations, params) (krige.hpp / krige.cpp:46-74):
+   out_i = σ²+τ² − c_iᵀ C11⁻¹ c_i, dense FP64 on device, n <= 4096 (HMGP_EINVAL beyond),
+   HMGP_ERUNTIME when C11 is not SPD.  Host buffers. */
+int hmgp_kriging_variance_dense(hmgp_ctx* ctx, const double* train, int n, int dim, const double* test, int m,
+                                const hmgp_matern* theta, double* out);
+/* mloe_mmom(locations, theta_true, theta_approx, MetricConfig{M, seed, dense_guard})
+   (metrics.hpp:24-31 / metrics.cpp:17-69): leave-one-out kriging MLOE / MMOM closed
+   forms, dense FP64 on device, n <= min(dense_guard, 4096).  Host buffers. */
+int hmgp_mloe_mmom(hmgp_ctx* ctx, const double* coords, int n, int dim, const hmgp_matern* theta_true,
+                   const hmgp_matern* theta_approx, int M, uint64_t seed, int dense_guard, double* mloe,
+                   double* mmom);
+
 #ifdef __cplusplus
 }
 #endif

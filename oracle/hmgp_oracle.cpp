@@ -2147,4 +2147,98 @@ int orc_normals(int n, uint64_t seed, double* out) {
   })
 }
 
+// kriging_variance_dense (krige.cpp:46-74): dense LLT of cov_dense(train),
+// v_i = (sigma2 + tau2) - c.solve(c), c_j = at_distance(|s_i - t_j|); rounding
+// clamp of (-1e-9, 0) to 0 on interpolation points.
+int orc_kriging_variance_dense(const double* train, int n, int dim, const double* test, int m,
+                               const double* th, double* out) {
+  ORC_GUARD({
+    const Matern p = mp(th);
+    p.validate();
+    if (n < 1) throw std::invalid_argument("kriging_variance_dense: empty training set");
+    if (n > 4096)
+      throw std::invalid_argument("kriging_variance_dense: dense path capped at n = 4096");
+    Mat c;
+    cov_dense(train, n, dim, p, c);
+    if (!dense_chol(c, 1))
+      throw std::runtime_error("kriging_variance_dense: C11 not SPD; increase nugget tau2");
+    Kernel k(train, dim, p);
+    const double prior = p.sigma2 + p.tau2;
+    std::vector<double> cv(n), x(n);
+    for (int i = 0; i < m; ++i) {
+      for (int j = 0; j < n; ++j)
+        cv[j] = k.at(Kernel::dist(test + static_cast<size_t>(i) * dim, train + static_cast<size_t>(j) * dim, dim));
+      x = cv;
+      trsm_left_lower(vw(c), View{x.data(), n, 1, n});
+      trsm_left_lower_t(vw(c), View{x.data(), n, 1, n});
+      double d = 0.0;
+      for (int j = 0; j < n; ++j) d += cv[j] * x[j];
+      double v = prior - d;
+      if (v < 0.0 && v > -1e-9) v = 0.0;
+      out[i] = v;
+    }
+  })
+}
+
+// mloe_mmom (metrics.cpp:17-69): M targets by a seeded partial Fisher-Yates over
+// mt19937_64, leave-one-out kriging closed forms under the true and the
+// approximating parameters.
+int orc_mloe_mmom(const double* x, int n, int dim, const double* tt, const double* ta, int M,
+                  uint64_t seed, int dense_guard, double* mloe, double* mmom) {
+  ORC_GUARD({
+    const Matern pt = mp(tt), pa = mp(ta);
+    pt.validate();
+    pa.validate();
+    if (n < 2) throw std::invalid_argument("mloe_mmom: need at least 2 locations");
+    if (n > dense_guard)
+      throw std::invalid_argument("mloe_mmom: dense evaluation capped at n = " + std::to_string(dense_guard));
+    if (M < 1) throw std::invalid_argument("mloe_mmom: M must be >= 1");
+    const int m = std::min(M, n);
+    std::vector<int> idx(n);
+    for (int i = 0; i < n; ++i) idx[i] = i;
+    std::mt19937_64 rng(seed);
+    for (int i = 0; i < m; ++i) {
+      const int j = i + static_cast<int>(rng() % static_cast<std::uint64_t>(n - i));
+      std::swap(idx[i], idx[j]);
+    }
+    Mat ct, lt, la;
+    cov_dense(x, n, dim, pt, ct);
+    lt = ct;
+    cov_dense(x, n, dim, pa, la);
+    if (!dense_chol(lt, 1) || !dense_chol(la, 1))
+      throw std::runtime_error("mloe_mmom: covariance not SPD; increase nugget tau2");
+    Mat gt(n, m), ga(n, m);
+    for (int k = 0; k < m; ++k) {
+      gt(idx[k], k) = 1.0;
+      ga(idx[k], k) = 1.0;
+    }
+    trsm_left_lower(vw(lt), vw(gt));
+    trsm_left_lower_t(vw(lt), vw(gt));
+    trsm_left_lower(vw(la), vw(ga));
+    trsm_left_lower_t(vw(la), vw(ga));
+    std::vector<double> gd(m);
+    for (int k = 0; k < m; ++k) {
+      gd[k] = ga(idx[k], k);
+      const double s = -1.0 / gd[k];
+      for (int i = 0; i < n; ++i) ga(i, k) *= s;
+    }
+    double lo = 0.0, mo = 0.0;
+    std::vector<double> w(n);
+    for (int k = 0; k < m; ++k) {
+      for (int i = 0; i < n; ++i) {  // (c_t g_a)(:, k)
+        double s = 0.0;
+        for (int l = 0; l < n; ++l) s += ct(i, l) * ga(l, k);
+        w[i] = s;
+      }
+      double d = 0.0;
+      for (int i = 0; i < n; ++i) d += ga(i, k) * w[i];
+      const double e_tt = 1.0 / gt(idx[k], k), e_aa = 1.0 / gd[k], e_ta = d;
+      lo += e_ta / e_tt - 1.0;
+      mo += e_aa / e_ta - 1.0;
+    }
+    *mloe = lo / m;
+    *mmom = mo / m;
+  })
+}
+
 }  // extern "C"

@@ -76,6 +76,10 @@ int orc_sample_grf(const double* x, int n, int dim, const double* theta, uint64_
 int orc_normal_quantile(double p, double* out);
 int orc_random_locations(int n, int dim, uint64_t seed, double* out);
 int orc_jittered_grid(int g, uint64_t seed, double* out);
+int orc_kriging_variance_dense(const double* train, int n, int dim, const double* test, int m,
+                               const double* th, double* out);
+int orc_mloe_mmom(const double* x, int n, int dim, const double* tt, const double* ta, int M,
+                  uint64_t seed, int dense_guard, double* mloe, double* mmom);
 int orc_normals(int n, uint64_t seed, double* out);
 
 #ifdef __cplusplus

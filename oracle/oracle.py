@@ -110,6 +110,9 @@ class Oracle:
         L.orc_cross_apply.argtypes = [_dp, C.c_int, C.c_int, _dp, _dp, C.c_int, _dp, C.c_int, _dp]
         L.orc_dense_loglik.argtypes = [_dp, C.c_int, C.c_int, _dp, _dp, C.c_int, _dp, _dp, _dp]
         L.orc_dense_predict.argtypes = [_dp, C.c_int, C.c_int, _dp, _dp, C.c_int, _dp, C.c_int, _dp]
+        L.orc_kriging_variance_dense.argtypes = [_dp, C.c_int, C.c_int, _dp, C.c_int, _dp, _dp]
+        L.orc_mloe_mmom.argtypes = [_dp, C.c_int, C.c_int, _dp, _dp, C.c_int, C.c_uint64, C.c_int,
+                                    _dp, _dp]
 
     def _chk(self, rc):
         if rc != 0:
@@ -246,6 +249,25 @@ class Oracle:
                                            _d(test), test.shape[0], _d(th),
                                            threads or os.cpu_count(), _d(out)))
         return out
+
+    def kriging_variance_dense(self, train, test, theta):
+        """krige.cpp:46-74 restated (hmgp_oracle.cpp orc_kriging_variance_dense)."""
+        train, test = _xy(train), _xy(test)
+        th = np.asarray(theta, dtype=np.float64)
+        out = np.empty(test.shape[0])
+        self._chk(self.L.orc_kriging_variance_dense(_d(train), train.shape[0], train.shape[1],
+                                                    _d(test), test.shape[0], _d(th), _d(out)))
+        return out
+
+    def mloe_mmom(self, x, theta_true, theta_approx, M=1000, seed=0, dense_guard=4096):
+        """metrics.cpp:17-69 restated (hmgp_oracle.cpp orc_mloe_mmom) -> (mloe, mmom)."""
+        x = _xy(x)
+        tt = np.asarray(theta_true, dtype=np.float64)
+        ta = np.asarray(theta_approx, dtype=np.float64)
+        a, b = C.c_double(), C.c_double()
+        self._chk(self.L.orc_mloe_mmom(_d(x), x.shape[0], x.shape[1], _d(tt), _d(ta), M, seed,
+                                       dense_guard, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def counters(self):
         out = np.zeros(11)

@@ -152,6 +152,10 @@ _sig("hmgp_predict", C.c_int, [_vp, _dp, C.c_int, C.c_int, _dp, _dp, C.c_int, C.
                                C.POINTER(_Config), _dp, _dp])
 _sig("hmgp_cross_apply_device", C.c_int, [_vp, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
                                           C.c_int, C.POINTER(Matern), C.c_void_p])
+_sig("hmgp_kriging_variance_dense", C.c_int, [_vp, _dp, C.c_int, C.c_int, _dp, C.c_int, C.POINTER(Matern),
+                                             _dp])
+_sig("hmgp_mloe_mmom", C.c_int, [_vp, _dp, C.c_int, C.c_int, C.POINTER(Matern), C.POINTER(Matern), C.c_int,
+                                 C.c_uint64, C.c_int, _dp, _dp])
 _sig("hmgp_random_locations", C.c_int, [C.c_int, C.c_int, C.c_uint64, _dp])
 _sig("hmgp_jittered_grid", C.c_int, [C.c_int, C.c_uint64, _dp])
 _sig("hmgp_normals", C.c_int, [C.c_int, C.c_uint64, _dp])
@@ -584,6 +588,57 @@ def predict(train, z1, new_locations, params, cfg: HConfig = None, ctx=None):
     _chk(_lib.hmgp_predict(ctx.h, _d(tr), tr.shape[0], tr.shape[1], _d(z1), _d(te), te.shape[0],
                            C.byref(m), C.byref(c), _d(out), C.byref(sec)))
     return PredictionResult(out, sec.value)
+
+
+def kriging_variance_dense(train, new_locations, params, ctx=None):
+    """kriging_variance_dense (krige.hpp / krige.cpp:46-74): σ²+τ² − cᵀC₁₁⁻¹c per new
+    location, dense FP64 on the GPU, n <= 4096."""
+    ctx = ctx or default_context()
+    tr = _pts(train)
+    te = np.ascontiguousarray(new_locations, dtype=np.float64).reshape(-1, tr.shape[1])
+    out = np.empty(te.shape[0])
+    m = _mp(params)
+    _chk(_lib.hmgp_kriging_variance_dense(ctx.h, _d(tr), tr.shape[0], tr.shape[1], _d(te), te.shape[0],
+                                          C.byref(m), _d(out)))
+    return out
+
+
+@dataclass
+class MetricConfig:
+    """metrics.hpp:13-17"""
+    M: int = 1000
+    seed: int = 0
+    dense_guard: int = 4096
+
+
+@dataclass
+class MloeMmom:
+    """metrics.hpp:19-22"""
+    mloe: float
+    mmom: float
+
+
+def mloe_mmom(locations, theta_true, theta_approx, cfg: MetricConfig = None, ctx=None):
+    """mloe_mmom (metrics.hpp:24-31 / metrics.cpp:17-69) on the GPU (dense FP64)."""
+    ctx = ctx or default_context()
+    cfg = cfg or MetricConfig()
+    x = _pts(locations)
+    mt, ma = _mp(theta_true), _mp(theta_approx)
+    a, b = C.c_double(), C.c_double()
+    _chk(_lib.hmgp_mloe_mmom(ctx.h, _d(x), x.shape[0], x.shape[1], C.byref(mt), C.byref(ma), cfg.M, cfg.seed,
+                             cfg.dense_guard, C.byref(a), C.byref(b)))
+    return MloeMmom(a.value, b.value)
+
+
+def rmse(z_hat, z_true):
+    """rmse (metrics.cpp:11-15): host arithmetic on two vectors, as in the reference."""
+    a = np.asarray(z_hat, dtype=np.float64)
+    b = np.asarray(z_true, dtype=np.float64)
+    if a.size != b.size:
+        raise ValueError("rmse: length mismatch")
+    if a.size == 0:
+        raise ValueError("rmse: empty input")
+    return float(np.sqrt(np.sum((a - b) ** 2) / a.size))
 
 
 # -------------------------------------------------------------- data utils

@@ -387,6 +387,51 @@ int hmgp_sample_grf(hmgp_ctx* ctx, const double* coords, int n, int dim, const h
   })
 }
 
+/* kriging_variance_dense(train, new_locations, params) (krige.cpp:46-74), dense, on device */
+int hmgp_kriging_variance_dense(hmgp_ctx* ctx, const double* train, int n, int dim, const double* test, int m,
+                                const hmgp_matern* theta, double* out) {
+  API_GUARD({
+    hmgp_validate_matern(theta);
+    if (dim != 2 && dim != 3) throw std::invalid_argument("dim must be 2 or 3");
+    if (n < 1) throw std::invalid_argument("kriging_variance_dense: empty training set");
+    if (n > 4096) throw std::invalid_argument("kriging_variance_dense: dense path capped at n = 4096");
+    if (m < 0) throw std::invalid_argument("kriging_variance_dense: m < 0");
+    HMGP_CUDA(cudaSetDevice(ctx->device));
+    kriging_variance_dense(ctx->stream, train, n, test, m, dim,
+                           make_matern(theta->sigma2, theta->ell, theta->nu, theta->tau2), out);
+  })
+}
+
+/* mloe_mmom(locations, theta_true, theta_approx, cfg) (metrics.cpp:17-69), dense, on device */
+int hmgp_mloe_mmom(hmgp_ctx* ctx, const double* coords, int n, int dim, const hmgp_matern* theta_true,
+                   const hmgp_matern* theta_approx, int M, uint64_t seed, int dense_guard, double* mloe,
+                   double* mmom) {
+  API_GUARD({
+    hmgp_validate_matern(theta_true);
+    hmgp_validate_matern(theta_approx);
+    if (dim != 2 && dim != 3) throw std::invalid_argument("dim must be 2 or 3");
+    if (n < 2) throw std::invalid_argument("mloe_mmom: need at least 2 locations");
+    if (n > dense_guard)
+      throw std::invalid_argument("mloe_mmom: dense evaluation capped at n = " + std::to_string(dense_guard));
+    if (n > 4096) throw std::invalid_argument("mloe_mmom: dense evaluation capped at n = 4096");
+    if (M < 1) throw std::invalid_argument("mloe_mmom: M must be >= 1");
+    const int m = std::min(M, n);
+    // M distinct targets by a seeded partial Fisher-Yates (metrics.cpp:30-36)
+    std::vector<int> idx(n);
+    for (int i = 0; i < n; ++i) idx[i] = i;
+    std::mt19937_64 rng(seed);
+    for (int i = 0; i < m; ++i) {
+      const int j = i + static_cast<int>(rng() % static_cast<uint64_t>(n - i));
+      std::swap(idx[i], idx[j]);
+    }
+    HMGP_CUDA(cudaSetDevice(ctx->device));
+    mloe_mmom(ctx->stream, coords, n, dim,
+              make_matern(theta_true->sigma2, theta_true->ell, theta_true->nu, theta_true->tau2),
+              make_matern(theta_approx->sigma2, theta_approx->ell, theta_approx->nu, theta_approx->tau2),
+              idx.data(), m, mloe, mmom);
+  })
+}
+
 }  // extern "C"
 
 int hmgp_fail(int code, const char* msg) { return fail(code, msg); }

@@ -57,6 +57,12 @@ void at_distance(cudaStream_t st, const MaternDev& p, const double* h, int64_t c
 // sample_grf (simgen.cpp:125-141): z = chol(cov_dense) w, host buffers
 void sample_grf_dense(cudaStream_t st, const double* coords, int n, int dim, const MaternDev& p,
                       const double* w, double* out);
+// kriging_variance_dense (krige.cpp:46-74) / mloe_mmom (metrics.cpp:17-69), dense,
+// n <= 4096, host buffers; idx = the m sampled targets
+void kriging_variance_dense(cudaStream_t st, const double* train, int n, const double* test, int m, int dim,
+                            const MaternDev& p, double* out);
+void mloe_mmom(cudaStream_t st, const double* x, int n, int dim, const MaternDev& pt, const MaternDev& pa,
+               const int* idx, int m, double* mloe, double* mmom);
 void bessel_batch(cudaStream_t st, const double* nu, const double* x, int64_t count, int generic,
                   double* out);
 void hmat_matvec(cudaStream_t st, const HMat& h, const double* x, double* y);

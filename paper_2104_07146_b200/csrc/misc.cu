@@ -482,3 +482,203 @@ void factor_reconstruct(cudaStream_t st, const Factor& F, double* out) {
 }
 
 }  // namespace hmgp_gpu
+
+// ------------------------------------ dense kriging variance / MLOE-MMOM (§8f 4)
+// kriging_variance_dense (krige.cpp:46-74) and mloe_mmom (metrics.cpp:17-69): the
+// reference's dense small-n diagnostics (n <= 4096), on the device.  Covariance
+// and cross-covariance entries come from the same Matérn kernel as the hot path;
+// the dense LLT / triangular solves / SYMM are library calls (cuSOLVER POTRF +
+// POTRS, cuBLAS DSYMM) since these are diagnostics outside every timed region.
+namespace hmgp_gpu {
+
+namespace {
+struct DenseLib {
+  cusolverDnHandle_t sh = nullptr;
+  cusolverDnParams_t prm = nullptr;
+  cublasHandle_t bh = nullptr;
+  explicit DenseLib(cudaStream_t st) {
+    if (cusolverDnCreate(&sh) != CUSOLVER_STATUS_SUCCESS) throw Error(HMGP_ECUDA, "cusolverDnCreate failed");
+    if (cublasCreate(&bh) != CUBLAS_STATUS_SUCCESS) {
+      cusolverDnDestroy(sh);
+      throw Error(HMGP_ECUDA, "cublasCreate failed");
+    }
+    cusolverDnSetStream(sh, st);
+    cublasSetStream(bh, st);
+    cusolverDnCreateParams(&prm);
+  }
+  ~DenseLib() {
+    cusolverDnDestroyParams(prm);
+    cusolverDnDestroy(sh);
+    cublasDestroy(bh);
+  }
+  // in-place lower Cholesky of the n x n column-major A; false if not SPD
+  bool potrf(cudaStream_t st, double* A, int64_t n) {
+    size_t db = 0, hb = 0;
+    if (cusolverDnXpotrf_bufferSize(sh, prm, CUBLAS_FILL_MODE_LOWER, n, CUDA_R_64F, A, n, CUDA_R_64F, &db, &hb) !=
+        CUSOLVER_STATUS_SUCCESS)
+      throw Error(HMGP_ECUDA, "cusolverDnXpotrf_bufferSize failed");
+    DBuf<char> dw(std::max<size_t>(db, 1));
+    std::vector<char> hw(std::max<size_t>(hb, 1));
+    DBuf<int> dinfo(1);
+    if (cusolverDnXpotrf(sh, prm, CUBLAS_FILL_MODE_LOWER, n, CUDA_R_64F, A, n, CUDA_R_64F, dw.p, db, hw.data(), hb,
+                         dinfo.p) != CUSOLVER_STATUS_SUCCESS)
+      throw Error(HMGP_ECUDA, "cusolverDnXpotrf failed");
+    int info = 0;
+    HMGP_CUDA(cudaMemcpyAsync(&info, dinfo.p, 4, cudaMemcpyDeviceToHost, st));
+    HMGP_CUDA(cudaStreamSynchronize(st));
+    return info == 0;
+  }
+  // B <- A^-1 B with A = L L^T from potrf, B n x k
+  void potrs(cudaStream_t st, const double* L, int64_t n, double* B, int64_t k) {
+    DBuf<int> dinfo(1);
+    if (cusolverDnXpotrs(sh, prm, CUBLAS_FILL_MODE_LOWER, n, k, CUDA_R_64F, L, n, CUDA_R_64F, B, n, dinfo.p) !=
+        CUSOLVER_STATUS_SUCCESS)
+      throw Error(HMGP_ECUDA, "cusolverDnXpotrs failed");
+  }
+};
+
+void cov_lower(cudaStream_t st, const double* d_x, int n, int dim, const MaternDev& p, double* d_C) {
+  k_cov_dense_lower<<<dim3(std::min((n + 255) / 256, 64), n), 256, 0, st>>>(d_x, n, dim, p, d_C, 0);
+  HMGP_LAUNCH_CHECK();
+}
+}  // namespace
+
+// C(j, k) = at_distance(|test_k - train_j|), column-major n x m (one column per
+// new location, the reference's c vector)
+__global__ void k_cov_cross(const double* __restrict__ train, int n, const double* __restrict__ test, int dim,
+                            MaternDev p, double* __restrict__ Cnm) {
+  const int k = blockIdx.y;
+  const double* pa = test + (size_t)k * dim;
+  const double ax = pa[0], ay = pa[1], az = dim == 3 ? pa[2] : 0.0;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const double* pb = train + (size_t)j * dim;
+    const double h = dim == 2 ? dist2d(ax, ay, pb[0], pb[1]) : dist3d(ax, ay, az, pb[0], pb[1], pb[2]);
+    Cnm[(size_t)k * n + j] = matern_at(p, h);
+  }
+}
+
+template <int NT>
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double red[NT / 32];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < NT / 32; ++w) s += red[w];
+  return s;  // valid on thread 0
+}
+
+// out[k] = prior - c_k . x_k with the reference's (-1e-9, 0) -> 0 clamp
+__global__ void k_kvar_finish(const double* __restrict__ Cnm, const double* __restrict__ X, int n, double prior,
+                              double* __restrict__ out) {
+  const int k = blockIdx.x;
+  double s = 0.0;
+  for (int j = threadIdx.x; j < n; j += 256) s += Cnm[(size_t)k * n + j] * X[(size_t)k * n + j];
+  s = block_sum<256>(s);
+  if (threadIdx.x == 0) {
+    double v = prior - s;
+    if (v < 0.0 && v > -1e-9) v = 0.0;
+    out[k] = v;
+  }
+}
+
+void kriging_variance_dense(cudaStream_t st, const double* train, int n, const double* test, int m, int dim,
+                            const MaternDev& p, double* out) {
+  if (m == 0) return;
+  DBuf<double> dx((size_t)n * dim), dL((size_t)n * n);
+  HMGP_CUDA(cudaMemcpyAsync(dx.p, train, 8ull * n * dim, cudaMemcpyHostToDevice, st));
+  cov_lower(st, dx.p, n, dim, p, dL.p);
+  DenseLib lib(st);
+  if (!lib.potrf(st, dL.p, n))
+    throw std::runtime_error("kriging_variance_dense: C11 not SPD; increase nugget tau2");
+  const int mb = std::min(m, 4096);
+  DBuf<double> dt((size_t)mb * dim), dC((size_t)n * mb), dX((size_t)n * mb), dv(mb);
+  const double prior = p.sigma2 + p.tau2;
+  for (int k0 = 0; k0 < m; k0 += mb) {
+    const int kb = std::min(mb, m - k0);
+    HMGP_CUDA(cudaMemcpyAsync(dt.p, test + (size_t)k0 * dim, 8ull * kb * dim, cudaMemcpyHostToDevice, st));
+    k_cov_cross<<<dim3(std::min((n + 255) / 256, 16), kb), 256, 0, st>>>(dx.p, n, dt.p, dim, p, dC.p);
+    HMGP_LAUNCH_CHECK();
+    HMGP_CUDA(cudaMemcpyAsync(dX.p, dC.p, 8ull * n * kb, cudaMemcpyDeviceToDevice, st));
+    lib.potrs(st, dL.p, n, dX.p, kb);
+    k_kvar_finish<<<kb, 256, 0, st>>>(dC.p, dX.p, n, prior, dv.p);
+    HMGP_LAUNCH_CHECK();
+    HMGP_CUDA(cudaMemcpyAsync(out + k0, dv.p, 8ull * kb, cudaMemcpyDeviceToHost, st));
+  }
+  HMGP_CUDA(cudaStreamSynchronize(st));
+}
+
+// E(idx[k], k) = 1 in a zeroed n x m matrix
+__global__ void k_unit_cols(const int* __restrict__ idx, int n, int m, double* __restrict__ E) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < m) E[(size_t)k * n + idx[k]] = 1.0;
+}
+
+// ga_diag(k) = G_a(idx[k], k); G_a(:, k) *= -1 / ga_diag(k)
+__global__ void k_loo_weights(const int* __restrict__ idx, int n, double* __restrict__ Ga, double* __restrict__ gd) {
+  const int k = blockIdx.x;
+  double* col = Ga + (size_t)k * n;
+  const double d = col[idx[k]];
+  __syncthreads();  // every thread has read the diagonal before it is scaled
+  const double s = -1.0 / d;
+  for (int i = threadIdx.x; i < n; i += 256) col[i] *= s;
+  if (threadIdx.x == 0) gd[k] = d;
+}
+
+// per target k: terms[2k] = E_t[(Zhat_a - Z)^2] / E_t[(Zhat_t - Z)^2] - 1 (MLOE),
+// terms[2k+1] = E_a[(Zhat_a - Z)^2] / E_t[(Zhat_a - Z)^2] - 1 (MMOM)
+__global__ void k_mloe_terms(const int* __restrict__ idx, int n, const double* __restrict__ Gt,
+                             const double* __restrict__ Ga, const double* __restrict__ CtW,
+                             const double* __restrict__ gd, double* __restrict__ terms) {
+  const int k = blockIdx.x;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += 256) s += Ga[(size_t)k * n + i] * CtW[(size_t)k * n + i];
+  s = block_sum<256>(s);
+  if (threadIdx.x == 0) {
+    const double e_tt = 1.0 / Gt[(size_t)k * n + idx[k]], e_aa = 1.0 / gd[k], e_ta = s;
+    terms[2 * k] = e_ta / e_tt - 1.0;
+    terms[2 * k + 1] = e_aa / e_ta - 1.0;
+  }
+}
+
+void mloe_mmom(cudaStream_t st, const double* x, int n, int dim, const MaternDev& pt, const MaternDev& pa,
+               const int* idx, int m, double* mloe, double* mmom) {
+  DBuf<double> dx((size_t)n * dim), dCt((size_t)n * n), dLt((size_t)n * n), dLa((size_t)n * n);
+  DBuf<double> dGt((size_t)n * m), dGa((size_t)n * m), dW((size_t)n * m), dgd(m), dterms(2ull * m);
+  DBuf<int> didx(m);
+  HMGP_CUDA(cudaMemcpyAsync(dx.p, x, 8ull * n * dim, cudaMemcpyHostToDevice, st));
+  HMGP_CUDA(cudaMemcpyAsync(didx.p, idx, 4ull * m, cudaMemcpyHostToDevice, st));
+  cov_lower(st, dx.p, n, dim, pt, dCt.p);
+  HMGP_CUDA(cudaMemcpyAsync(dLt.p, dCt.p, 8ull * n * n, cudaMemcpyDeviceToDevice, st));
+  cov_lower(st, dx.p, n, dim, pa, dLa.p);
+  DenseLib lib(st);
+  if (!lib.potrf(st, dLt.p, n) || !lib.potrf(st, dLa.p, n))
+    throw std::runtime_error("mloe_mmom: covariance not SPD; increase nugget tau2");
+  HMGP_CUDA(cudaMemsetAsync(dGt.p, 0, 8ull * n * m, st));
+  k_unit_cols<<<(m + 255) / 256, 256, 0, st>>>(didx.p, n, m, dGt.p);
+  HMGP_LAUNCH_CHECK();
+  HMGP_CUDA(cudaMemcpyAsync(dGa.p, dGt.p, 8ull * n * m, cudaMemcpyDeviceToDevice, st));
+  lib.potrs(st, dLt.p, n, dGt.p, m);
+  lib.potrs(st, dLa.p, n, dGa.p, m);
+  k_loo_weights<<<m, 256, 0, st>>>(didx.p, n, dGa.p, dgd.p);
+  HMGP_LAUNCH_CHECK();
+  const double one = 1.0, zero = 0.0;  // W = C_t G_a (C_t symmetric, lower stored)
+  if (cublasDsymm(lib.bh, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, n, m, &one, dCt.p, n, dGa.p, n, &zero, dW.p,
+                  n) != CUBLAS_STATUS_SUCCESS)
+    throw Error(HMGP_ECUDA, "cublasDsymm failed");
+  k_mloe_terms<<<m, 256, 0, st>>>(didx.p, n, dGt.p, dGa.p, dW.p, dgd.p, dterms.p);
+  HMGP_LAUNCH_CHECK();
+  std::vector<double> t(2ull * m);
+  HMGP_CUDA(cudaMemcpyAsync(t.data(), dterms.p, 16ull * m, cudaMemcpyDeviceToHost, st));
+  HMGP_CUDA(cudaStreamSynchronize(st));
+  double lo = 0.0, mo = 0.0;  // summed in target order, as the reference does
+  for (int k = 0; k < m; ++k) {
+    lo += t[2 * k];
+    mo += t[2 * k + 1];
+  }
+  *mloe = lo / m;
+  *mmom = mo / m;
+}
+
+}  // namespace hmgp_gpu

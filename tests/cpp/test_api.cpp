@@ -149,6 +149,31 @@ int main() {
     const Matrix l = h_ldl(h, 1e-6).lower_dense();
     CHECK(l(0, 0) == 1.0 && l(0, 1) == 0.0);
   }
+  {  // kriging variance and MLOE/MMOM (test_krige_metrics.cpp:80-91, 137-145, 212-244)
+    const auto train = random_locations(256, 9);
+    const MaternParams p{2.0, 0.1, 1.5, 0.0};
+    std::vector<Location> test{train[17], {123.0, -55.0}};
+    const Vector var = kriging_variance_dense(train, test, p);
+    CHECK(std::abs(var[0]) <= 1e-10);
+    CHECK(std::abs(var[1] - 2.0) <= 2e-12);
+    const auto pts = random_locations(64, 20);
+    MetricConfig cfg;
+    cfg.M = 64;
+    const MaternParams t{1.5, 0.1, 0.5, 0.0};
+    const MloeMmom m = mloe_mmom(pts, t, t, cfg);
+    CHECK(std::abs(m.mloe) <= 1e-8 && std::abs(m.mmom) <= 1e-8);
+    const auto pts30 = random_locations(64, 30);
+    const MloeMmom v = mloe_mmom(pts30, t, MaternParams{0.6, 0.1, 0.5, 0.0}, cfg);
+    CHECK(std::abs(v.mloe) <= 1e-10 && std::abs(v.mmom) > 0.1);
+    MetricConfig bad;
+    bad.M = 0;
+    CHECK_THROWS_AS(mloe_mmom(random_locations(8, 1), t, t, bad), std::invalid_argument);
+    bad.M = 4;
+    bad.dense_guard = 4;
+    CHECK_THROWS_AS(mloe_mmom(random_locations(8, 1), t, t, bad), std::invalid_argument);
+    CHECK(std::abs(rmse(Vector{1, 2, 3}, Vector{0, 0, 0}) - 2.1602468994692869) <= 1e-14);
+    CHECK_THROWS_AS(rmse(Vector{1, 1}, Vector{1, 1, 1}), std::invalid_argument);
+  }
   std::printf("%s (%d failures)\n", g_fail ? "FAILED" : "ALL PASSED", g_fail);
   return g_fail ? 1 : 0;
 }
