@@ -29,3 +29,14 @@ def test_cpp_api_on_gpu(hm):
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "ALL PASSED" in r.stdout
+
+
+def test_cpp_dataset_io(hm):
+    """include/hmgp/dataset.hpp (dataset.cpp:46-210): host-only port of test_io.cpp."""
+    exe = os.path.join(ROOT, "tests", "cpp", "test_dataset")
+    lib_dir = os.path.join(ROOT, "paper_2104_07146_b200")
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "test_dataset.cpp"), "-L", lib_dir, "-lhmgp_cuda",
+                    f"-Wl,-rpath,{lib_dir}", "-o", exe], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "ALL PASSED" in r.stdout, r.stdout + r.stderr
