@@ -236,6 +236,16 @@ def run_ours(args):
                     "(hmgp_fp64_peak) on this B200; MEASURED_PEAKS.json has no FP64 entry",
                     "share_of_step": pms / (ms / args.steps),
                     "algorithmic_flops_per_launch": flops}
+        # Matérn assembly (K3 dense near-field leaves, general-ν Bessel path at C3):
+        # flop-model work of the untimed counting pass over the live K3 phase time
+        k3_ms = phases["dense_K3"]
+        k3_ach = work["kernel_flops"] / (k3_ms / 1e3) / 1e12 if k3_ms > 0 else 0.0
+        roofline_asm = {"bound": "fp64", "kernel": "dense_K3 (k_dense_leaves)", "achieved": k3_ach,
+                        "peak": fp64_peak, "unit": "TFLOP/s",
+                        "frac": k3_ach / fp64_peak if fp64_peak else None,
+                        "algorithmic_flops_per_launch": work["kernel_flops"],
+                        "entries_per_launch": work["dense_entries"],
+                        "flop_model": "per-entry Temme/Steed iteration path, exp/log/sin/sinh/cosh = 20, pow = 45"}
         line = {
             "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -250,6 +260,7 @@ def run_ours(args):
             "e2e": {"value": e2e_value, "unit": "evals/s",
                     "h2d_bytes_per_step": 8 * n * 2 + 8 * n, "d2h_bytes_per_step": C.sizeof(res)},
             "roofline": roofline,
+            "roofline_assembly": roofline_asm,
             "hbm_peak_gbs": peaks.get("hbm_gbs"),
         }
         if not args.no_extras and not args.small:

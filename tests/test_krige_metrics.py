@@ -97,7 +97,8 @@ def test_oracle_guards(oracle):
 @pytest.mark.parametrize("n,m,th,dim", [
     (256, 300, [2.0, 0.1, 1.5, 0.0], 2),
     (1000, 777, [1.3, 0.12, 0.7, 0.05], 2),      # general-ν Bessel path
-    (4096, 5000, [1.0, 0.1, 0.5, 0.01], 2),      # maximum n, two column batches
+    (4096, 300, [1.0, 0.1, 0.5, 0.01], 2),       # maximum n
+    (300, 5000, [1.0, 0.1, 1.5, 0.01], 2),       # two column batches
     (800, 200, [1.0, 0.2, 2.5, 0.005], 3),
 ])
 def test_gpu_variance_matches_oracle(hm, oracle, n, m, th, dim):
