@@ -153,6 +153,16 @@ int hmgp_factor_diagonal(hmgp_ctx* ctx, const hmgp_factor* f, double* out);
    HMatrix::to_dense (hmatrix.cpp:274-297, original order),
    HFactor::lower_dense (hfactor.cpp:421-434, tree order),
    HFactor::reconstruct (hfactor.cpp:436-449, L D L^T / L L^T, original order) */
+/* Leaf-range shard of assemble for multi-GPU assembly: the
+   DFS-ordered stored-leaf list is cut into n_shards contiguous ranges of near-equal
+   cost (dense m·n, admissible 16·(m+n); hmgp_balanced_ranges) and only range
+   `shard` is assembled — its leaves are bit-identical to a full hmgp_assemble.
+   The result is for leaf queries only (hmgp_hmat_leaves reports rank -2 outside
+   the range; matvec / factorize / to_dense refuse it). */
+int hmgp_assemble_shard(hmgp_ctx* ctx, hmgp_geom* g, const hmgp_matern* theta, const hmgp_rank_control* rc,
+                        int shard, int n_shards, hmgp_hmat** out, int* leaf_begin, int* leaf_end);
+/* bounds[0..parts]: contiguous ranges of cost[0..count) with near-equal sums (host) */
+int hmgp_balanced_ranges(const double* cost, int count, int parts, int* bounds);
 int hmgp_hmat_to_dense(hmgp_ctx* ctx, const hmgp_hmat* h, double* out);
 int hmgp_factor_lower_dense(hmgp_ctx* ctx, const hmgp_factor* f, double* out);
 int hmgp_factor_reconstruct(hmgp_ctx* ctx, const hmgp_factor* f, double* out);

@@ -127,6 +127,9 @@ _sig("hmgp_kernel_pairs", C.c_int, [_vp, _dp, C.c_int, C.c_int, C.POINTER(Matern
 _sig("hmgp_at_distance", C.c_int, [_vp, C.POINTER(Matern), _dp, C.c_int64, _dp])
 _sig("hmgp_bessel_k", C.c_int, [_vp, _dp, _dp, C.c_int64, C.c_int, _dp])
 _sig("hmgp_assemble", C.c_int, [_vp, _vp, C.POINTER(Matern), C.POINTER(_RankControl), C.POINTER(_vp)])
+_sig("hmgp_assemble_shard", C.c_int, [_vp, _vp, C.POINTER(Matern), C.POINTER(_RankControl), C.c_int, C.c_int,
+                                     C.POINTER(_vp), C.POINTER(C.c_int), C.POINTER(C.c_int)])
+_sig("hmgp_balanced_ranges", C.c_int, [_dp, C.c_int, C.c_int, _ip])
 _sig("hmgp_hmat_stats", C.c_int, [_vp, _dp, C.POINTER(C.c_int), _dp])
 _sig("hmgp_hmat_leaves", C.c_int, [_vp, _ip, C.c_int64, C.POINTER(C.c_int64)])
 _sig("hmgp_hmat_leaf_data", C.c_int, [_vp, C.c_int64, _dp, _dp])
@@ -388,13 +391,23 @@ def bessel_k(nu, x, generic=False, ctx=None):
 
 # ----------------------------------------------------------------- H-matrix
 class HMatrix:
-    def __init__(self, geom: Geometry, params, rc: RankControl):
+    def __init__(self, geom: Geometry, params, rc: RankControl, shard=None):
+        """shard=(i, n): assemble only the i-th of n cost-balanced contiguous ranges
+        of the stored-leaf list (multi-GPU assembly); leaf_range is
+        the [begin, end) this object holds payload for."""
         self.g = geom
         self.ctx = geom.ctx
         m = _mp(params)
         r = rc.c()
         h = _vp()
-        _chk(_lib.hmgp_assemble(self.ctx.h, geom.h, C.byref(m), C.byref(r), C.byref(h)))
+        if shard is None:
+            _chk(_lib.hmgp_assemble(self.ctx.h, geom.h, C.byref(m), C.byref(r), C.byref(h)))
+            self.leaf_range = None
+        else:
+            lb, le = C.c_int(), C.c_int()
+            _chk(_lib.hmgp_assemble_shard(self.ctx.h, geom.h, C.byref(m), C.byref(r), int(shard[0]),
+                                          int(shard[1]), C.byref(h), C.byref(lb), C.byref(le)))
+            self.leaf_range = (lb.value, le.value)
         self.h = h
 
     def __del__(self):
@@ -452,6 +465,19 @@ class HMatrix:
 def assemble(geom, params, rc=None):
     """hmatrix.hpp:88-89"""
     return HMatrix(geom, params, rc or RankControl.fixed_accuracy(1e-6))
+
+
+def assemble_shard(geom, params, shard, n_shards, rc=None):
+    """One GPU's share of a sharded assembly."""
+    return HMatrix(geom, params, rc or RankControl.fixed_accuracy(1e-6), shard=(shard, n_shards))
+
+
+def balanced_ranges(cost, parts):
+    """Contiguous ranges of `cost` with near-equal sums: bounds[0..parts] (host, C ABI)."""
+    c = np.ascontiguousarray(cost, dtype=np.float64)
+    b = np.empty(parts + 1, dtype=np.int32)
+    _chk(_lib.hmgp_balanced_ranges(_d(c), c.size, parts, _i(b)))
+    return b
 
 
 class HFactor:

@@ -350,8 +350,24 @@ static int lr_capacity(int m, int n, int rank) {
   return std::min(mn, want) + 16;
 }
 
+// Greedy prefix split: range p ends at the first leaf whose prefix cost reaches
+// (p+1)/parts of the total, so every range is contiguous in DFS order.
+void balanced_ranges(const double* cost, int L, int parts, int* bounds) {
+  double total = 0.0;
+  for (int k = 0; k < L; ++k) total += cost[k];
+  bounds[0] = 0;
+  double acc = 0.0;
+  int k = 0;
+  for (int q = 1; q < parts; ++q) {
+    const double target = total * q / parts;
+    while (k < L && acc + 0.5 * cost[k] < target) acc += cost[k++];
+    bounds[q] = k;
+  }
+  bounds[parts] = L;
+}
+
 void assemble(HMat& h, Geometry& g, const MaternDev& p, double eps, bool fixed_rank, int rank_k,
-              int max_rank, cudaStream_t st, double* stats) {
+              int max_rank, cudaStream_t st, double* stats, int shard, int n_shards) {
   h.g = &g;
   h.p = p;
   h.eps = eps;
@@ -364,9 +380,6 @@ void assemble(HMat& h, Geometry& g, const MaternDev& p, double eps, bool fixed_r
   const int L = static_cast<int>(h.leaf_node.size());
 
   // ---- ACA over admissible leaves, in chunks bounded by workspace size ----
-  std::vector<int> adm, den;
-  for (int k = 0; k < L; ++k)
-    (h.nodes[h.leaf_node[k]].kind == LOWRANK ? adm : den).push_back(k);
   std::vector<int> rank(L, -1);
   std::vector<int> mm(L), nn(L), r0v(L), c0v(L);
   for (int k = 0; k < L; ++k) {
@@ -376,7 +389,22 @@ void assemble(HMat& h, Geometry& g, const MaternDev& p, double eps, bool fixed_r
     mm[k] = g.nend[nd.row] - r0v[k];
     nn[k] = g.nend[nd.col] - c0v[k];
   }
+  h.leaf_begin = 0;
+  h.leaf_end = -1;
+  if (n_shards > 1) {  // cost: dense m n entries, admissible (m + n) r with r ~ 16
+    std::vector<double> cost(L);
+    for (int k = 0; k < L; ++k)
+      cost[k] = h.nodes[h.leaf_node[k]].kind == LOWRANK ? 16.0 * (mm[k] + nn[k]) : (double)mm[k] * nn[k];
+    std::vector<int> b(n_shards + 1);
+    balanced_ranges(cost.data(), L, n_shards, b.data());
+    h.leaf_begin = b[shard];
+    h.leaf_end = b[shard + 1];
+  }
+  std::vector<int> adm, den;
+  for (int k = 0; k < L; ++k)
+    if (h.in_shard(k)) (h.nodes[h.leaf_node[k]].kind == LOWRANK ? adm : den).push_back(k);
   int* d_rank_tmp = dmalloc<int>(L);
+  HMGP_CUDA(cudaMemsetAsync(d_rank_tmp, 0, (size_t)L * 4, st));
   int* d_err = dmalloc<int>(1);
   HMGP_CUDA(cudaMemsetAsync(d_err, 0, 4, st));
   // Device staging buffers per chunk; results copied into the final pool after
@@ -544,6 +572,10 @@ void assemble(HMat& h, Geometry& g, const MaternDev& p, double eps, bool fixed_r
     if (kd == LOWRANK && static_cast<long>(m + n) * rank[k] >= static_cast<long>(m) * n) kd = DENSE;
     kind[k] = kd;
     off[k] = total;
+    if (!h.in_shard(k)) {  // outside this shard: no payload
+      if (kd == LOWRANK) rank[k] = 0;
+      continue;
+    }
     if (kd == DENSE) {
       total += (size_t)m * n;
     } else {
@@ -647,7 +679,7 @@ void assemble(HMat& h, Geometry& g, const MaternDev& p, double eps, bool fixed_r
     std::vector<int> diag;
     for (int k = 0; k < L; ++k) {
       const HNode& nd = h.nodes[h.leaf_node[k]];
-      if (nd.row == nd.col && kind[k] == DENSE) diag.push_back(k);
+      if (nd.row == nd.col && kind[k] == DENSE && h.in_shard(k)) diag.push_back(k);
     }
     int* d_diag = upload(diag, st);
     double* d_out = dmalloc<double>(1);

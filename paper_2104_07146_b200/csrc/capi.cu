@@ -277,6 +277,38 @@ int hmgp_assemble(hmgp_ctx* ctx, hmgp_geom* g, const hmgp_matern* theta,
   })
 }
 
+/* leaf-range shard of assemble */
+int hmgp_assemble_shard(hmgp_ctx* ctx, hmgp_geom* g, const hmgp_matern* theta, const hmgp_rank_control* rc,
+                        int shard, int n_shards, hmgp_hmat** out, int* leaf_begin, int* leaf_end) {
+  API_GUARD({
+    hmgp_validate_matern(theta);
+    if (rc->mode == 0 && !(rc->eps > 0.0)) throw std::invalid_argument("assemble: eps must be positive");
+    if (rc->mode == 1 && rc->rank < 1) throw std::invalid_argument("assemble: fixed rank must be >= 1");
+    if (n_shards < 1 || shard < 0 || shard >= n_shards)
+      throw std::invalid_argument("assemble_shard: need 0 <= shard < n_shards");
+    HMGP_CUDA(cudaSetDevice(ctx->device));
+    auto h = new hmgp_hmat();
+    try {
+      assemble(h->h, g->g, make_matern(theta->sigma2, theta->ell, theta->nu, theta->tau2), rc->eps,
+               rc->mode == 1, rc->rank, rc->max_rank > 0 ? rc->max_rank : 256, ctx->stream, nullptr, shard,
+               n_shards);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    if (leaf_begin) *leaf_begin = h->h.leaf_begin;
+    if (leaf_end) *leaf_end = h->h.leaf_end < 0 ? (int)h->h.leaf.size() : h->h.leaf_end;
+    *out = h;
+  })
+}
+
+int hmgp_balanced_ranges(const double* cost, int count, int parts, int* bounds) {
+  API_GUARD({
+    if (count < 0 || parts < 1) throw std::invalid_argument("balanced_ranges: count >= 0, parts >= 1");
+    balanced_ranges(cost, count, parts, bounds);
+  })
+}
+
 int hmgp_hmat_stats(const hmgp_hmat* hm, double* bytes, int* max_rank, double* max_diag) {
   API_GUARD({
     const HMat& h = hm->h;
@@ -310,7 +342,7 @@ int hmgp_hmat_leaves(const hmgp_hmat* hm, int32_t* out6, int64_t cap, int64_t* c
       out6[6 * k + 2] = G.nbeg[nd.col];
       out6[6 * k + 3] = G.nend[nd.col];
       out6[6 * k + 4] = h.leaf[k].kind;
-      out6[6 * k + 5] = h.leaf[k].kind == LOWRANK ? h.rank_host[k] : -1;
+      out6[6 * k + 5] = !h.in_shard((int)k) ? -2 : h.leaf[k].kind == LOWRANK ? h.rank_host[k] : -1;
     }
   })
 }
@@ -319,6 +351,7 @@ int hmgp_hmat_leaf_data(const hmgp_hmat* hm, int64_t k, double* a, double* b) {
   API_GUARD({
     const HMat& h = hm->h;
     if (k < 0 || k >= (int64_t)h.leaf.size()) throw std::out_of_range("leaf index");
+    if (!h.in_shard((int)k)) throw std::out_of_range("leaf outside this shard's leaf range");
     const LeafDev& l = h.leaf[k];
     if (l.kind == DENSE) {
       HMGP_CUDA(cudaMemcpy(a, l.a, 8ull * l.m * l.n, cudaMemcpyDeviceToHost));
@@ -333,6 +366,7 @@ int hmgp_hmat_leaf_data(const hmgp_hmat* hm, int64_t k, double* a, double* b) {
 int hmgp_hmat_matvec(hmgp_ctx* ctx, const hmgp_hmat* hm, const double* x, double* y) {
   API_GUARD({
     HMGP_CUDA(cudaSetDevice(ctx->device));
+    if (hm->h.partial()) throw std::invalid_argument("matvec: H-matrix is a leaf-range shard");
     hmat_matvec(ctx->stream, hm->h, x, y);
   })
 }

@@ -85,12 +85,21 @@ struct HMat {
   size_t pool_doubles = 0;
   double max_diag = 0.0;
   int n_dense_leaves = 0, n_lr_leaves = 0;
+  // leaf-range shard: only stored leaves [leaf_begin, leaf_end)
+  // carry payload; a partial H-matrix is refused by matvec / factorize / to_dense
+  int leaf_begin = 0, leaf_end = -1;
+  bool partial() const { return leaf_begin != 0 || (leaf_end >= 0 && leaf_end != (int)leaf.size()); }
+  bool in_shard(int k) const { return k >= leaf_begin && (leaf_end < 0 || k < leaf_end); }
   ~HMat();
 };
 
 // Assembly (K3 dense leaves, K4 batched ACA + K5 truncation), hmatrix.cpp:174-221.
+// shard/n_shards > 1: assemble only the shard-th of n_shards contiguous,
+// cost-balanced ranges of the DFS-ordered stored-leaf list (balanced_ranges).
 void assemble(HMat& h, Geometry& g, const MaternDev& p, double eps, bool fixed_rank, int rank_k,
-              int max_rank, cudaStream_t st, double* stats);
+              int max_rank, cudaStream_t st, double* stats, int shard = 0, int n_shards = 1);
+// bounds[0..parts]: contiguous ranges of cost[0..L) with near-equal sums
+void balanced_ranges(const double* cost, int L, int parts, int* bounds);
 
 MaternDev make_matern(double sigma2, double ell, double nu, double tau2);
 

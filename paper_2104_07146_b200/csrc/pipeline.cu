@@ -177,6 +177,7 @@ extern "C" {
 int hmgp_factorize(hmgp_ctx* ctx, hmgp_hmat* h, double eps_f, int form, hmgp_factor** out,
                    hmgp_factor_info* info) {
   API_GUARD2({
+    if (h->h.partial()) throw std::invalid_argument("factorize: H-matrix is a leaf-range shard");
     HMGP_CUDA(cudaSetDevice(ctx->device));
     auto f = do_factorize(h->h, eps_f, form == 1, ctx->stream);
     if (info) {
@@ -235,6 +236,7 @@ int hmgp_factor_diagonal(hmgp_ctx* ctx, const hmgp_factor* f, double* out) {
 
 int hmgp_hmat_to_dense(hmgp_ctx* ctx, const hmgp_hmat* h, double* out) {
   API_GUARD2({
+    if (h->h.partial()) throw std::invalid_argument("to_dense: H-matrix is a leaf-range shard");
     HMGP_CUDA(cudaSetDevice(ctx->device));
     hmat_to_dense(ctx->stream, h->h, out);
   })

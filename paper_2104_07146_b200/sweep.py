@@ -75,3 +75,47 @@ def run_sweep(geom, d_z_ptr, thetas, idx, cfg, ctx):
     c = cfg.c()
     _chk(_lib.hmgp_loglik_batch(ctx.h, geom.h, C.c_void_p(d_z_ptr), arr, len(idx), C.byref(c), res))
     return np.array([[r.loglik, r.logdet, r.quad_form, r.status] for r in res])
+
+
+# ------------------------------------------------ kriging and assembly shards
+def predict_ranges(m, world):
+    """Contiguous [begin, end) of the m new locations per rank (SURVEY.md §8e:
+    every GPU factors C̃₁₁ itself — a replica — and predicts m/G points)."""
+    b = [(m * r) // world for r in range(world + 1)]
+    return [(b[r], b[r + 1]) for r in range(world)]
+
+
+def predict_sharded(train, z1, new_locations, theta, cfg=None, dist=None, device=None, predictor=None):
+    """Sharded predict (krige.cpp:9-44): this rank predicts its contiguous slice,
+    one all-gather (NCCL on GPUs, gloo in the CPU tests) assembles the m values in
+    order on every rank."""
+    import torch
+    x2 = np.ascontiguousarray(new_locations, dtype=np.float64)
+    m = x2.shape[0]
+    ws = dist.get_world_size() if dist is not None and dist.is_initialized() else 1
+    rk = dist.get_rank() if ws > 1 else 0
+    lo, hi = predict_ranges(m, ws)[rk]
+    run = predictor
+    if run is None:
+        from . import predict
+        run = lambda te: predict(train, z1, te, theta, cfg).z2_hat  # noqa: E731
+    local = np.asarray(run(x2[lo:hi]), dtype=np.float64) if hi > lo else np.empty(0)
+    if ws == 1:
+        return local
+    cap = (m + ws - 1) // ws
+    buf = np.zeros(cap)
+    buf[: hi - lo] = local
+    t = torch.from_numpy(buf).to(device or "cpu")
+    outs = [torch.empty_like(t) for _ in range(ws)]
+    dist.all_gather(outs, t)
+    parts = [o.cpu().numpy()[: e - b] for o, (b, e) in zip(outs, predict_ranges(m, ws))]
+    return np.concatenate(parts)
+
+
+def assemble_sharded(geom, theta, rc=None, dist=None):
+    """Sharded assembly (C2): this rank assembles its cost-balanced contiguous
+    range of the stored-leaf list (no data-path collective; payloads stay local)."""
+    from . import assemble_shard
+    ws = dist.get_world_size() if dist is not None and dist.is_initialized() else 1
+    rk = dist.get_rank() if ws > 1 else 0
+    return assemble_shard(geom, theta, rk, ws, rc)

@@ -87,3 +87,57 @@ def test_gather_world2_gloo_matches_serial():
     k, th, L = sw.argmax_theta(g, table)
     assert th[2] != 0.3  # failed probes (status -1) never win
     assert L == np.max(np.where(serial[:, 3] >= 0, serial[:, 0], -np.inf))
+
+
+def _predict_worker(rank, world, port, m, out):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sw = _import_sweep()
+    x2 = np.random.default_rng(3).random((m, 2))
+    # stand-in predictor (the GPU path calls hmgp_predict on this rank's slice)
+    got = sw.predict_sharded(None, None, x2, None, dist=dist,
+                             predictor=lambda te: np.sin(7 * te[:, 0]) + te[:, 1] ** 2)
+    out.put((rank, got))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(180)
+@pytest.mark.parametrize("m", [10000, 3])
+def test_predict_sharded_world2_gloo(m):
+    """Kriging shards: contiguous m/G slices, one all-gather, every
+    rank ends with all m predictions in order (m = 3: ragged slices)."""
+    sw = _import_sweep()
+    for world in (1, 2, 3, 8):
+        r = sw.predict_ranges(m, world)
+        assert r[0][0] == 0 and r[-1][1] == m and all(a[1] == b[0] for a, b in zip(r, r[1:]))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_predict_worker, args=(rk, 2, port, m, q)) for rk in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=150) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    x2 = np.random.default_rng(3).random((m, 2))
+    want = np.sin(7 * x2[:, 0]) + x2[:, 1] ** 2
+    for rk in range(2):
+        assert np.array_equal(res[rk], want)
+
+
+def test_balanced_leaf_ranges(hm):
+    """Assembly shards: contiguous, covering, near-equal cost."""
+    rng = np.random.default_rng(0)
+    cost = np.where(rng.random(5000) < 0.25, 64.0 * 64, 16.0 * 128)  # dense / admissible mix
+    for parts in (1, 2, 4, 8):
+        b = hm.balanced_ranges(cost, parts)
+        assert b[0] == 0 and b[-1] == cost.size and np.all(np.diff(b) >= 0)
+        sums = np.array([cost[b[i]:b[i + 1]].sum() for i in range(parts)])
+        assert sums.max() - sums.min() <= 2 * cost.max()
+    b = hm.balanced_ranges(np.ones(3), 8)  # more parts than leaves: empty ranges allowed
+    assert b[0] == 0 and b[-1] == 3 and np.all(np.diff(b) >= 0)
+    assert hm.balanced_ranges(np.empty(0), 2).tolist() == [0, 0, 0]
