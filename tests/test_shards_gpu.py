@@ -25,8 +25,10 @@ def _check_shards(hm, x, leaf, eps, th, worlds, data=True):
             prev_end = le
             covered[lb:le] += 1
             sl = h.leaves()
-            assert np.array_equal(sl[:, :5], fl[:, :5])            # same structure
-            assert np.array_equal(sl[lb:le, 5], fl[lb:le, 5])      # same ranks in range
+            assert np.array_equal(sl[:, :4], fl[:, :4])            # same block structure
+            # in range: same kind (incl. rank-driven coarsening to dense) and rank;
+            # outside, the kind is the structural one (no rank, no coarsening)
+            assert np.array_equal(sl[lb:le, 4:], fl[lb:le, 4:])
             assert np.all(sl[:lb, 5] == -2) and np.all(sl[le:, 5] == -2)
             if data:
                 for k in range(lb, le):
