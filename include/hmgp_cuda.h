@@ -224,7 +224,7 @@ int hmgp_kriging_variance_dense(hmgp_ctx* ctx, const double* train, int n, int d
                                 const hmgp_matern* theta, double* out);
 /* mloe_mmom(locations, theta_true, theta_approx, MetricConfig{M, seed, dense_guard})
    (metrics.hpp:24-31 / metrics.cpp:17-69): leave-one-out kriging MLOE / MMOM closed
-   forms, dense FP64 on device, n <= min(dense_guard, 4096).  Host buffers. */
+   forms, dense FP64 on device, n <= min(dense_guard, 32768).  Host buffers. */
 int hmgp_mloe_mmom(hmgp_ctx* ctx, const double* coords, int n, int dim, const hmgp_matern* theta_true,
                    const hmgp_matern* theta_approx, int M, uint64_t seed, int dense_guard, double* mloe,
                    double* mmom);

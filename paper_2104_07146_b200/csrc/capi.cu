@@ -447,7 +447,9 @@ int hmgp_mloe_mmom(hmgp_ctx* ctx, const double* coords, int n, int dim, const hm
     if (n < 2) throw std::invalid_argument("mloe_mmom: need at least 2 locations");
     if (n > dense_guard)
       throw std::invalid_argument("mloe_mmom: dense evaluation capped at n = " + std::to_string(dense_guard));
-    if (n > 4096) throw std::invalid_argument("mloe_mmom: dense evaluation capped at n = 4096");
+    // the reference allows any dense_guard; three n x n FP64 matrices must fit the
+    // device and the 32-bit cuSOLVER API
+    if (n > 32768) throw std::invalid_argument("mloe_mmom: dense evaluation refused beyond n = 32768");
     if (M < 1) throw std::invalid_argument("mloe_mmom: M must be >= 1");
     const int m = std::min(M, n);
     // M distinct targets by a seeded partial Fisher-Yates (metrics.cpp:30-36)

@@ -195,3 +195,18 @@ def test_rmse_hand_values(hm):
         hm.rmse([1, 1], [1, 2, 3])
     with pytest.raises(ValueError):
         hm.rmse([], [])
+
+
+@pytest.mark.gpu
+def test_gpu_mloe_beyond_4096_with_guard(hm, oracle):
+    """dense_guard above the default (metrics.hpp:16): n = 6000, size-independent
+    properties (matching models -> 0; pure σ² misspecification -> MLOE 0)."""
+    x = oracle.random_locations(6000, 77)
+    t = [1.0, 0.1, 0.5, 0.01]
+    cfg = hm.MetricConfig(M=200, seed=1, dense_guard=8192)
+    r = hm.mloe_mmom(x, t, t, cfg)
+    assert abs(r.mloe) <= 1e-8 and abs(r.mmom) <= 1e-8
+    r = hm.mloe_mmom(x, t, [0.5, 0.1, 0.5, 0.005], cfg)  # (σ², τ²) scaled together
+    assert abs(r.mloe) <= 1e-8 and r.mmom == pytest.approx(-0.5, rel=1e-8)
+    with pytest.raises(ValueError):
+        hm.mloe_mmom(x, t, t, hm.MetricConfig(M=10))  # default guard 4096
