@@ -2340,6 +2340,15 @@ Factor::~Factor() {
   cudaFree(d_part);
 }
 
+// Capacities (TCAP, low-rank column growth) of the last factorization that
+// succeeded on this thread, keyed by the block structure: the next evaluation on
+// the same structure (a θ-sweep, repeated L(θ)) starts there instead of repeating
+// a failed attempt.  Capacities never change results, only memory and retries.
+struct CapMemo {
+  int n = -1, dim = 0, leaves = -1, tcap = 256, grow = 1;
+};
+static thread_local CapMemo t_cap_memo;
+
 void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size_t arena_bytes) {
   const Geometry& G = *H.g;
   F.g = H.g;
@@ -2363,7 +2372,17 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
   // A low-rank block whose rank outgrows its column capacity, or a product wider
   // than TCAP, is detected on device; the factorization is then redone with
   // doubled capacities (results do not depend on the capacities that succeed).
-  int grow = 1;
+  int grow = 1, tcap0 = 256;
+  // 3-D admissible blocks carry ranks up to ~256 and their updates outgrow the
+  // 2-D starting capacities (C5-shaped n = 262144: one full failed attempt)
+  if (G.dim == 3) {
+    grow = 2;
+    tcap0 = 512;
+  }
+  if (t_cap_memo.n == G.n && t_cap_memo.dim == G.dim && t_cap_memo.leaves == L) {
+    grow = std::max(grow, t_cap_memo.grow);
+    tcap0 = std::max(tcap0, t_cap_memo.tcap);
+  }
   size_t pool_doubles = 0;
   // task flow (dag.h) on request (HMGP_DAG=1, or HMGP_DAG_DIAG for its critical-path
   // report).  Measured at C3 its DAG critical path is within 1.33x of the serial
@@ -2371,7 +2390,7 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
   // off by default.
   bool use_dag = getenv("HMGP_STATS") == nullptr && getenv("HMGP_SERIAL") == nullptr &&
                  ((getenv("HMGP_DAG") && atoi(getenv("HMGP_DAG")) != 0) || getenv("HMGP_DAG_DIAG"));
-  for (int tcap = 256;;) {
+  for (int tcap = tcap0;;) {
     // clone payload (hblock.cpp:17-28) into the factor's own layout; compact_cols = 0
     F.leaf = H.leaf;
     size_t total = 0;
@@ -2483,7 +2502,10 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
       use_dag = false;
       continue;
     }
-    if (!err) break;
+    if (!err) {
+      t_cap_memo = CapMemo{G.n, G.dim, L, tcap, grow};
+      break;
+    }
     if (tcap >= 1024 && grow >= 16)
       throw Error(6, "factorize: low-rank capacity exceeded (code " + std::to_string(err) + ")");
     tcap = std::min(1024, tcap * 2);
