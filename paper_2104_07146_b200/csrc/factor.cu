@@ -41,6 +41,7 @@ namespace cg = cooperative_groups;
 // ------------------------------------------------------------ utilities ---
 extern thread_local bool t_one_stream;
 constexpr int kSubArenaFull = 1007;  // internal: task-flow sub-arenas too small -> serial redo
+constexpr int kArenaFull = 1008;     // internal: arena too small with side streams -> one-stream redo
 
 struct Arena {
   char* base = nullptr;
@@ -100,7 +101,7 @@ struct Arena {
   void* raw(size_t bytes) {
     if (K == 1) {
       const size_t a = (top + 255) & ~size_t(255);
-      if (a + bytes > cap) throw Error(6, "factorize: device temporary arena exhausted");
+      if (a + bytes > cap) throw Error(kArenaFull, "factorize: device temporary arena exhausted");
       top = a + bytes;
       peak = std::max(peak, top);
       total += bytes;
@@ -2375,15 +2376,28 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
   int grow = 1, tcap0 = 256;
   // 3-D admissible blocks carry ranks up to ~256 and their updates outgrow the
   // 2-D starting capacities (C5-shaped n = 262144: one full failed attempt)
+  bool start_3d = false;  // heuristic start, dropped if its pool does not fit
   if (G.dim == 3) {
     grow = 2;
     tcap0 = 512;
+    start_3d = true;
   }
   if (t_cap_memo.n == G.n && t_cap_memo.dim == G.dim && t_cap_memo.leaves == L) {
+    start_3d = false;
     grow = std::max(grow, t_cap_memo.grow);
     tcap0 = std::max(tcap0, t_cap_memo.tcap);
   }
   size_t pool_doubles = 0;
+  struct OneStreamScope {  // restores t_one_stream when factorize leaves
+    bool on = false;
+    void engage() {
+      on = true;
+      t_one_stream = true;
+    }
+    ~OneStreamScope() {
+      if (on) t_one_stream = false;
+    }
+  } one_stream;
   // task flow (dag.h) on request (HMGP_DAG=1, or HMGP_DAG_DIAG for its critical-path
   // report).  Measured at C3 its DAG critical path is within 1.33x of the serial
   // sum and it does not beat the in-order stream + sections schedule, so it is
@@ -2414,7 +2428,17 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
         cudaGetLastError();
         F.pool = nullptr;
         release_thread_workspace();
-        HMGP_CUDA(cudaMalloc(&F.pool, std::max<size_t>(1, total) * 8));
+        if (start_3d && cudaMalloc(&F.pool, std::max<size_t>(1, total) * 8) != cudaSuccess) {
+          // the doubled 3-D start does not fit: fall back to the 2-D start
+          cudaGetLastError();
+          F.pool = nullptr;
+          start_3d = false;
+          grow = 1;
+          tcap = 256;
+          pool_doubles = 0;
+          continue;
+        }
+        if (!F.pool) HMGP_CUDA(cudaMalloc(&F.pool, std::max<size_t>(1, total) * 8));
       }
       pool_doubles = total;
     }
@@ -2494,9 +2518,18 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
       g_work.arena_peak = std::max(g_work.arena_peak, (double)E.ar.peak);
       g_work.factor_attempts += 1;
     } catch (const Error& e) {
-      if (e.code != kSubArenaFull) throw;
-      HMGP_CUDA(cudaDeviceSynchronize());
-      redo_serial = true;
+      if (e.code == kArenaFull) {
+        // side-stream sections hold their temporaries until the join; on one
+        // stream the arena is reused step by step (lower peak).  Redo once there.
+        if (t_one_stream) throw Error(6, e.what());
+        HMGP_CUDA(cudaDeviceSynchronize());
+        one_stream.engage();
+        redo_serial = true;
+      } else {
+        if (e.code != kSubArenaFull) throw;
+        HMGP_CUDA(cudaDeviceSynchronize());
+        redo_serial = true;
+      }
     }
     if (redo_serial) {  // task-flow sub-arenas too small: redo in program order
       use_dag = false;
