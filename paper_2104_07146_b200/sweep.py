@@ -94,6 +94,8 @@ def predict_sharded(train, z1, new_locations, theta, cfg=None, dist=None, device
     m = x2.shape[0]
     ws = dist.get_world_size() if dist is not None and dist.is_initialized() else 1
     rk = dist.get_rank() if ws > 1 else 0
+    if m == 0:
+        return np.empty(0)
     lo, hi = predict_ranges(m, ws)[rk]
     run = predictor
     if run is None:
