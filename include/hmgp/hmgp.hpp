@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdint>
 #include <memory>
+#include <utility>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -238,6 +239,18 @@ class HMatrix {  // hmatrix.hpp:44-83
     detail::check(hmgp_assemble(detail::context(), bt.handle(), &m, &r, &h));
     h_.reset(h, hmgp_hmat_destroy);
   }
+  // one GPU's share of a sharded assembly: stored leaves
+  // [leaf_range().first, leaf_range().second) only; leaf queries only
+  HMatrix(const BlockClusterTree& bt, const MaternParams& p, const RankControl& rc, int shard, int n_shards)
+      : n_(bt.rows().size()) {
+    const hmgp_matern m = p.c();
+    const hmgp_rank_control r = rc.c();
+    hmgp_hmat* h = nullptr;
+    detail::check(hmgp_assemble_shard(detail::context(), bt.handle(), &m, &r, shard, n_shards, &h,
+                                      &range_.first, &range_.second));
+    h_.reset(h, hmgp_hmat_destroy);
+  }
+  std::pair<int, int> leaf_range() const { return range_; }  // (0, -1): the whole matrix
   int rows() const { return n_; }
   int cols() const { return n_; }
   bool symmetric() const { return true; }
@@ -276,8 +289,15 @@ class HMatrix {  // hmatrix.hpp:44-83
 
  private:
   int n_;
+  std::pair<int, int> range_{0, -1};
   std::shared_ptr<hmgp_hmat> h_;
 };
+
+inline HMatrix assemble_shard(const BlockClusterTree& block_tree, const MaternParams& params,
+                              const RankControl& rc, int shard, int n_shards) {
+  params.validate();
+  return HMatrix(block_tree, params, rc, shard, n_shards);
+}
 
 inline HMatrix assemble(const BlockClusterTree& block_tree, std::span<const Location>,
                         const MaternParams& params, const RankControl& rc, int threads = 1) {

@@ -174,6 +174,17 @@ int main() {
     CHECK(std::abs(rmse(Vector{1, 2, 3}, Vector{0, 0, 0}) - 2.1602468994692869) <= 1e-14);
     CHECK_THROWS_AS(rmse(Vector{1, 1}, Vector{1, 1, 1}), std::invalid_argument);
   }
+  {  // sharded assembly: contiguous ranges, shards refuse matvec
+    const auto pts = random_locations(2000, 8);
+    ClusterTree t(pts, 32);
+    BlockClusterTree b(t, t, 2.0);
+    const MaternParams p{1.0, 0.1, 0.5, 0.01};
+    const HMatrix s0 = assemble_shard(b, p, RankControl::fixed_accuracy(1e-6), 0, 2);
+    const HMatrix s1 = assemble_shard(b, p, RankControl::fixed_accuracy(1e-6), 1, 2);
+    CHECK(s0.leaf_range().first == 0 && s0.leaf_range().second == s1.leaf_range().first);
+    CHECK(s1.leaf_range().second > s1.leaf_range().first);
+    CHECK_THROWS_AS(s0.matvec(Vector(2000, 1.0)), std::invalid_argument);
+  }
   std::printf("%s (%d failures)\n", g_fail ? "FAILED" : "ALL PASSED", g_fail);
   return g_fail ? 1 : 0;
 }
