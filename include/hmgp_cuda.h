@@ -111,6 +111,10 @@ int hmgp_geometry_clusters(const hmgp_geom* g, int32_t* out4, double* box6, int 
 int hmgp_geometry_block_count(const hmgp_geom* g, int64_t* count, int* n_admissible,
                               int* n_dense);
 int hmgp_geometry_blocks(const hmgp_geom* g, hmgp_block* out, int64_t cap);
+/* BlockClusterTree(rows, cols, eta) for two different cluster trees (geometry.cpp:100-154,
+ * geometry.hpp:76): leaves in DFS order; out == NULL returns the count only */
+int hmgp_block_tree_rect(hmgp_ctx* ctx, const hmgp_geom* rows, const hmgp_geom* cols, double eta,
+                         hmgp_block* out, int64_t cap, int64_t* count, int* n_adm, int* n_dense);
 void hmgp_geometry_destroy(hmgp_geom* g);
 
 /* -------------------------------------------------------------- kernel --- */

@@ -209,6 +209,26 @@ int hmgp_geometry_blocks(const hmgp_geom* g, hmgp_block* out, int64_t cap) {
   })
 }
 
+int hmgp_block_tree_rect(hmgp_ctx* ctx, const hmgp_geom* rows, const hmgp_geom* cols, double eta,
+                         hmgp_block* out, int64_t cap, int64_t* count, int* n_adm, int* n_dense) {
+  API_GUARD({
+    if (!(eta > 0.0)) throw std::invalid_argument("eta must be positive");  // geometry.cpp:103
+    HMGP_CUDA(cudaSetDevice(ctx->device));
+    std::vector<int> b5;
+    int na = 0, nd = 0;
+    block_tree_rect(rows->g, cols->g, eta, b5, na, nd, ctx->stream);
+    const int64_t cnt = (int64_t)(b5.size() / 5);
+    *count = cnt;
+    if (n_adm) *n_adm = na;
+    if (n_dense) *n_dense = nd;
+    if (out) {
+      if (cnt > cap) throw std::out_of_range("hmgp_block_tree_rect: cap");
+      for (int64_t k = 0; k < cnt; ++k)
+        out[k] = hmgp_block{b5[5 * k], b5[5 * k + 1], b5[5 * k + 2], b5[5 * k + 3], b5[5 * k + 4]};
+    }
+  })
+}
+
 void hmgp_geometry_destroy(hmgp_geom* g) {
   if (!g) return;
   geometry_free(g->g);

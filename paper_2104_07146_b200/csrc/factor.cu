@@ -427,9 +427,7 @@ struct Engine {
     int tiles = 1;
     for (auto& g : v) {
       const int t = ((g.M.v + 63) / 64) * ((g.N.v + 63) / 64);
-      // accumulate-mode items with a long K get split-K CTAs (linalg.cu)
-      const int ks = g.atomic != 2 ? std::min(32, std::max(1, (g.K.v + 511) / 512)) : 1;
-      tiles = std::max(tiles, std::min(128, t * ks));
+      tiles = std::max(tiles, std::min(128, t));
     }
     acc_all(v);
     const char* lab = "gemm";
@@ -913,25 +911,41 @@ struct Engine {
   }
 
   // y += alpha op(B) x for a list of (B, x, y); every H-block is flattened to
-  // its leaves, so any block costs three launches: dense leaves, and the two
-  // low-rank stages.  Leaves of one block may share y rows -> FP64 atomics.
+  // its leaves, so any block costs a fixed number of launches: dense leaves,
+  // the two low-rank stages and one ordered add.  Leaves of a branch share y
+  // rows: each writes its own temporary, and k_ordered_add applies them to y in
+  // the reference's DFS leaf order (hblock.cpp:46-60) — no FP64 atomics, so the
+  // result is bit-reproducible.  Long contractions V^T x (K >= 2048) are split
+  // into K-range items on separate slabs summed in a fixed order.
   void apply(const std::vector<Ap>& its0) {
     if (its0.empty()) return;
     site = "apply";
+    const size_t mk = ar.mark();
     std::vector<Ap> its;
-    std::vector<int> shared;
-    for (const Ap& a : its0) {
+    std::vector<int> grp;  // index into its0 for branch leaves, -1 otherwise
+    for (size_t q = 0; q < its0.size(); ++q) {
+      const Ap& a = its0[q];
       const size_t before = its.size();
       flatten(a, its);
-      for (size_t i = before; i < its.size(); ++i) shared.push_back(kind(a.b) == BRANCH);
+      for (size_t i = before; i < its.size(); ++i) grp.push_back(kind(a.b) == BRANCH ? (int)q : -1);
     }
+    // branch leaves: redirect y to a private temporary (alpha applied in the ordered add)
+    std::vector<OrdSeg> seg(its.size(), OrdSeg{nullptr, 0, 0});
+    for (size_t i = 0; i < its.size(); ++i) {
+      if (grp[i] < 0) continue;
+      Ap& a = its[i];
+      const MV t = temp(a.y.rows, a.y.cols);
+      seg[i] = OrdSeg{t.p, t.ld, (int)(a.y.p - its0[grp[i]].y.p)};
+      a.y.p = t.p;
+      a.y.ld = t.ld;
+      a.alpha = 1.0;
+    }
+    auto own = [&](size_t i) { return grp[i] >= 0; };  // y is a private temporary: overwrite
     std::vector<GemmItem> g;
-    std::vector<Ap> lr, br;
-    std::vector<int> lr_shared;
+    std::vector<size_t> lr;
     for (size_t ii = 0; ii < its.size(); ++ii) {
       const Ap& a = its[ii];
-      const int k = kind(a.b);
-      if (k == DENSE) {
+      if (kind(a.b) == DENSE) {
         const LeafDev& l = LF(a.b);
         GemmItem gi{};
         gi.A = l.a;
@@ -946,67 +960,115 @@ struct Engine {
         gi.N = a.x.cols;
         gi.K = dimv(a.trans ? l.m : l.n);
         gi.alpha = a.alpha;
-        gi.atomic = shared[ii];
+        gi.atomic = own(ii) ? 2 : 0;
         g.push_back(gi);
       } else {
-        lr.push_back(a);
-        lr_shared.push_back(shared[ii]);
+        lr.push_back(ii);
       }
     }
     gemm(g);
     if (!lr.empty()) {
-      const size_t mk = ar.mark();
       std::vector<MV> T;
-      for (const Ap& a : lr) {
-        const LeafDev& l = LF(a.b);
-        T.push_back(temp(l.cap, a.x.cols));
-      }
-      std::vector<CopyScaleItem> zf;
-      for (size_t i = 0; i < lr.size(); ++i) {  // T = (trans ? U : V)^T x   (rank x c)
-        const Ap& a = lr[i];
+      std::vector<SlabSumItem> ss;
+      for (size_t i : lr) {  // T = (trans ? U : V)^T x   (rank x c)
+        const Ap& a = its[i];
         const LeafDev& l = LF(a.b);
         const int kk = a.trans ? l.m : l.n;
-        // long contractions are split over CTAs (accumulate into a zeroed T)
-        const bool split = kk >= 2048;
-        if (split) zf.push_back(cpy(nullptr, 0, T[i], a.x.cols, 0, 0.0, nullptr, 0));
-        GemmItem gi{};
-        gi.A = a.trans ? l.a : l.b;
-        gi.lda = a.trans ? l.m : l.n;
-        gi.ta = 1;
-        gi.B = a.x.p;
-        gi.ldb = a.x.ld;
-        gi.C = T[i].p;
-        gi.ldc = T[i].ld;
-        gi.M = dimp(rankp(a.b), l.cap);
-        gi.N = a.x.cols;
-        gi.K = dimv(a.trans ? l.m : l.n);
-        gi.alpha = 1.0;
-        gi.atomic = split ? 1 : 2;  // T is this item's own: overwrite (no zero fill) unless split
-        g.push_back(gi);
+        const int ns = kk >= 2048 ? std::min(32, (kk + 1023) / 1024) : 1;
+        const int kc = (kk + ns - 1) / ns;
+        MV t = temp(l.cap, Dim{a.x.cols.v * ns, nullptr});
+        t.cols = a.x.cols;
+        T.push_back(t);
+        const size_t slab = (size_t)t.ld * std::max(a.x.cols.v, 1);
+        for (int s = 0; s < ns; ++s) {
+          const int k0 = s * kc, k1 = std::min(kk, k0 + kc);
+          GemmItem gi{};
+          gi.A = (a.trans ? l.a : l.b) + k0;
+          gi.lda = kk;
+          gi.ta = 1;
+          gi.B = a.x.p + k0;
+          gi.ldb = a.x.ld;
+          gi.C = t.p + s * slab;
+          gi.ldc = t.ld;
+          gi.M = dimp(rankp(a.b), l.cap);
+          gi.N = a.x.cols;
+          gi.K = dimv(k1 - k0);
+          gi.alpha = 1.0;
+          gi.atomic = 2;  // every slab is written by exactly one item
+          g.push_back(gi);
+        }
+        if (ns > 1) ss.push_back(SlabSumItem{t.p, t.ld, dimp(rankp(a.b), l.cap), a.x.cols, ns, slab});
       }
-      for (CopyScaleItem& z : zf) z.mode = 0;
-      copy(zf);
       gemm(g);
-      for (size_t i = 0; i < lr.size(); ++i) {  // y += alpha (trans ? V : U) T
-        const Ap& a = lr[i];
+      if (!ss.empty()) {
+        int mx = 1;
+        for (auto& x : ss) mx = std::max(mx, x.rows.v * x.cols.v);
+        for (auto& x : ss) A(x.p, 1);
+        run("slab-sum", [&](cudaStream_t s) { launch_slab_sum(sg.put(ss), (int)ss.size(), mx, s); });
+        stat(S_COPY, ss.size());
+      }
+      for (size_t q = 0; q < lr.size(); ++q) {  // y += alpha (trans ? V : U) T
+        const Ap& a = its[lr[q]];
         const LeafDev& l = LF(a.b);
         GemmItem gi{};
         gi.A = a.trans ? l.b : l.a;
         gi.lda = a.trans ? l.n : l.m;
-        gi.B = T[i].p;
-        gi.ldb = T[i].ld;
+        gi.B = T[q].p;
+        gi.ldb = T[q].ld;
         gi.C = a.y.p;
         gi.ldc = a.y.ld;
         gi.M = dimv(a.trans ? l.n : l.m);
         gi.N = a.x.cols;
         gi.K = dimp(rankp(a.b), l.cap);
         gi.alpha = a.alpha;
-        gi.atomic = lr_shared[i];
+        gi.atomic = own(lr[q]) ? 2 : 0;
         g.push_back(gi);
       }
       gemm(g);
-      ar.release(mk);
     }
+    // ordered application of the branch leaves' temporaries
+    std::vector<OrdIv> iv;
+    std::vector<OrdSeg> sl;
+    int mx = 1;
+    for (size_t q = 0; q < its0.size(); ++q) {
+      if (kind(its0[q].b) != BRANCH) continue;
+      std::vector<size_t> mine;
+      std::vector<int> cut;
+      for (size_t i = 0; i < its.size(); ++i)
+        if (grp[i] == (int)q) {
+          mine.push_back(i);
+          cut.push_back(seg[i].r0);
+          cut.push_back(seg[i].r0 + its[i].y.rows);
+        }
+      if (mine.empty()) continue;
+      std::sort(cut.begin(), cut.end());
+      cut.erase(std::unique(cut.begin(), cut.end()), cut.end());
+      std::vector<std::vector<int>> lists(cut.size());
+      for (size_t i : mine) {  // DFS order is the order of `mine`
+        const int a0 = (int)(std::lower_bound(cut.begin(), cut.end(), seg[i].r0) - cut.begin());
+        const int a1 = (int)(std::lower_bound(cut.begin(), cut.end(), seg[i].r0 + its[i].y.rows) - cut.begin());
+        for (int k = a0; k < a1; ++k) lists[k].push_back((int)i);
+      }
+      const Ap& root = its0[q];
+      for (size_t k = 0; k + 1 < cut.size(); ++k) {
+        if (lists[k].empty()) continue;
+        OrdIv v{root.y.p, root.y.ld, root.x.cols, root.alpha, cut[k], cut[k + 1], (int)sl.size(), 0};
+        for (int i : lists[k]) sl.push_back(seg[i]);
+        v.l1 = (int)sl.size();
+        iv.push_back(v);
+        mx = std::max(mx, (cut[k + 1] - cut[k]) * root.x.cols.v);
+        A(root.y.p, 1);
+      }
+      for (size_t i : mine) A(seg[i].src, 0);
+    }
+    if (!iv.empty()) {
+      run("ordered-add", [&](cudaStream_t s) {
+        const OrdSeg* ds = sg.put(sl);
+        launch_ordered_add(sg.put(iv), (int)iv.size(), ds, mx, s);
+      });
+      stat(S_COPY, iv.size());
+    }
+    ar.release(mk);
   }
 
   // multiply(B, X) into preallocated Y (zeroed here), hblock.cpp:89-92

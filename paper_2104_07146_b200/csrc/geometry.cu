@@ -266,6 +266,109 @@ int host_layout(Geometry& g, int b, int e, int level) {
 }
 }  // namespace
 
+// Level-synchronous K2 frontier from the root pair (root_row, root_col) over the
+// node arrays box/left/right (one tree, or two trees concatenated for a
+// rectangular block tree); returns every node in DFS pre-order (geometry.cpp:
+// 100-154).  maxdepth bounds the block depth (<= deeper tree's depth + 1).
+std::vector<BlockNodeRec> block_frontier(const double* d_box, const int* d_left, const int* d_right,
+                                         int dim, double eta, int maxdepth, int root_row,
+                                         int root_col, cudaStream_t st) {
+  std::vector<FrontItem> root{FrontItem{root_row, root_col, 0ull, 0}};
+  size_t cap_front = 16, cap_all = 64;
+  FrontItem* f_cur = dalloc<FrontItem>(cap_front);
+  FrontItem* f_next = dalloc<FrontItem>(cap_front);
+  HMGP_CUDA(cudaMemcpyAsync(f_cur, root.data(), sizeof(FrontItem), cudaMemcpyHostToDevice, st));
+  BlockNodeRec* d_all = dalloc<BlockNodeRec>(cap_all);
+  int* d_cnt = dalloc<int>(2);
+  int ncur = 1, nall = 0;
+  for (int level = 0; ncur > 0; ++level) {
+    // capacity: each item emits <= 4 children and 1 record
+    if ((size_t)ncur * 4 > cap_front) {
+      size_t nc = std::max<size_t>((size_t)ncur * 4, cap_front * 2);
+      FrontItem* a = dalloc<FrontItem>(nc);
+      FrontItem* b = dalloc<FrontItem>(nc);
+      HMGP_CUDA(cudaMemcpyAsync(a, f_cur, ncur * sizeof(FrontItem), cudaMemcpyDeviceToDevice, st));
+      HMGP_CUDA(cudaStreamSynchronize(st));
+      cudaFree(f_cur);
+      cudaFree(f_next);
+      f_cur = a;
+      f_next = b;
+      cap_front = nc;
+    }
+    if ((size_t)nall + ncur > cap_all) {
+      size_t nc = std::max<size_t>((size_t)nall + ncur, cap_all * 2);
+      BlockNodeRec* a = dalloc<BlockNodeRec>(nc);
+      HMGP_CUDA(cudaMemcpyAsync(a, d_all, nall * sizeof(BlockNodeRec), cudaMemcpyDeviceToDevice, st));
+      HMGP_CUDA(cudaStreamSynchronize(st));
+      cudaFree(d_all);
+      d_all = a;
+      cap_all = nc;
+    }
+    int init[2] = {0, nall};
+    HMGP_CUDA(cudaMemcpyAsync(d_cnt, init, 8, cudaMemcpyHostToDevice, st));
+    k_block_expand<<<(ncur + 127) / 128, 128, 0, st>>>(f_cur, ncur, d_box, d_left, d_right, dim, eta,
+                                                       maxdepth, f_next, d_cnt, d_all, d_cnt + 1);
+    HMGP_LAUNCH_CHECK();
+    int out[2];
+    HMGP_CUDA(cudaMemcpyAsync(out, d_cnt, 8, cudaMemcpyDeviceToHost, st));
+    HMGP_CUDA(cudaStreamSynchronize(st));
+    ncur = out[0];
+    nall = out[1];
+    std::swap(f_cur, f_next);
+  }
+  // DFS pre-order of all nodes: sort by (key, depth) -> parent before first child.
+  std::vector<BlockNodeRec> nodes(nall);
+  HMGP_CUDA(cudaMemcpyAsync(nodes.data(), d_all, nall * sizeof(BlockNodeRec), cudaMemcpyDeviceToHost, st));
+  HMGP_CUDA(cudaStreamSynchronize(st));
+  std::sort(nodes.begin(), nodes.end(), [](const BlockNodeRec& a, const BlockNodeRec& b) {
+    return a.key != b.key ? a.key < b.key : a.depth < b.depth;
+  });
+  cudaFree(f_cur);
+  cudaFree(f_next);
+  cudaFree(d_all);
+  cudaFree(d_cnt);
+  return nodes;
+}
+
+// Rectangular block tree BlockClusterTree(rows, cols, eta) (geometry.cpp:100-154)
+// over two cluster trees: their node arrays are concatenated (column-tree ids
+// offset by the row tree's node count) and the same frontier kernel runs from
+// the pair of roots.  Leaves in DFS order as hmgp_block rows (tree positions).
+void block_tree_rect(const Geometry& R, const Geometry& Cg, double eta, std::vector<int>& out5,
+                     int& n_adm, int& n_dense, cudaStream_t st) {
+  if (R.dim != Cg.dim) throw std::invalid_argument("block tree: row and column trees differ in dimension");
+  const int nr = static_cast<int>(R.nbeg.size()), nc = static_cast<int>(Cg.nbeg.size()), dim = R.dim;
+  std::vector<int> left(nr + nc), right(nr + nc);
+  for (int i = 0; i < nr; ++i) {
+    left[i] = R.nleft[i];
+    right[i] = R.nright[i];
+  }
+  for (int i = 0; i < nc; ++i) {
+    left[nr + i] = Cg.nleft[i] < 0 ? -1 : Cg.nleft[i] + nr;
+    right[nr + i] = Cg.nright[i] < 0 ? -1 : Cg.nright[i] + nr;
+  }
+  int* d_l = dalloc<int>(nr + nc);
+  int* d_r = dalloc<int>(nr + nc);
+  double* d_b = dalloc<double>((size_t)(nr + nc) * 6);
+  HMGP_CUDA(cudaMemcpyAsync(d_l, left.data(), 4ull * (nr + nc), cudaMemcpyHostToDevice, st));
+  HMGP_CUDA(cudaMemcpyAsync(d_r, right.data(), 4ull * (nr + nc), cudaMemcpyHostToDevice, st));
+  HMGP_CUDA(cudaMemcpyAsync(d_b, R.d_box, 48ull * nr, cudaMemcpyDeviceToDevice, st));
+  HMGP_CUDA(cudaMemcpyAsync(d_b + (size_t)nr * 6, Cg.d_box, 48ull * nc, cudaMemcpyDeviceToDevice, st));
+  const std::vector<BlockNodeRec> nodes =
+      block_frontier(d_b, d_l, d_r, dim, eta, std::max(R.depth, Cg.depth) + 1, 0, nr, st);
+  cudaFree(d_l);
+  cudaFree(d_r);
+  cudaFree(d_b);
+  out5.clear();
+  n_adm = n_dense = 0;
+  for (const BlockNodeRec& b : nodes) {
+    if (b.tag == 2) continue;
+    const int c = b.col - nr;
+    out5.insert(out5.end(), {R.nbeg[b.row], R.nend[b.row], Cg.nbeg[c], Cg.nend[c], b.tag});
+    (b.tag == 0 ? n_adm : n_dense)++;
+  }
+}
+
 void geometry_build(Geometry& g, cudaStream_t st) {
   const int n = g.n, dim = g.dim;
   // ---- host tree shape (pre-order ids, like the reference's recursion) ----
@@ -347,59 +450,8 @@ void geometry_build(Geometry& g, cudaStream_t st) {
   HMGP_LAUNCH_CHECK();
 
   // ---- K2: block tree frontier ----
-  const int maxdepth = depth + 1;  // block depth <= cluster depth
-  std::vector<FrontItem> root{FrontItem{0, 0, 0ull, 0}};
-  size_t cap_front = 16, cap_all = 64;
-  FrontItem* f_cur = dalloc<FrontItem>(cap_front);
-  FrontItem* f_next = dalloc<FrontItem>(cap_front);
-  HMGP_CUDA(cudaMemcpyAsync(f_cur, root.data(), sizeof(FrontItem), cudaMemcpyHostToDevice, st));
-  BlockNodeRec* d_all = dalloc<BlockNodeRec>(cap_all);
-  int* d_cnt = dalloc<int>(2);
-  int ncur = 1, nall = 0;
-  for (int level = 0; ncur > 0; ++level) {
-    // capacity: each item emits <= 4 children and 1 record
-    if ((size_t)ncur * 4 > cap_front) {
-      size_t nc = std::max<size_t>((size_t)ncur * 4, cap_front * 2);
-      FrontItem* a = dalloc<FrontItem>(nc);
-      FrontItem* b = dalloc<FrontItem>(nc);
-      HMGP_CUDA(cudaMemcpyAsync(a, f_cur, ncur * sizeof(FrontItem), cudaMemcpyDeviceToDevice, st));
-      HMGP_CUDA(cudaStreamSynchronize(st));
-      cudaFree(f_cur);
-      cudaFree(f_next);
-      f_cur = a;
-      f_next = b;
-      cap_front = nc;
-    }
-    if ((size_t)nall + ncur > cap_all) {
-      size_t nc = std::max<size_t>((size_t)nall + ncur, cap_all * 2);
-      BlockNodeRec* a = dalloc<BlockNodeRec>(nc);
-      HMGP_CUDA(cudaMemcpyAsync(a, d_all, nall * sizeof(BlockNodeRec), cudaMemcpyDeviceToDevice, st));
-      HMGP_CUDA(cudaStreamSynchronize(st));
-      cudaFree(d_all);
-      d_all = a;
-      cap_all = nc;
-    }
-    int init[2] = {0, nall};
-    HMGP_CUDA(cudaMemcpyAsync(d_cnt, init, 8, cudaMemcpyHostToDevice, st));
-    k_block_expand<<<(ncur + 127) / 128, 128, 0, st>>>(f_cur, ncur, g.d_box, d_left, d_right, dim,
-                                                       g.eta, maxdepth, f_next, d_cnt, d_all,
-                                                       d_cnt + 1);
-    HMGP_LAUNCH_CHECK();
-    int out[2];
-    HMGP_CUDA(cudaMemcpyAsync(out, d_cnt, 8, cudaMemcpyDeviceToHost, st));
-    HMGP_CUDA(cudaStreamSynchronize(st));
-    ncur = out[0];
-    nall = out[1];
-    std::swap(f_cur, f_next);
-  }
-  // DFS pre-order of all nodes: sort by (key, depth) -> parent before first child.
-  g.bnodes.resize(nall);
-  HMGP_CUDA(cudaMemcpyAsync(g.bnodes.data(), d_all, nall * sizeof(BlockNodeRec),
-                            cudaMemcpyDeviceToHost, st));
-  HMGP_CUDA(cudaStreamSynchronize(st));
-  std::sort(g.bnodes.begin(), g.bnodes.end(), [](const BlockNodeRec& a, const BlockNodeRec& b) {
-    return a.key != b.key ? a.key < b.key : a.depth < b.depth;
-  });
+  g.bnodes = block_frontier(g.d_box, d_left, d_right, dim, g.eta, depth + 1, 0, 0, st);
+  const int nall = static_cast<int>(g.bnodes.size());
   // link children: a stack walk over the pre-order
   g.bkids.assign(nall, {});
   {
@@ -442,10 +494,6 @@ void geometry_build(Geometry& g, cudaStream_t st) {
   cudaFree(d_ranks);
   cudaFree(d_tmp);
   cudaFree(d_perm2);
-  cudaFree(f_cur);
-  cudaFree(f_next);
-  cudaFree(d_all);
-  cudaFree(d_cnt);
 }
 
 void geometry_free(Geometry& g) {

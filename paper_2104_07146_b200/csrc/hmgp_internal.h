@@ -42,6 +42,10 @@ struct Geometry {
 
 void geometry_build(Geometry& g, cudaStream_t st);
 void geometry_free(Geometry& g);
+// rectangular BlockClusterTree(rows, cols, eta): leaves in DFS order, 5 ints each
+// (row_begin, row_end, col_begin, col_end, tag 0 admissible / 1 dense)
+void block_tree_rect(const Geometry& rows, const Geometry& cols, double eta, std::vector<int>& out5,
+                     int& n_adm, int& n_dense, cudaStream_t st);
 
 // ---------------------------------------------------------------- H-matrix --
 enum Kind { BRANCH = 0, DENSE = 1, LOWRANK = 2 };

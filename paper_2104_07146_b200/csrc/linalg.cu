@@ -68,22 +68,12 @@ __device__ void gemm_item(const GemmItem& it, int tile0, int tstride, bool count
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int wr = (w >> 2) * 32, wc = (w & 3) * 16;  // warp sub-tile origin
   const int fr = lane >> 2, fk = lane & 3;           // fragment row / k index
-  // split-K when the item has fewer output tiles than CTAs (long, thin
-  // products such as V^T x over a big block): the partial products are added
-  // with FP64 atomics, so it needs an accumulate mode (C pre-zeroed by the
-  // caller for temporaries)
+  // No split-K inside an item and no atomics: every output element is written
+  // by exactly one CTA with a fixed summation order (bit-reproducible).  Long
+  // contractions are split by the host into K-range items writing separate
+  // slabs, summed in a fixed order by k_slab_sum.
   const int T = tm * tn;
-  int nsplit = 1, tbeg = tile0, tstep = tstride, kbeg = 0, kend = K;
-  if (it.atomic != 2 && tstride > T) nsplit = min(tstride / T, max(1, (K + 255) / 256));
-  if (nsplit > 1) {
-    if (tile0 >= T * nsplit) return;
-    const int kc = ((K + nsplit - 1) / nsplit + GK - 1) / GK * GK;
-    tbeg = tile0 % T;
-    tstep = T;
-    kbeg = (tile0 / T) * kc;
-    kend = min(K, kbeg + kc);
-    if (kbeg >= kend) return;
-  }
+  const int tbeg = tile0, tstep = tstride, kbeg = 0, kend = K;
   for (int tile = tbeg; tile < T; tile += tstep) {
     const int i0 = (tile % tm) * GT, j0 = (tile / tm) * GT;
     double acc[4][2][2];
@@ -148,9 +138,7 @@ __device__ void gemm_item(const GemmItem& it, int tile0, int tstride, bool count
           const int gi = i0 + wr + rb * 8 + fr;
           if (gi >= M) continue;
           const double v = acc[rb][cb][h];
-          if (it.atomic == 1 || nsplit > 1)
-            atomicAdd(&it.C[(size_t)gj * it.ldc + gi], it.alpha * v);
-          else if (it.atomic == 2)
+          if (it.atomic == 2)
             it.C[(size_t)gj * it.ldc + gi] = it.alpha * v;
           else
             it.C[(size_t)gj * it.ldc + gi] += it.alpha * v;
@@ -519,6 +507,56 @@ void launch_copy_scale(const CopyScaleItem* d_items, int count, int max_elems, c
   if (count <= 0) return;
   const int gy = max(1, min((max_elems + 255) / 256, 64));
   k_copy_scale<<<dim3(count, gy), 256, 0, st>>>(d_items);
+  HMGP_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------ ordered adds ---
+// y[i, c] += alpha * sum over the interval's segments, in segment order (the
+// reference's DFS order of hblk::apply over a branch, hblock.cpp:46-60).  The
+// host cuts the rows of every target into intervals covered by the same
+// segments, so intervals are independent and every element has one writer.
+__global__ void k_ordered_add(const OrdIv* __restrict__ ivs, const OrdSeg* __restrict__ segs) {
+  const OrdIv iv = ivs[blockIdx.x];
+  const int cols = iv.cols.get(), len = iv.i1 - iv.i0;
+  const size_t tot = (size_t)len * cols;
+  for (size_t e = blockIdx.y * (size_t)blockDim.x + threadIdx.x; e < tot;
+       e += (size_t)gridDim.y * blockDim.x) {
+    const int i = iv.i0 + (int)(e % len), c = (int)(e / len);
+    double v = iv.y[(size_t)c * iv.ldy + i];
+    for (int l = iv.l0; l < iv.l1; ++l) {
+      const OrdSeg sg = segs[l];
+      v += iv.alpha * sg.src[(size_t)c * sg.lds + (i - sg.r0)];
+    }
+    iv.y[(size_t)c * iv.ldy + i] = v;
+  }
+}
+
+void launch_ordered_add(const OrdIv* d_iv, int count, const OrdSeg* d_segs, int max_elems,
+                        cudaStream_t st) {
+  if (count <= 0) return;
+  const int gy = max(1, min((max_elems + 255) / 256, 32));
+  k_ordered_add<<<dim3(count, gy), 256, 0, st>>>(d_iv, d_segs);
+  HMGP_LAUNCH_CHECK();
+}
+
+// slab 0 <- slab 0 + slab 1 + ... + slab (nslab-1), fixed order (split-K partials)
+__global__ void k_slab_sum(const SlabSumItem* __restrict__ items) {
+  const SlabSumItem it = items[blockIdx.x];
+  const int rows = it.rows.get(), cols = it.cols.get();
+  const size_t tot = (size_t)rows * cols;
+  for (size_t e = blockIdx.y * (size_t)blockDim.x + threadIdx.x; e < tot;
+       e += (size_t)gridDim.y * blockDim.x) {
+    const size_t o = (e / rows) * it.ld + (e % rows);
+    double v = it.p[o];
+    for (int s = 1; s < it.nslab; ++s) v += it.p[s * it.slab + o];
+    it.p[o] = v;
+  }
+}
+
+void launch_slab_sum(const SlabSumItem* d_items, int count, int max_elems, cudaStream_t st) {
+  if (count <= 0) return;
+  const int gy = max(1, min((max_elems + 255) / 256, 16));
+  k_slab_sum<<<dim3(count, gy), 256, 0, st>>>(d_items);
   HMGP_LAUNCH_CHECK();
 }
 

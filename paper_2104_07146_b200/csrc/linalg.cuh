@@ -25,8 +25,9 @@ struct GemmItem {
   Dim M, N, K;
   int ta, tb;
   double alpha;
-  int atomic;  // 0: C += ..., 1: accumulate with FP64 atomics (several items share C
-               // rows), 2: C = ... (overwrite; the item owns its C)
+  int atomic;  // 0: C += ..., 2: C = ... (overwrite; the item owns its C).  (No FP64
+               // atomics: shared targets go through k_ordered_add, split-K through
+               // separate slabs + k_slab_sum, so results are bit-reproducible.)
 };
 
 // M (b x cols) <- L^{-1} M (trans = 0) or L^{-T} M (trans = 1); L b x b lower,
@@ -83,6 +84,28 @@ struct AppendItem {
   int cap;
 };
 
+// ordered accumulation (see k_ordered_add)
+struct OrdSeg {
+  const double* src;  // rows [r0, r0 + rows) of the target, column stride lds
+  int lds, r0;
+};
+struct OrdIv {
+  double* y;
+  int ldy;
+  Dim cols;
+  double alpha;
+  int i0, i1;  // target rows of the interval
+  int l0, l1;  // its segments (in order) in the segment array
+};
+// p[0 .. rows x cols, ld] += sum_{s >= 1} p[s * slab + ...]
+struct SlabSumItem {
+  double* p;
+  int ld;
+  Dim rows, cols;
+  int nslab;
+  size_t slab;
+};
+
 struct LeafFactorStatus {
   int fail_pos;  // min tree position of a failing pivot (INT_MAX if none)
   int clamped, negative;
@@ -94,6 +117,9 @@ struct LeafFactorStatus {
 void launch_gemm(const GemmItem* d_items, int count, int max_tiles, cudaStream_t st);
 // per-target ordered sequences: CTA b runs items[off[b]..off[b+1]) in order
 void launch_gemm_seq(const GemmItem* d_items, const int* d_off, int targets, cudaStream_t st);
+void launch_ordered_add(const OrdIv* d_iv, int count, const OrdSeg* d_segs, int max_elems,
+                        cudaStream_t st);
+void launch_slab_sum(const SlabSumItem* d_items, int count, int max_elems, cudaStream_t st);
 void launch_trsm_left(const TrsmLItem* d_items, int count, int max_cols, cudaStream_t st,
                       int max_b);
 void launch_trsm_right(const TrsmRItem* d_items, int count, int max_rows, cudaStream_t st,

@@ -160,8 +160,14 @@ def test_kernel_validation(hm):
 
 
 # --------------------------------------------------------------- assembly --
-@pytest.mark.parametrize("nu", [0.5, 0.325])
+@pytest.mark.parametrize("nu", [0.5, 0.325, 1.0])
 def test_assembly_vs_oracle(hm, oracle, nu):
+    """the same partition after coarsening (leaf kinds), and per
+    admissible block ||U V^T - U_o V_o^T||_F <= eps ||U_o V_o^T||_F.  Both sides run
+    the reference's ACA pivot rules (hmatrix.cpp:13-102); the recompression keeps
+    #{sigma_i > eps sigma_0} (hblock.cpp:151-153), so a rank can differ only by
+    singular values within rounding of the cut — those are counted and must be
+    +-1 with the error bar still met."""
     x = oracle.random_locations(1024, 17)
     th = [1.0, 0.1, nu, 0.01]
     eps = 1e-7
@@ -171,30 +177,33 @@ def test_assembly_vs_oracle(hm, oracle, nu):
     from oracle.oracle import make_config
     pr.assemble(th, make_config(leaf_size=32, eps=eps, threads=4))
     gl, ol = h.leaves(), pr.leaves()
-    assert np.array_equal(gl[:, :4], ol[:, :4])  # same stored-leaf layout
-    same_rank = np.mean(gl[:, 5] == ol[:, 5])
-    assert same_rank > 0.97, same_rank
-    worst_dense, worst_lr = 0.0, 0.0
+    assert np.array_equal(gl[:, :5], ol[:, :5])  # same stored-leaf layout AND kinds
+    ob = oracle.block_leaves(x, 32, 2.0)[0]
+    dense_geom = {tuple(b[:4]) for b in ob if b[4] == 1}
+    worst_dense, worst_lr, rank_diff = 0.0, 0.0, 0
     for k in range(len(gl)):
-        if gl[k, 4] == 1 and ol[k, 4] == 1:
+        if gl[k, 4] == 1:
             a, b = h.leaf_data(k, gl[k]), pr.leaf_data(k, ol[k])
-            if gl[k, 0] == ol[k, 0] and gl[k, 2] == gl[k, 0] or True:
-                scale = np.max(np.abs(b))
-                worst_dense = max(worst_dense, np.max(np.abs(a - b)) / scale)
-        if gl[k, 4] == 2 and ol[k, 4] == 2:
+            if tuple(gl[k, :4]) in dense_geom:  # kernel leaf: entries
+                assert np.max(np.abs(a - b) / np.abs(b)) < 1e-10
+            else:  # coarsened admissible block: U V^T product
+                worst_dense = max(worst_dense, np.linalg.norm(a - b) / np.linalg.norm(b))
+        else:
             u, v = h.leaf_data(k, gl[k])
             uo, vo = pr.leaf_data(k, ol[k])
             A, B = u @ v.T, uo @ vo.T
-            worst_lr = max(worst_lr, np.linalg.norm(A - B) / max(np.linalg.norm(B), 1e-300))
-    assert worst_dense < 1e-6  # coarsened blocks compare UV^T; pure kernel leaves are ~1e-15
-    assert worst_lr < 20 * eps, worst_lr
-    # exact kernel entries in every never-coarsened dense leaf
-    ob = oracle.block_leaves(x, 32, 2.0)[0]
-    dense_geom = {tuple(b[:4]) for b in ob if b[4] == 1}
-    for k in range(len(gl)):
-        if gl[k, 4] == 1 and tuple(gl[k, :4]) in dense_geom:
-            a, b = h.leaf_data(k, gl[k]), pr.leaf_data(k, ol[k])
-            assert np.max(np.abs(a - b) / np.abs(b)) < 1e-10
+            nb = np.linalg.norm(B)
+            if nb == 0.0:
+                assert np.linalg.norm(A) == 0.0
+                continue
+            worst_lr = max(worst_lr, np.linalg.norm(A - B) / nb)
+            if gl[k, 5] != ol[k, 5]:
+                assert abs(int(gl[k, 5]) - int(ol[k, 5])) == 1, (k, gl[k], ol[k])
+                rank_diff += 1
+    print(f"nu={nu}: blocks {len(gl)}, worst LR {worst_lr:.2e} (eps {eps}), coarsened {worst_dense:.2e}, "
+          f"rank +-1 in {rank_diff}")
+    assert worst_lr <= eps, worst_lr
+    assert worst_dense <= eps, worst_dense
 
 
 def test_assembly_accuracy_vs_dense(hm, oracle):
