@@ -129,18 +129,28 @@ int hmgp_at_distance(hmgp_ctx* ctx, const hmgp_matern* theta, const double* h, i
 int hmgp_bessel_k(hmgp_ctx* ctx, const double* nu, const double* x, int64_t count, int generic,
                   double* out);
 
+/* matern(h, params) (covkernel.cpp:206-214: pref * t^nu * bessel_k, no closed forms) and
+ * detail::matern_generic (generic = 1: bessel_k_generic, covkernel.cpp:184-194), on device */
+int hmgp_matern_values(hmgp_ctx* ctx, const hmgp_matern* theta, const double* h, int64_t count, int generic,
+                       double* out);
+
 /* ------------------------------------------------------------ H-matrix --- */
 /* assemble(block_tree, locations, params, rc) (hmatrix.hpp:88-89) */
 int hmgp_assemble(hmgp_ctx* ctx, hmgp_geom* g, const hmgp_matern* theta,
                   const hmgp_rank_control* rc, hmgp_hmat** out);
 /* HMatrix::storage / max_leaf_rank / max_diagonal (hmatrix.hpp:60-66) */
 int hmgp_hmat_stats(const hmgp_hmat* h, double* bytes, int* max_rank, double* max_diag);
-/* stored leaves in assembly order: row_begin,row_end,col_begin,col_end,kind(1 dense, 2 low-rank),rank */
+/* stored leaves in assembly order: row_begin,row_end,col_begin,col_end,kind(1 dense, 2 low-rank),rank
+ * (out6 == NULL: *count only) */
 int hmgp_hmat_leaves(const hmgp_hmat* h, int32_t* out6, int64_t cap, int64_t* count);
 /* payload of stored leaf k: dense -> a (m x n col-major); low-rank -> a = U, b = V */
 int hmgp_hmat_leaf_data(const hmgp_hmat* h, int64_t k, double* a, double* b);
 /* HMatrix::matvec (hmatrix.cpp:244-272), original order */
 int hmgp_hmat_matvec(hmgp_ctx* ctx, const hmgp_hmat* h, const double* x, double* y);
+/* from_dense(m) (hmatrix.cpp:223-242): single Dense leaf, self-contained tree; a is n x n
+ * column-major (host).  hmgp_hmat_symmetric: HMatrix::symmetric() (isApprox(m, m^T)) */
+int hmgp_hmat_from_dense(hmgp_ctx* ctx, const double* a, int n, hmgp_hmat** out);
+int hmgp_hmat_symmetric(const hmgp_hmat* h, int* out);
 void hmgp_hmat_destroy(hmgp_hmat* h);
 
 /* -------------------------------------------------------------- factor --- */

@@ -297,7 +297,7 @@ namespace {
 template <class T>
 T* dmalloc(size_t count) {
   T* p = nullptr;
-  HMGP_CUDA(cudaMalloc(&p, std::max<size_t>(1, count) * sizeof(T)));
+  p = dev_alloc_n<T>(count);
   return p;
 }
 template <class T>
@@ -336,10 +336,10 @@ int build_payload(HMat& h, const Geometry& g, int bn, bool sym) {
 }  // namespace
 
 HMat::~HMat() {
-  cudaFree(d_leaf);
-  cudaFree(d_rank);
-  cudaFree(d_compact);
-  cudaFree(pool);
+  dev_free(d_leaf);
+  dev_free(d_rank);
+  dev_free(d_compact);
+  dev_free(pool);
 }
 
 // Column capacity of a stored low-rank leaf for the factorization: its assembled
@@ -504,12 +504,12 @@ void assemble(HMat& h, Geometry& g, const MaternDev& p, double eps, bool fixed_r
           for (size_t q = 0; q <= tm.size(); ++q) off[q] = (int)q;
           int* d_off = upload(off, st);
           int* d_dfr = nullptr;
-          if (pass == 1) HMGP_CUDA(cudaMalloc(&d_dfr, tm.size() * 4));
+          if (pass == 1) d_dfr = dev_alloc_n<int>(tm.size());
           launch_truncate_pair(d_tm, d_off, (int)tm.size(), eps, d_err, st, d_dfr);
           HMGP_CUDA(cudaStreamSynchronize(st));
-          cudaFree(d_tm);
-          cudaFree(d_off);
-          cudaFree(d_dfr);
+          dev_free(d_tm);
+          dev_free(d_off);
+          dev_free(d_dfr);
         }
         if (!tbig.empty()) {  // large blocks: one 8-CTA cluster each
           TruncItem* d_tb = upload(tbig, st);
@@ -518,8 +518,8 @@ void assemble(HMat& h, Geometry& g, const MaternDev& p, double eps, bool fixed_r
           int* d_off = upload(off, st);
           launch_truncate_cluster(d_tb, d_off, (int)tbig.size(), eps, d_err, st, false);
           HMGP_CUDA(cudaStreamSynchronize(st));
-          cudaFree(d_tb);
-          cudaFree(d_off);
+          dev_free(d_tb);
+          dev_free(d_off);
         }
         if (!tsmall.empty()) {
           TruncItem* d_ti = upload(tsmall, st);
@@ -527,14 +527,14 @@ void assemble(HMat& h, Geometry& g, const MaternDev& p, double eps, bool fixed_r
           for (const TruncItem& x : tsmall) trunc_smem_dims(x.m, x.n, &sw, &smn);
           launch_truncate(d_ti, (int)tsmall.size(), eps, d_err, st, sw, smn);
           HMGP_CUDA(cudaStreamSynchronize(st));
-          cudaFree(d_ti);
+          dev_free(d_ti);
         }
-        cudaFree(c.ws);
+        dev_free(c.ws);
         c.ws = nullptr;
       }
       HMGP_CUDA(cudaStreamSynchronize(st));
-      cudaFree(d_items);
-      cudaFree(d_flags);
+      dev_free(d_items);
+      dev_free(d_flags);
       c.valid.assign(c.leaves.size(), 1);
       chunks.push_back(std::move(c));
     }
@@ -626,11 +626,11 @@ void assemble(HMat& h, Geometry& g, const MaternDev& p, double eps, bool fixed_r
         HMGP_CUDA(cudaMemcpyAsync(&fl, d_f, 8, cudaMemcpyDeviceToHost, st));
         HMGP_CUDA(cudaStreamSynchronize(st));
         g_work.kernel_flops += fl;
-        cudaFree(d_f);
+        dev_free(d_f);
         phase_mark(PH_LAYOUT);
       }
       HMGP_CUDA(cudaStreamSynchronize(st));
-      cudaFree(d_di);
+      dev_free(d_di);
     }
     for (int k : den) g_work.dense_entries += (double)mm[k] * nn[k];
   }
@@ -655,21 +655,21 @@ void assemble(HMat& h, Geometry& g, const MaternDev& p, double eps, bool fixed_r
       k_copy<<<(int)cp.size(), 256, 0, st>>>(d);
       HMGP_LAUNCH_CHECK();
       HMGP_CUDA(cudaStreamSynchronize(st));
-      cudaFree(d);
+      dev_free(d);
     }
     if (!oi.empty()) {
       OuterItem* d = upload(oi, st);
       k_outer<<<(int)oi.size(), 256, 0, st>>>(d);
       HMGP_LAUNCH_CHECK();
       HMGP_CUDA(cudaStreamSynchronize(st));
-      cudaFree(d);
+      dev_free(d);
     }
-    cudaFree(c.buf);
+    dev_free(c.buf);
     c.buf = nullptr;
   }
   phase_mark(PH_LAYOUT);
-  cudaFree(d_rank_tmp);
-  cudaFree(d_err);
+  dev_free(d_rank_tmp);
+  dev_free(d_err);
   h.d_leaf = upload(h.leaf, st);
   h.d_rank = upload(rank, st);
   h.d_compact = upload(compact, st);
@@ -687,8 +687,8 @@ void assemble(HMat& h, Geometry& g, const MaternDev& p, double eps, bool fixed_r
     HMGP_LAUNCH_CHECK();
     HMGP_CUDA(cudaMemcpyAsync(&h.max_diag, d_out, 8, cudaMemcpyDeviceToHost, st));
     HMGP_CUDA(cudaStreamSynchronize(st));
-    cudaFree(d_diag);
-    cudaFree(d_out);
+    dev_free(d_diag);
+    dev_free(d_out);
   }
   if (stats) {
     double entries_dense = 0;

@@ -274,6 +274,17 @@ int hmgp_bessel_k(hmgp_ctx* ctx, const double* nu, const double* x, int64_t coun
   })
 }
 
+int hmgp_matern_values(hmgp_ctx* ctx, const hmgp_matern* theta, const double* h, int64_t count, int generic,
+                double* out) {
+  API_GUARD({
+    hmgp_validate_matern(theta);  // covkernel.cpp:185, 207
+    for (int64_t t = 0; t < count; ++t)
+      if (!(h[t] >= 0.0) || !std::isfinite(h[t])) throw std::invalid_argument("matern: invalid distance");
+    HMGP_CUDA(cudaSetDevice(ctx->device));
+    matern_batch(ctx->stream, h, count, theta->sigma2, theta->ell, theta->nu, theta->tau2, generic, out);
+  })
+}
+
 // ---------------------------------------------------------------- H-matrix
 int hmgp_assemble(hmgp_ctx* ctx, hmgp_geom* g, const hmgp_matern* theta,
                   const hmgp_rank_control* rc, hmgp_hmat** out) {
@@ -354,6 +365,7 @@ int hmgp_hmat_leaves(const hmgp_hmat* hm, int32_t* out6, int64_t cap, int64_t* c
     const HMat& h = hm->h;
     const Geometry& G = *h.g;
     *count = (int64_t)h.leaf.size();
+    if (!out6) return HMGP_OK;  // count query
     if (*count > cap) throw std::out_of_range("hmgp_hmat_leaves: cap");
     for (size_t k = 0; k < h.leaf.size(); ++k) {
       const HNode& nd = h.nodes[h.leaf_node[k]];
@@ -392,6 +404,43 @@ int hmgp_hmat_matvec(hmgp_ctx* ctx, const hmgp_hmat* hm, const double* x, double
 }
 
 void hmgp_hmat_destroy(hmgp_hmat* h) { delete h; }
+
+// from_dense (hmatrix.cpp:223-242): a single Dense leaf over a one-cluster tree of
+// n points on a line (i/n, 0) with leaf size n (perm = identity).  The leaf
+// payload is the given matrix; symmetric() as Eigen's isApprox(m, m^T).
+int hmgp_hmat_from_dense(hmgp_ctx* ctx, const double* a, int n, hmgp_hmat** out) {
+  API_GUARD({
+    if (n < 1) throw std::invalid_argument("from_dense: need a nonempty square matrix");
+    HMGP_CUDA(cudaSetDevice(ctx->device));
+    std::vector<double> line(2 * (size_t)n, 0.0);
+    for (int i = 0; i < n; ++i) line[2 * (size_t)i] = static_cast<double>(i) / n;
+    hmgp_geom* g = nullptr;
+    const int rc = hmgp_geometry_build(ctx, line.data(), n, 2, n, 2.0, &g);
+    if (rc != HMGP_OK) return rc;
+    std::shared_ptr<hmgp_geom> gs(g, hmgp_geometry_destroy);
+    auto h = std::make_unique<hmgp_hmat>();
+    h->owned_geom = gs;
+    assemble(h->h, g->g, make_matern(1.0, 1.0, 0.5, 0.0), 1e-6, false, 16, 256, ctx->stream, nullptr);
+    if (h->h.leaf.size() != 1 || h->h.leaf[0].kind != DENSE)
+      throw std::runtime_error("from_dense: unexpected layout");
+    HMGP_CUDA(cudaMemcpyAsync(h->h.leaf[0].a, a, 8ull * n * n, cudaMemcpyHostToDevice, ctx->stream));
+    double md = -INFINITY, d2 = 0.0, t2 = 0.0;  // max_diagonal (hmatrix.cpp:306-313); isApprox
+    for (int i = 0; i < n; ++i) md = std::max(md, a[(size_t)i * n + i]);
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < n; ++i) {
+        const double x = a[(size_t)j * n + i], y = a[(size_t)i * n + j];
+        d2 += (x - y) * (x - y);
+        t2 += x * x;
+      }
+    h->h.max_diag = md;
+    h->symmetric = std::sqrt(d2) <= 1e-12 * std::sqrt(t2);
+    HMGP_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out = h.release();
+  })
+}
+int hmgp_hmat_symmetric(const hmgp_hmat* h, int* out) {
+  API_GUARD({ *out = h->symmetric ? 1 : 0; })
+}
 
 // ---------------------------------------------------------- data utilities
 static double u01(std::mt19937_64& g) { return (static_cast<double>(g() >> 11) + 0.5) * 0x1.0p-53; }

@@ -37,6 +37,28 @@ extern std::atomic<uint64_t> g_launches;
 
 namespace hmgp_gpu {
 
+// Device memory for per-evaluation buffers (alloc.cu).  Inside an AllocScope
+// (one L(θ) evaluation on its stream) buffers come from the device's
+// stream-ordered pool (cudaMallocAsync / cudaFreeAsync on that stream): freeing
+// them never synchronises the device, so concurrent θ workers do not serialise
+// each other on cudaFree.  Outside a scope: cudaMalloc / cudaFree.  Allocation
+// failures trim the pool's cached memory and retry once.
+void* dev_alloc(size_t bytes);
+void dev_free(void* p);
+template <class T>
+T* dev_alloc_n(size_t count) {
+  return static_cast<T*>(dev_alloc((count ? count : 1) * sizeof(T)));
+}
+struct AllocScope {
+  cudaStream_t prev;
+  explicit AllocScope(cudaStream_t s);
+  ~AllocScope();
+};
+// plain cudaMalloc with the same trim-and-retry on failure (persistent buffers)
+cudaError_t dev_malloc_plain(void** p, size_t bytes);
+// release the pool's cached (freed) blocks to the device (synchronises the device)
+void dev_pool_trim();
+
 constexpr int kSMs = 148;  // B200
 
 __device__ __forceinline__ double warp_sum(double v) {

@@ -25,6 +25,7 @@
 #include <map>
 #include <set>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -62,10 +63,10 @@ struct Arena {
     cur = 0;
     marks.clear();
     if (!(base && cap >= bytes)) {
-      if (base) cudaFree(base);
+      if (base) cudaFree(base);  // persistent (plain cudaMalloc)
       base = nullptr;
       cap = bytes;
-      if (cudaMalloc(&base, cap) != cudaSuccess) {
+      if (dev_malloc_plain((void**)&base, cap) != cudaSuccess) {
         // less free memory than planned (e.g. after a pool regrowth): take what
         // is there minus 1 GiB; device-detected overflow still reports cleanly
         cudaGetLastError();
@@ -73,7 +74,7 @@ struct Arena {
         size_t fr = 0, tot = 0;
         cudaMemGetInfo(&fr, &tot);
         cap = fr > ((size_t)2 << 30) ? fr - ((size_t)1 << 30) : fr / 2;
-        HMGP_CUDA(cudaMalloc(&base, cap));
+        HMGP_CUDA(dev_malloc_plain((void**)&base, cap));
       }
     }
     sub_cap = (cap / K) & ~size_t(255);
@@ -219,6 +220,18 @@ struct SidePool {
     for (cudaEvent_t x : evs) cudaEventDestroy(x);
   }
 };
+
+// cudaMalloc-or-pool allocation that reports failure instead of throwing
+static bool try_alloc(double** p, size_t bytes) {
+  try {
+    *p = static_cast<double*>(dev_alloc(bytes));
+    return false;
+  } catch (const Error&) {
+    cudaGetLastError();
+    *p = nullptr;
+    return true;
+  }
+}
 
 thread_local Arena g_arena;
 thread_local Stager g_stager;
@@ -2387,20 +2400,20 @@ static void solve_sweep(const Factor& F, double* v, bool trans, cudaStream_t st)
 
 // ------------------------------------------------------------ Factor API --
 Factor::~Factor() {
-  cudaFree(pool);
-  cudaFree(d_leaf);
-  cudaFree(d_rank);
-  cudaFree(d_compact);
-  cudaFree(d_d);
-  cudaFree(d_status);
-  cudaFree(d_fwd);
-  cudaFree(d_bwd);
-  cudaFree(d_work);
-  cudaFree(d_fsteps);
-  cudaFree(d_funits);
-  cudaFree(d_bsteps);
-  cudaFree(d_bunits);
-  cudaFree(d_part);
+  dev_free(pool);
+  dev_free(d_leaf);
+  dev_free(d_rank);
+  dev_free(d_compact);
+  dev_free(d_d);
+  dev_free(d_status);
+  dev_free(d_fwd);
+  dev_free(d_bwd);
+  dev_free(d_work);
+  dev_free(d_fsteps);
+  dev_free(d_funits);
+  dev_free(d_bsteps);
+  dev_free(d_bunits);
+  dev_free(d_part);
 }
 
 // Capacities (TCAP, low-rank column growth) of the last factorization that
@@ -2422,11 +2435,11 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
   const int L = (int)H.leaf.size();
   t_last_pool_bytes = H.pool_doubles * 8;
   // clone payload (hblock.cpp:17-28): same layout, new pool; compact_cols = 0
-  HMGP_CUDA(cudaMalloc(&F.d_leaf, sizeof(LeafDev) * std::max(L, 1)));
-  HMGP_CUDA(cudaMalloc(&F.d_rank, 4 * std::max(L, 1)));
-  HMGP_CUDA(cudaMalloc(&F.d_compact, 4 * std::max(L, 1)));
-  HMGP_CUDA(cudaMalloc(&F.d_d, 8ull * G.n));
-  HMGP_CUDA(cudaMalloc(&F.d_status, sizeof(LeafFactorStatus)));
+  F.d_leaf = static_cast<std::remove_reference_t<decltype(F.d_leaf)>>(dev_alloc(sizeof(LeafDev) * std::max(L, 1)));
+  F.d_rank = static_cast<std::remove_reference_t<decltype(F.d_rank)>>(dev_alloc(4 * std::max(L, 1)));
+  F.d_compact = static_cast<std::remove_reference_t<decltype(F.d_compact)>>(dev_alloc(4 * std::max(L, 1)));
+  F.d_d = static_cast<std::remove_reference_t<decltype(F.d_d)>>(dev_alloc(8ull * G.n));
+  F.d_status = static_cast<std::remove_reference_t<decltype(F.d_status)>>(dev_alloc(sizeof(LeafFactorStatus)));
   F.clamp_tol = 1e-14 * H.max_diag;  // hfactor.cpp:349
 
   // Temporaries are sized with a width capacity TCAP; a product wider than that
@@ -2482,15 +2495,15 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
       }
     }
     if (total != pool_doubles) {
-      cudaFree(F.pool);
+      dev_free(F.pool);
       F.pool = nullptr;
-      if (cudaMalloc(&F.pool, std::max<size_t>(1, total) * 8) != cudaSuccess) {
+      if (try_alloc(&F.pool, std::max<size_t>(1, total) * 8)) {
         // a regrown pool (doubled capacities) may not fit next to the persistent
         // temporary arena: drop the arena (re-sized to what is left below) first
         cudaGetLastError();
         F.pool = nullptr;
         release_thread_workspace();
-        if (start_3d && cudaMalloc(&F.pool, std::max<size_t>(1, total) * 8) != cudaSuccess) {
+        if (start_3d && try_alloc(&F.pool, std::max<size_t>(1, total) * 8)) {
           // the doubled 3-D start does not fit: fall back to the 2-D start
           cudaGetLastError();
           F.pool = nullptr;
@@ -2500,7 +2513,7 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
           pool_doubles = 0;
           continue;
         }
-        if (!F.pool) HMGP_CUDA(cudaMalloc(&F.pool, std::max<size_t>(1, total) * 8));
+        if (!F.pool) F.pool = dev_alloc_n<double>(std::max<size_t>(1, total));
       }
       pool_doubles = total;
     }
@@ -2520,12 +2533,12 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
     HMGP_CUDA(cudaMemcpyAsync(F.d_leaf, F.leaf.data(), sizeof(LeafDev) * L, cudaMemcpyHostToDevice, st));
     if (!ci.empty()) {
       CloneItem* d_ci = nullptr;
-      HMGP_CUDA(cudaMalloc(&d_ci, sizeof(CloneItem) * ci.size()));
+      d_ci = static_cast<std::remove_reference_t<decltype(d_ci)>>(dev_alloc(sizeof(CloneItem) * ci.size()));
       HMGP_CUDA(cudaMemcpyAsync(d_ci, ci.data(), sizeof(CloneItem) * ci.size(), cudaMemcpyHostToDevice, st));
       k_clone<<<(int)ci.size(), 256, 0, st>>>(d_ci);
       HMGP_LAUNCH_CHECK();
       HMGP_CUDA(cudaStreamSynchronize(st));
-      cudaFree(d_ci);
+      dev_free(d_ci);
     }
     HMGP_CUDA(cudaMemcpyAsync(F.d_rank, H.d_rank, 4ull * L, cudaMemcpyDeviceToDevice, st));
     HMGP_CUDA(cudaMemsetAsync(F.d_compact, 0, 4ull * L, st));
@@ -2627,15 +2640,15 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
   F.diag_leaf = dl;
   if (!ldl) {
     int *d1, *d2;
-    HMGP_CUDA(cudaMalloc(&d1, 4 * dl.size()));
-    HMGP_CUDA(cudaMalloc(&d2, 4 * dl.size()));
+    d1 = static_cast<std::remove_reference_t<decltype(d1)>>(dev_alloc(4 * dl.size()));
+    d2 = static_cast<std::remove_reference_t<decltype(d2)>>(dev_alloc(4 * dl.size()));
     HMGP_CUDA(cudaMemcpyAsync(d1, dl.data(), 4 * dl.size(), cudaMemcpyHostToDevice, st));
     HMGP_CUDA(cudaMemcpyAsync(d2, db.data(), 4 * db.size(), cudaMemcpyHostToDevice, st));
     k_collect_diag<<<(int)dl.size(), 128, 0, st>>>(F.d_leaf, d1, d2, (int)dl.size(), F.d_d);
     HMGP_LAUNCH_CHECK();
     HMGP_CUDA(cudaStreamSynchronize(st));
-    cudaFree(d1);
-    cudaFree(d2);
+    dev_free(d1);
+    dev_free(d2);
   }
   F.rank_host.resize(L);
   HMGP_CUDA(cudaMemcpyAsync(F.rank_host.data(), F.d_rank, 4ull * L, cudaMemcpyDeviceToHost, st));
@@ -2670,17 +2683,17 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
   F.fwd_off[nd] = (int)flat_f.size();
   F.bwd_off[nd] = (int)flat_b.size();
   F.diag_base = db;
-  HMGP_CUDA(cudaMalloc(&F.d_fwd, sizeof(SolveBlk) * std::max<size_t>(1, flat_f.size())));
-  HMGP_CUDA(cudaMalloc(&F.d_bwd, sizeof(SolveBlk) * std::max<size_t>(1, flat_b.size())));
+  F.d_fwd = static_cast<std::remove_reference_t<decltype(F.d_fwd)>>(dev_alloc(sizeof(SolveBlk) * std::max<size_t>(1, flat_f.size())));
+  F.d_bwd = static_cast<std::remove_reference_t<decltype(F.d_bwd)>>(dev_alloc(sizeof(SolveBlk) * std::max<size_t>(1, flat_b.size())));
   HMGP_CUDA(cudaMemcpyAsync(F.d_fwd, flat_f.data(), sizeof(SolveBlk) * flat_f.size(), cudaMemcpyHostToDevice, st));
   HMGP_CUDA(cudaMemcpyAsync(F.d_bwd, flat_b.data(), sizeof(SolveBlk) * flat_b.size(), cudaMemcpyHostToDevice, st));
-  HMGP_CUDA(cudaMalloc(&F.d_work, 8ull * (2 * G.n + 1024)));
+  F.d_work = static_cast<std::remove_reference_t<decltype(F.d_work)>>(dev_alloc(8ull * (2 * G.n + 1024)));
   {  // persistent-sweep plans (K10)
     const SolvePlan pf = build_solve_plan(F, flat_f, F.fwd_off, false);
     const SolvePlan pb = build_solve_plan(F, flat_b, F.bwd_off, true);
     auto up = [&](const void* src, size_t bytes) {
       void* d = nullptr;
-      HMGP_CUDA(cudaMalloc(&d, std::max<size_t>(bytes, 16)));
+      d = static_cast<std::remove_reference_t<decltype(d)>>(dev_alloc(std::max<size_t>(bytes, 16)));
       if (bytes) HMGP_CUDA(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, st));
       return d;
     };
@@ -2690,7 +2703,7 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
     F.d_bunits = up(pb.units.data(), pb.units.size() * sizeof(SUnit));
     F.solve_stride = std::max(pf.stride, pb.stride);
     const size_t pd = (size_t)std::max(pf.slots, pb.slots) * F.solve_stride;
-    HMGP_CUDA(cudaMalloc(&F.d_part, std::max<size_t>(pd, 1) * 8));
+    F.d_part = static_cast<std::remove_reference_t<decltype(F.d_part)>>(dev_alloc(std::max<size_t>(pd, 1) * 8));
   }
   phase_mark(PH_LAYOUT);
   HMGP_CUDA(cudaStreamSynchronize(st));

@@ -36,12 +36,17 @@ struct hmgp_geom {
 };
 struct hmgp_hmat {
   hmgp_gpu::HMat h;
+  // from_dense (hmatrix.cpp:223-242): the H-matrix owns its one-cluster tree;
+  // factors of it share the ownership (the reference's owned_tree_)
+  std::shared_ptr<hmgp_geom> owned_geom;
+  bool symmetric = true;
 };
 namespace hmgp_gpu {
 struct Factor;
 }
 struct hmgp_factor {
   std::unique_ptr<hmgp_gpu::Factor> f;
+  std::shared_ptr<hmgp_geom> owned_geom;
   ~hmgp_factor();
 };
 
@@ -63,6 +68,8 @@ void kriging_variance_dense(cudaStream_t st, const double* train, int n, const d
                             const MaternDev& p, double* out);
 void mloe_mmom(cudaStream_t st, const double* x, int n, int dim, const MaternDev& pt, const MaternDev& pa,
                const int* idx, int m, double* mloe, double* mmom);
+void matern_batch(cudaStream_t st, const double* h, int64_t count, double sigma2, double ell, double nu,
+                  double tau2, int generic, double* out);
 void bessel_batch(cudaStream_t st, const double* nu, const double* x, int64_t count, int generic,
                   double* out);
 void hmat_matvec(cudaStream_t st, const HMat& h, const double* x, double* y);

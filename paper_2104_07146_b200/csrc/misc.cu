@@ -17,8 +17,8 @@ namespace {
 template <class T>
 struct DBuf {
   T* p = nullptr;
-  explicit DBuf(size_t n) { HMGP_CUDA(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T))); }
-  ~DBuf() { cudaFree(p); }
+  explicit DBuf(size_t n) { p = hmgp_gpu::dev_alloc_n<T>(n); }
+  ~DBuf() { hmgp_gpu::dev_free(p); }
 };
 }  // namespace
 
@@ -108,6 +108,44 @@ void bessel_batch(cudaStream_t st, const double* nu, const double* x, int64_t co
   HMGP_CUDA(cudaMemcpyAsync(dn.p, nu, 8ull * count, cudaMemcpyHostToDevice, st));
   HMGP_CUDA(cudaMemcpyAsync(dx.p, x, 8ull * count, cudaMemcpyHostToDevice, st));
   k_bessel<<<kSMs * 8, 256, 0, st>>>(dn.p, dx.p, count, generic, dout.p);
+  HMGP_LAUNCH_CHECK();
+  HMGP_CUDA(cudaMemcpyAsync(out, dout.p, 8ull * count, cudaMemcpyDeviceToHost, st));
+  HMGP_CUDA(cudaStreamSynchronize(st));
+}
+
+// matern(h, p) / detail::matern_generic (covkernel.cpp:184-194, 206-214): the
+// public entry point uses pref * t^nu * K_nu(t) (no closed forms), K_nu with the
+// half-integer shortcut unless `generic`.  pref = sigma2 2^(1-nu) / Gamma(nu) is
+// computed on the host, as the reference does.
+__global__ void k_matern_values(const double* __restrict__ h, int64_t count, double sigma2,
+                                double ell, double nu, double tau2, double pref, int generic,
+                                double* __restrict__ out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const double hv = h[t];
+    if (hv == 0.0) {
+      out[t] = sigma2 + tau2;
+      continue;
+    }
+    const double x = hv / ell;
+    if (x < 1e-10) {
+      out[t] = sigma2;
+      continue;
+    }
+    const double hs = nu - 0.5;
+    const double k = (!generic && hs == floor(hs) && hs >= 0.0) ? bessel_half((int)hs, x)
+                                                                : bessel_k_generic_dev(nu, x);
+    out[t] = pref * pow(x, nu) * k;
+  }
+}
+
+void matern_batch(cudaStream_t st, const double* h, int64_t count, double sigma2, double ell, double nu,
+                  double tau2, int generic, double* out) {
+  if (count <= 0) return;
+  const double pref = sigma2 * std::pow(2.0, 1.0 - nu) / std::tgamma(nu);
+  DBuf<double> dh(count), dout(count);
+  HMGP_CUDA(cudaMemcpyAsync(dh.p, h, 8ull * count, cudaMemcpyHostToDevice, st));
+  k_matern_values<<<kSMs * 8, 256, 0, st>>>(dh.p, count, sigma2, ell, nu, tau2, pref, generic, dout.p);
   HMGP_LAUNCH_CHECK();
   HMGP_CUDA(cudaMemcpyAsync(out, dout.p, 8ull * count, cudaMemcpyDeviceToHost, st));
   HMGP_CUDA(cudaStreamSynchronize(st));

@@ -1,9 +1,11 @@
 // Pipeline entry points of the C ABI: factorize / solves / L(θ) / θ-batch /
 // predict, and K12 (the streamed kriging cross-covariance product).
 //   evaluate_loglik  loglik.cpp:18-38      predict  krige.cpp:9-44
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <exception>
+#include <mutex>
 #include <thread>
 #include <climits>
 #include <cmath>
@@ -24,8 +26,8 @@ namespace {
 template <class T>
 struct DBuf {
   T* p = nullptr;
-  explicit DBuf(size_t n) { HMGP_CUDA(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T))); }
-  ~DBuf() { cudaFree(p); }
+  explicit DBuf(size_t n) { p = hmgp_gpu::dev_alloc_n<T>(n); }
+  ~DBuf() { hmgp_gpu::dev_free(p); }
 };
 
 }  // namespace
@@ -73,6 +75,7 @@ void loglik_on_geom(hmgp_ctx* ctx, Geometry& g, const double* d_z, const hmgp_ma
   hmgp_validate_matern(th);
   if (cfg->rank.mode == 0 && !(cfg->rank.eps > 0.0))
     throw std::invalid_argument("assemble: eps must be positive");
+  AllocScope as(ctx->stream);  // per-evaluation buffers: stream-ordered (declared before h, f)
   HMat h;
   assemble(h, g, make_matern(th->sigma2, th->ell, th->nu, th->tau2), cfg->rank.eps,
            cfg->rank.mode == 1, cfg->rank.rank, cfg->rank.max_rank > 0 ? cfg->rank.max_rank : 256,
@@ -178,6 +181,7 @@ int hmgp_factorize(hmgp_ctx* ctx, hmgp_hmat* h, double eps_f, int form, hmgp_fac
                    hmgp_factor_info* info) {
   API_GUARD2({
     if (h->h.partial()) throw std::invalid_argument("factorize: H-matrix is a leaf-range shard");
+    if (!h->symmetric) throw std::invalid_argument("factorize: requires a symmetric H-matrix");  // hfactor.cpp:333-334
     HMGP_CUDA(cudaSetDevice(ctx->device));
     auto f = do_factorize(h->h, eps_f, form == 1, ctx->stream);
     if (info) {
@@ -188,6 +192,7 @@ int hmgp_factorize(hmgp_ctx* ctx, hmgp_hmat* h, double eps_f, int form, hmgp_fac
       info->storage_bytes = factor_storage_bytes(*f);
     }
     auto r = new hmgp_factor();
+    r->owned_geom = h->owned_geom;
     r->f = std::move(f);
     *out = r;
   })
@@ -301,12 +306,21 @@ int hmgp_loglik_batch(hmgp_ctx* ctx, hmgp_geom* g, const double* d_z, const hmgp
                       int ntheta, const hmgp_config* cfg, hmgp_loglik_result* res) {
   API_GUARD2({
     HMGP_CUDA(cudaSetDevice(ctx->device));
+    // θ whose worker ran out of device workspace: re-run on the caller thread
+    // with the full workspace afterwards (never scored -inf for lack of memory)
+    std::mutex retry_mu;
+    std::vector<int> retry;
     auto one = [&](hmgp_ctx* c, int t) {
       const double t0 = now();
-      try {  // fit() maps any failure to -inf (mle.cpp:152-158)
+      try {  // fit() maps numerical failures to -inf (mle.cpp:152-158)
         loglik_on_geom(c, g->g, d_z, &thetas[t], cfg, &res[t]);
       } catch (const hmgp_gpu::Error& e) {
-        if (e.code != HMGP_ENOTSPD && e.code != HMGP_ECAPACITY) throw;
+        if (e.code == HMGP_ECAPACITY && c != ctx) {
+          std::lock_guard<std::mutex> lk(retry_mu);
+          retry.push_back(t);
+          return;
+        }
+        if (e.code != HMGP_ENOTSPD) throw;
         res[t] = hmgp_loglik_result{-std::numeric_limits<double>::infinity(), 0, 0, g->g.n, 0, -1};
       } catch (const std::domain_error&) {
         res[t] = hmgp_loglik_result{-std::numeric_limits<double>::infinity(), 0, 0, g->g.n, 0, -1};
@@ -324,9 +338,12 @@ int hmgp_loglik_batch(hmgp_ctx* ctx, hmgp_geom* g, const double* d_z, const hmgp
     }
     // per worker: the first θ's arena peak with headroom, plus the H-matrix and
     // factor payloads; the caller's own arena is released first
-    const size_t peak = t_last_arena_peak, pool = t_last_pool_bytes;
+    // (a first θ that failed before its factorization leaves no peak: assume 8 GiB)
+    const size_t peak = t_last_arena_peak ? t_last_arena_peak : ((size_t)8 << 30);
+    const size_t pool = t_last_pool_bytes;
     HMGP_CUDA(cudaStreamSynchronize(ctx->stream));
     release_thread_workspace();
+    dev_pool_trim();
     size_t fr = 0, tot = 0;
     HMGP_CUDA(cudaMemGetInfo(&fr, &tot));
     const size_t share = peak + peak / 2 + ((size_t)1 << 30);
@@ -357,6 +374,9 @@ int hmgp_loglik_batch(hmgp_ctx* ctx, hmgp_geom* g, const double* d_z, const hmgp
     for (auto& th : ws) th.join();
     for (auto& e : errs)
       if (e) std::rethrow_exception(e);
+    std::sort(retry.begin(), retry.end());
+    if (!retry.empty()) dev_pool_trim();
+    for (int t : retry) one(ctx, t);  // caller thread, full workspace (arena_bytes_for)
   })
 }
 

@@ -4,6 +4,7 @@
 // that a reference user would compile against.  Prints one line per check and
 // exits non-zero on any failure.  Run by tests/test_cpp_api.py on a GPU box.
 #include <cmath>
+#include <algorithm>
 #include <cstdio>
 #include <random>
 #include <vector>
@@ -34,7 +35,209 @@ static int g_fail = 0;
 
 // random_locations (simgen.cpp:114-123) comes from hmgp/hmgp.hpp
 
+
+static double rel_err(double a, double b) { return std::abs(a - b) / std::abs(b); }
+
+// covkernel.hpp through the drop-in (test_covkernel.cpp:29-187 ported)
+static void covkernel_cases() {
+  {
+    MaternParams p{2.0, 0.3, 0.7, 0.25};
+    CHECK(matern(0.0, p) == 2.25);
+    MaternParams q{1.5, 0.1, 1.2, 0.0};
+    CHECK(matern(0.0, q) == 1.5);
+  }
+  CHECK(rel_err(matern(1.0, {1.0, 1.0, 0.5, 0.0}), 0.36787944117144233) < 1e-13);
+  CHECK(rel_err(detail::matern_generic(1.0, {1.0, 1.0, 0.5, 0.0}), 0.36787944117144233) < 1e-12);
+  CHECK(rel_err(matern(1.0, {1.0, 1.0, 1.5, 0.0}), 0.73575888234288464) < 1e-13);
+  CHECK(rel_err(detail::matern_generic(1.0, {1.0, 1.0, 1.5, 0.0}), 0.73575888234288464) < 1e-12);
+  CHECK(rel_err(matern(0.7, {1.3, 0.2, 0.6, 0.0}), 0.050105793549337933) < 1e-12);
+  CHECK(rel_err(matern(0.05, {2.0, 0.1, 2.5, 0.0}), 1.9206804224233392) < 1e-13);
+  CHECK(rel_err(matern(0.3, {1.0, 0.1, 1.5, 0.0}), 0.19914827347145577) < 1e-13);
+  CHECK(rel_err(bessel_k(0.5, 1.0), 0.46106850444789456) < 1e-14);
+  for (double x : {0.02, 0.7, 1.9, 3.5, 20.0, 300.0}) {
+    const double kh = std::sqrt(M_PI / (2.0 * x)) * std::exp(-x);
+    CHECK(rel_err(bessel_k(0.5, x), kh) < 1e-14);
+    CHECK(rel_err(bessel_k(1.5, x), kh * (1.0 + 1.0 / x)) < 1e-14);
+    CHECK(rel_err(detail::bessel_k_generic(0.5, x), kh) < 1e-12);
+    CHECK(rel_err(detail::bessel_k_generic(1.5, x), kh * (1.0 + 1.0 / x)) < 1e-12);
+  }
+  const double refs[][3] = {
+      {1.0, 1.0, 0.60190723019723457},   {0.3, 0.5, 0.97647412438178792},
+      {0.6, 1.0, 0.47971569489286612},   {1.0, 1e-6, 999999.99999278428},
+      {2.7, 3.2, 0.072917852205606608},  {5.5, 10.0, 7.3304530079850216e-5},
+      {10.0, 0.01, 1.8579404390480640e+28}, {25.0, 30.0, 3.7775319791336277e-10},
+      {0.9, 650.0, 2.5140676518253439e-284}, {7.3, 2.0, 543.63827738445926},
+      {12.6, 0.37, 1.4985106123100319e+17}, {3.0, 1e-8, 7.9999999999999999e+24},
+      {0.01, 0.02, 4.0298381770492421},  {24.5, 1e-8, 1.4946625757169951e+226},
+      {1.9, 700.0, 4.6818247046354968e-306}};
+  for (const auto& r : refs) {
+    CHECK(rel_err(bessel_k(r[0], r[1]), r[2]) < 1e-12);
+    CHECK(rel_err(detail::bessel_k_generic(r[0], r[1]), r[2]) < 1e-12);
+  }
+  CHECK_THROWS_AS(bessel_k(0.5, 0.0), std::domain_error);
+  CHECK_THROWS_AS(bessel_k(0.5, -1.0), std::domain_error);
+  CHECK_THROWS_AS(bessel_k(-1.0, 1.0), std::domain_error);
+  CHECK(bessel_k(0.5, 800.0) >= 0.0 && bessel_k(0.5, 800.0) < 1e-300);
+  for (double nu : {0.37, 0.5, 1.1, 2.5, 4.8}) {  // positive, non-increasing
+    MaternParams p{1.0, 0.2, nu, 0.0};
+    double prev = matern(1e-9, p);
+    for (int i = 1; i <= 50; ++i) {
+      const double v = matern(10.0 * i / 50.0, p);
+      CHECK(v > 0.0 && v <= prev * (1.0 + 1e-14) && v <= p.sigma2 + p.tau2);
+      prev = v;
+    }
+  }
+  {  // cov_block basics
+    std::vector<Location> pts{{0.2, 0.2}, {0.2, 0.2}, {0.5, 0.2}};
+    MaternParams p{2.0, 0.3, 0.5, 0.5};
+    const std::vector<int> one{1}, r{0}, c{1}, bad{7};
+    CHECK(cov_block(one, one, pts, p)(0, 0) == 2.5);
+    CHECK(std::abs(cov_block(r, c, pts, p)(0, 0) - 2.0) <= 2e-14);
+    CHECK_THROWS_AS(cov_block(bad, c, pts, p), std::out_of_range);
+  }
+  {  // Toeplitz exponential block
+    std::vector<Location> pts{{0.0, 0.0}, {0.1, 0.0}, {0.2, 0.0}};
+    std::vector<int> all{0, 1, 2};
+    const Matrix b = cov_block(all, all, pts, {1.3, 0.1, 0.5, 0.0});
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) CHECK(rel_err(b(i, j), 1.3 * std::exp(-std::abs(i - j))) < 1e-13);
+  }
+  {  // cov_dense symmetric, nugget on the diagonal
+    const auto pts = random_locations(40, 42);
+    const Matrix c = cov_dense(pts, {1.0, 0.1, 1.5, 1e-8});
+    for (int i = 0; i < 40; ++i) {
+      CHECK(c(i, i) == 1.0 + 1e-8);
+      for (int j = 0; j < 40; ++j) CHECK(c(i, j) == c(j, i));
+    }
+  }
+  CHECK_THROWS_AS(matern(1.0, {0.0, 1.0, 0.5, 0.0}), std::invalid_argument);
+  CHECK_THROWS_AS(matern(1.0, {1.0, -1.0, 0.5, 0.0}), std::invalid_argument);
+  CHECK_THROWS_AS(matern(1.0, {1.0, 1.0, 0.0, 0.0}), std::invalid_argument);
+  CHECK_THROWS_AS(matern(1.0, {1.0, 1.0, 0.5, -0.1}), std::invalid_argument);
+  CHECK_THROWS_AS(matern(std::nan(""), {1.0, 1.0, 0.5, 0.0}), std::invalid_argument);
+  {  // KernelEvaluator matches matern
+    const auto pts = random_locations(50, 8);
+    for (double nu : {0.5, 1.5, 2.5, 3.5, 0.82}) {
+      MaternParams p{1.4, 0.07, nu, 0.3};
+      KernelEvaluator k(pts, p);
+      for (int i = 0; i < 50; i += 7)
+        for (int j = 0; j < 50; j += 5) {
+          const double want = i == j ? p.sigma2 + p.tau2 : matern(distance(pts[i], pts[j]), p);
+          CHECK(rel_err(k(i, j), want) < 1e-13);
+        }
+      CHECK(k.at_distance(0.0) == p.sigma2);
+    }
+  }
+}
+
+// geometry.hpp / hmatrix.hpp / pipeline.hpp structure through the drop-in
+static void structure_cases() {
+  const auto pts = random_locations(1500, 3);
+  ClusterTree t(pts, 32);
+  {  // Cluster tree: root covers everything, children partition, leaves left to right
+    CHECK(t.root().begin == 0 && t.root().end == 1500 && !t.root().is_leaf());
+    const auto lv = t.leaves();
+    int pos = 0;
+    for (const Cluster* c : lv) {
+      CHECK(c->is_leaf() && c->begin == pos && c->size() <= 32 && c->size() > 0);
+      pos = c->end;
+      for (int k = c->begin; k < c->end; ++k) {  // box containment (test_geometry.cpp:48-64)
+        const Location& p = pts[t.perm()[k]];
+        CHECK(p.x >= c->box.lo[0] && p.x <= c->box.hi[0] && p.y >= c->box.lo[1] && p.y <= c->box.hi[1]);
+      }
+    }
+    CHECK(pos == 1500);
+    Box a{{0, 0}, {1, 1}}, b{{2, 0}, {3, 1}};
+    CHECK(a.diameter() == std::sqrt(2.0) && Box::distance(a, b) == 1.0 && Box::distance(a, a) == 0.0);
+  }
+  BlockClusterTree bt(t, t, 2.0);
+  {  // Node tree: DFS leaves = flat list; admissibility rule; square_symmetric
+    CHECK(bt.square_symmetric() && &bt.rows() == &t && &bt.cols() == &t);
+    CHECK(bt.leaves().size() == bt.blocks().size());
+    CHECK(static_cast<int>(bt.leaves().size()) == bt.admissible_count() + bt.dense_count());
+    for (size_t k = 0; k < bt.leaves().size(); ++k) {
+      const auto* l = bt.leaves()[k];
+      CHECK(l->row->begin == bt.blocks()[k].row_begin && l->col->end == bt.blocks()[k].col_end);
+      if (l->tag == BlockClusterTree::Node::Tag::Admissible) {
+        const double d = Box::distance(l->row->box, l->col->box);
+        CHECK(d > 0.0 && std::min(l->row->box.diameter(), l->col->box.diameter()) <= 2.0 * d);
+      } else {
+        CHECK(l->row->is_leaf() && l->col->is_leaf());
+      }
+    }
+    CHECK(!bt.root().is_leaf() && bt.root().children.size() == 4);
+  }
+  {  // rectangular block tree (two different cluster trees): tiles rows x cols exactly
+    const auto q = random_locations(700, 5);
+    ClusterTree t2(q, 16);
+    BlockClusterTree rb(t, t2, 2.0);
+    CHECK(!rb.square_symmetric());
+    long long area = 0;
+    for (const auto* l : rb.leaves()) area += (long long)l->row->size() * l->col->size();
+    CHECK(area == 1500LL * 700);
+    CHECK(rb.admissible_count() > 0);
+    CHECK_THROWS_AS(assemble(rb, pts, MaternParams{}, RankControl::fixed_accuracy(1e-6)), std::invalid_argument);
+  }
+  {  // assemble honours `locations`; HMatrix structure accessors; root() payload view
+    const MaternParams p{1.0, 0.1, 0.5, 0.01};
+    auto moved = pts;
+    moved[3].x += 1e-3;
+    CHECK_THROWS_AS(assemble(bt, moved, p, RankControl::fixed_accuracy(1e-6)), std::invalid_argument);
+    const HMatrix h = assemble(bt, pts, p, RankControl::fixed_accuracy(1e-6));
+    CHECK(&h.row_tree() == &t && &h.col_tree() == &t && h.rank_control().eps == 1e-6 && h.symmetric());
+    CHECK(h.leaf_range().first == 0 && h.leaf_range().second == h.leaf_count());
+    const HBlock& r = h.root();
+    CHECK(r.kind == BlockKind::Branch && r.nrows() == 1500 && r.child(0, 1) == nullptr);
+    // payload bytes of the view == storage(); U V^T of one low-rank leaf == matvec action
+    std::size_t bytes = 0;
+    std::vector<const HBlock*> st{&r};
+    const HBlock* lr = nullptr;
+    while (!st.empty()) {
+      const HBlock* b = st.back();
+      st.pop_back();
+      bytes += b->payload_bytes();
+      if (b->kind == BlockKind::LowRank && !lr) lr = b;
+      for (const auto& c : b->children)
+        if (c) st.push_back(c.get());
+    }
+    CHECK(bytes == h.storage().bytes);
+    CHECK(lr && lr->U.rows() == lr->nrows() && lr->V.rows() == lr->ncols() && lr->compact_cols == lr->rank());
+  }
+  {  // AssembledCov / assemble_covariance (loglik.cpp:9-16)
+    HConfig cfg;
+    cfg.leaf_size = 32;
+    const AssembledCov ac = assemble_covariance(pts, MaternParams{1.0, 0.1, 0.5, 0.01}, cfg);
+    CHECK(ac.tree->size() == 1500 && ac.blocks->square_symmetric() && ac.matrix.rows() == 1500);
+    CHECK(ac.tree->perm() == t.perm());
+  }
+  {  // from_dense (hmatrix.cpp:223-242): [[4,2],[2,5]] -> LDL L21 = 0.5, D = (4, 4)
+    Matrix m(2, 2);
+    m(0, 0) = 4;
+    m(1, 0) = 2;
+    m(0, 1) = 2;
+    m(1, 1) = 5;
+    const HMatrix h = from_dense(m);
+    CHECK(h.symmetric() && h.rows() == 2 && h.root().kind == BlockKind::Dense);
+    const HFactor f = h_ldl(h, 1e-10);
+    const Vector d = f.diagonal();
+    CHECK(d[0] == 4.0 && d[1] == 4.0);
+    CHECK(f.lower_dense()(1, 0) == 0.5);
+    Matrix one(1, 1);
+    one(0, 0) = 4.0;
+    CHECK(h_cholesky(from_dense(one), 1e-10).diagonal()[0] == 2.0);  // 1x1 Cholesky => 2
+    Matrix ns(2, 2);
+    ns(0, 0) = 1;
+    ns(1, 0) = 0.5;
+    ns(1, 1) = 1;
+    CHECK(!from_dense(ns).symmetric());
+    CHECK_THROWS_AS(factorize(from_dense(ns), 1e-6, FactorForm::Ldl), std::invalid_argument);
+    CHECK_THROWS_AS(from_dense(Matrix(2, 3)), std::invalid_argument);
+  }
+}
+
 int main() {
+  covkernel_cases();
+  structure_cases();
   {  // single point tree (test_geometry.cpp:20-27)
     std::vector<Location> pts{{0.3, 0.7}};
     ClusterTree t(pts, 32);
@@ -55,10 +258,10 @@ int main() {
     ClusterTree t(pts, 16);
     BlockClusterTree bt(t, t, 2.0);
     std::vector<int> cnt(256 * 256, 0);
-    for (const auto& l : bt.leaves()) {
-      for (int i = l.row_begin; i < l.row_end; ++i)
-        for (int j = l.col_begin; j < l.col_end; ++j) cnt[i * 256 + j]++;
-      if (l.row_begin == l.col_begin && l.row_end == l.col_end) CHECK(!l.admissible);
+    for (const BlockClusterTree::Node* l : bt.leaves()) {
+      for (int i = l->row->begin; i < l->row->end; ++i)
+        for (int j = l->col->begin; j < l->col->end; ++j) cnt[i * 256 + j]++;
+      if (l->row == l->col) CHECK(l->tag != BlockClusterTree::Node::Tag::Admissible);
     }
     for (int c : cnt) CHECK(c == 1);
     CHECK(bt.admissible_count() + bt.dense_count() == static_cast<int>(bt.leaves().size()));
