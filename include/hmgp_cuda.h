@@ -201,6 +201,34 @@ int hmgp_cross_apply_device(hmgp_ctx* ctx, const double* d_train, int n, int dim
                             const double* d_w, const double* d_test, int m,
                             const hmgp_matern* theta, double* d_out);
 
+/* ------------------------------------------- θ-sweep / kriging shards (§8e) */
+/* One rank's share of a θ list on its GPU, z in HOST memory (uploaded once):
+   the independent probes of the reference's MLE (mle.cpp:152-158).  Same result
+   rows and failure mapping as hmgp_loglik_batch. */
+int hmgp_loglik_sweep(hmgp_ctx* ctx, hmgp_geom* g, const double* z, const hmgp_matern* thetas,
+                      int ntheta, const hmgp_config* cfg, hmgp_loglik_result* res);
+/* Indices of the θ that `rank` of `world` evaluates: round-robin over the list
+   sorted ν-major (stable), returned ascending.  idx may be NULL (count only). */
+int hmgp_sweep_shard(const hmgp_matern* thetas, int ntheta, int rank, int world, int32_t* idx,
+                     int* count);
+/* Contiguous [begin, end) of m new locations predicted by `rank` of `world`. */
+int hmgp_predict_range(int m, int rank, int world, int* begin, int* end);
+/* NCCL plumbing for the two result gathers (libnccl resolved at first use).
+   id128: a 128-byte ncclUniqueId made on one rank and sent to the others by the
+   caller's launcher (MPI, torch.distributed, a file). */
+typedef struct hmgp_comm hmgp_comm;
+int hmgp_comm_unique_id(void* id128);
+int hmgp_comm_create(hmgp_ctx* ctx, const void* id128, int rank, int world, hmgp_comm** out);
+void hmgp_comm_destroy(hmgp_comm* comm);
+/* ONE all-gather of this rank's rows into the θ-ordered table (ntheta rows) on
+   every rank; rows nobody evaluated keep status -2 and loglik NaN.  comm == NULL
+   or world 1: local scatter, no collective. */
+int hmgp_sweep_gather(hmgp_ctx* ctx, hmgp_comm* comm, const int32_t* idx, const hmgp_loglik_result* local,
+                      int count, int ntheta, hmgp_loglik_result* table);
+/* ONE all-gather of the prediction slices (hmgp_predict_range) into out[m] on
+   every rank; m == 0 returns without a collective. */
+int hmgp_predict_gather(hmgp_ctx* ctx, hmgp_comm* comm, const double* local, int m, double* out);
+
 /* ------------------------------------------------------- instrumentation */
 /* the context's CUDA stream (cudaStream_t), for event timing by callers */
 int hmgp_ctx_stream(hmgp_ctx* ctx, void** stream);

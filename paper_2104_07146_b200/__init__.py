@@ -151,6 +151,15 @@ _sig("hmgp_loglik_geom", C.c_int, [_vp, _vp, C.c_void_p, C.POINTER(Matern), C.PO
                                    C.POINTER(_LogLik)])
 _sig("hmgp_loglik_batch", C.c_int, [_vp, _vp, C.c_void_p, C.POINTER(Matern), C.c_int, C.POINTER(_Config),
                                     C.POINTER(_LogLik)])
+_sig("hmgp_loglik_sweep", C.c_int, [_vp, _vp, _dp, C.POINTER(Matern), C.c_int, C.POINTER(_Config),
+                                    C.POINTER(_LogLik)])
+_sig("hmgp_sweep_shard", C.c_int, [C.POINTER(Matern), C.c_int, C.c_int, C.c_int, _ip, C.POINTER(C.c_int)])
+_sig("hmgp_predict_range", C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)])
+_sig("hmgp_comm_unique_id", C.c_int, [C.c_void_p])
+_sig("hmgp_comm_create", C.c_int, [_vp, C.c_void_p, C.c_int, C.c_int, C.POINTER(_vp)])
+_sig("hmgp_comm_destroy", None, [_vp])
+_sig("hmgp_sweep_gather", C.c_int, [_vp, _vp, _ip, C.POINTER(_LogLik), C.c_int, C.c_int, C.POINTER(_LogLik)])
+_sig("hmgp_predict_gather", C.c_int, [_vp, _vp, _dp, C.c_int, _dp])
 _sig("hmgp_predict", C.c_int, [_vp, _dp, C.c_int, C.c_int, _dp, _dp, C.c_int, C.POINTER(Matern),
                                C.POINTER(_Config), _dp, _dp])
 _sig("hmgp_cross_apply_device", C.c_int, [_vp, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p,

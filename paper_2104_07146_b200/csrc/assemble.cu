@@ -368,6 +368,7 @@ void balanced_ranges(const double* cost, int L, int parts, int* bounds) {
 
 void assemble(HMat& h, Geometry& g, const MaternDev& p, double eps, bool fixed_rank, int rank_k,
               int max_rank, cudaStream_t st, double* stats, int shard, int n_shards) {
+  NvtxRange nvtx_range("hmgp:assemble(K3-K5)");
   h.g = &g;
   h.p = p;
   h.eps = eps;

@@ -1,6 +1,7 @@
 // Shared device/host helpers for the hmgp B200 library (sm_100a, FP64).
 #pragma once
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 #include <atomic>
@@ -8,6 +9,16 @@
 #include <string>
 
 namespace hmgp_gpu {
+
+// NVTX phase range (SURVEY.md §5 tracing): visible in Nsight Systems / ncu --nvtx,
+// a no-op costing one load when no tool is attached (header-only NVTX3).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 
 // Error raised inside the library; mapped to a C-ABI status code.
 struct Error : std::runtime_error {

@@ -152,12 +152,23 @@ struct Stager {
     wrap_ms = 0;
     if (h) return;
     cap = bytes;
-    HMGP_CUDA(cudaMallocHost(&h, cap));
-    HMGP_CUDA(cudaMalloc(&d, cap));
+    // Descriptors are copied into a device ring (one cudaMemcpyAsync per batch).
+    // HMGP_DESC_ZEROCOPY=1 lets the kernels read them in place from mapped pinned
+    // host memory instead: measured on B200 (profiles/r2_exp_desc.txt) that is 6 %
+    // slower for one C3 L(θ) (11.2 s vs 10.5 s) and no faster for concurrent θ, so
+    // the copy-engine FIFO is not what limits θ-batch concurrency.
+    zero_copy = getenv("HMGP_DESC_ZEROCOPY") != nullptr;
+    HMGP_CUDA(cudaHostAlloc(&h, cap, cudaHostAllocMapped | cudaHostAllocPortable));
+    if (zero_copy) {
+      HMGP_CUDA(cudaHostGetDevicePointer((void**)&d, h, 0));
+    } else {
+      HMGP_CUDA(cudaMalloc(&d, cap));
+    }
   }
+  bool zero_copy = false;
   ~Stager() {
+    if (d && !zero_copy) cudaFree(d);
     if (h) cudaFreeHost(h);
-    if (d) cudaFree(d);
   }
   template <class T>
   const T* put(const std::vector<T>& v) {
@@ -172,7 +183,8 @@ struct Stager {
       off = 0;
     }
     std::memcpy(h + off, v.data(), v.size() * sizeof(T));
-    HMGP_CUDA(cudaMemcpyAsync(d + off, h + off, v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+    if (!zero_copy)
+      HMGP_CUDA(cudaMemcpyAsync(d + off, h + off, v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
     const T* r = reinterpret_cast<const T*>(d + off);
     off += bytes;
     return r;
@@ -2426,6 +2438,7 @@ struct CapMemo {
 static thread_local CapMemo t_cap_memo;
 
 void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size_t arena_bytes) {
+  NvtxRange nvtx_range("hmgp:factorize(K6-K9)");
   const Geometry& G = *H.g;
   F.g = H.g;
   F.ldl = ldl;
@@ -2764,6 +2777,7 @@ static double reduce(const Factor& F, const double* v, int mode, cudaStream_t st
 
 // HFactor::log_det (hfactor.cpp:399-403)
 double factor_log_det(const Factor& F, cudaStream_t st) {
+  NvtxRange nvtx_range("hmgp:log_det(K11)");
   const int n = F.g->n;
   if (F.ldl) {
     int* cnt = reinterpret_cast<int*>(F.d_work + 2 * (size_t)n + 600);
@@ -2781,6 +2795,7 @@ double factor_log_det(const Factor& F, cudaStream_t st) {
 
 // HFactor::quad_form with b in original order on device (hfactor.cpp:389-397)
 double factor_quad_form_dev(const Factor& F, const double* d_b, cudaStream_t st) {
+  NvtxRange nvtx_range("hmgp:quad_form(K10)");
   const int n = F.g->n;
   double* v = F.d_work;
   k_gather<<<(n + 255) / 256, 256, 0, st>>>(d_b, F.g->d_perm, n, v);
@@ -2791,6 +2806,7 @@ double factor_quad_form_dev(const Factor& F, const double* d_b, cudaStream_t st)
 
 // solve_factored / solve_lower with device b, x in original order
 void factor_solve_dev(const Factor& F, const double* d_b, double* d_x, bool full, cudaStream_t st) {
+  NvtxRange nvtx_range("hmgp:solve(K10)");
   const int n = F.g->n;
   double* v = F.d_work;
   k_gather<<<(n + 255) / 256, 256, 0, st>>>(d_b, F.g->d_perm, n, v);

@@ -370,6 +370,7 @@ void block_tree_rect(const Geometry& R, const Geometry& Cg, double eta, std::vec
 }
 
 void geometry_build(Geometry& g, cudaStream_t st) {
+  NvtxRange nvtx_range("hmgp:geometry(K1-K2)");
   const int n = g.n, dim = g.dim;
   // ---- host tree shape (pre-order ids, like the reference's recursion) ----
   g.nbeg.clear();

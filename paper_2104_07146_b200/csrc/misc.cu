@@ -211,6 +211,7 @@ __global__ void k_permute_out(const double* __restrict__ yt, const int* __restri
 }
 
 void hmat_matvec(cudaStream_t st, const HMat& h, const double* x, double* y) {
+  NvtxRange nvtx_range("hmgp:matvec");
   const Geometry& G = *h.g;
   const int n = G.n, L = (int)h.leaf.size();
   std::vector<int> r0(L), c0(L);

@@ -161,6 +161,7 @@ __global__ void k_cross_reduce(const double* __restrict__ part, int m, int slice
 
 void cross_apply(cudaStream_t st, const double* d_train, int n, int dim, const double* d_w,
                  const double* d_test, int m, const MaternDev& p, double* d_out) {
+  NvtxRange nvtx_range("hmgp:cross_apply(K12)");
   if (m <= 0) return;
   const int bx = (m + 255) / 256;
   int slices = std::max(1, (kSMs * 4 + bx - 1) / bx);

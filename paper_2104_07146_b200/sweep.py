@@ -121,3 +121,84 @@ def assemble_sharded(geom, theta, rc=None, dist=None):
     ws = dist.get_world_size() if dist is not None and dist.is_initialized() else 1
     rk = dist.get_rank() if ws > 1 else 0
     return assemble_shard(geom, theta, rk, ws, rc)
+
+
+# ------------------------------------------------- the C-ABI path (no torch)
+class Comm:
+    """NCCL communicator of the C ABI (hmgp_comm_*): rank 0 makes the 128-byte
+    unique id, the launcher hands it to the other ranks (here: any callable
+    ``bcast(bytes_or_None) -> bytes``, e.g. torch.distributed / a file)."""
+
+    def __init__(self, ctx, rank, world, bcast=None):
+        import ctypes as C
+
+        from . import _chk, _lib
+        self.ctx, self.rank, self.world = ctx, rank, world
+        self.h = C.c_void_p()
+        ident = C.create_string_buffer(128)
+        if world > 1:
+            if rank == 0:
+                _chk(_lib.hmgp_comm_unique_id(ident))
+            raw = bcast(ident.raw if rank == 0 else None)
+            ident = C.create_string_buffer(bytes(raw), 128)
+        _chk(_lib.hmgp_comm_create(ctx.h, ident, rank, world, C.byref(self.h)))
+
+    def close(self):
+        from . import _lib
+        if self.h:
+            _lib.hmgp_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def shard_c(thetas, rank, world):
+    """hmgp_sweep_shard: the same ν-major round-robin as ``shard`` above."""
+    import ctypes as C
+
+    from . import Matern, _chk, _i, _lib
+    th = np.asarray(thetas, dtype=np.float64).reshape(-1, 4)
+    arr = (Matern * max(1, len(th)))(*[Matern(*t) for t in th])
+    idx = np.empty(max(1, len(th)), dtype=np.int32)
+    cnt = C.c_int()
+    _chk(_lib.hmgp_sweep_shard(arr, len(th), rank, world, _i(idx), C.byref(cnt)))
+    return idx[: cnt.value].copy()
+
+
+def sweep_host(geom, z, thetas, idx, cfg, ctx):
+    """hmgp_loglik_sweep: θ[idx] on this rank's GPU, z a HOST array (uploaded once).
+    Returns the ctypes result rows (for hmgp_sweep_gather) and the value table."""
+    import ctypes as C
+
+    from . import Matern, _LogLik, _chk, _d, _lib
+    z = np.ascontiguousarray(z, dtype=np.float64)
+    k = len(idx)
+    arr = (Matern * max(1, k))(*[Matern(*thetas[i]) for i in idx])
+    res = (_LogLik * max(1, k))()
+    c = cfg.c()
+    _chk(_lib.hmgp_loglik_sweep(ctx.h, geom.h, _d(z), arr, k, C.byref(c), res))
+    return res, np.array([[r.loglik, r.logdet, r.quad_form, r.status] for r in res[:k]]).reshape(k, 4)
+
+
+def gather_c(ctx, comm, idx, res, n_theta):
+    """hmgp_sweep_gather: ONE NCCL all-gather -> (n_theta, 4) table on every rank."""
+    from . import _LogLik, _chk, _i, _lib
+    idx = np.ascontiguousarray(idx, dtype=np.int32)
+    table = (_LogLik * max(1, n_theta))()
+    _chk(_lib.hmgp_sweep_gather(ctx.h, comm.h if comm is not None else None, _i(idx), res, len(idx),
+                                n_theta, table))
+    return np.array([[r.loglik, r.logdet, r.quad_form, r.status] for r in table[:n_theta]]).reshape(n_theta, 4)
+
+
+def predict_gather_c(ctx, comm, local, m):
+    """hmgp_predict_gather: ONE NCCL all-gather of the contiguous prediction slices."""
+    from . import _chk, _d, _lib
+    local = np.ascontiguousarray(local, dtype=np.float64)
+    out = np.empty(max(1, m))
+    loc = local if local.size else np.zeros(1)
+    _chk(_lib.hmgp_predict_gather(ctx.h, comm.h if comm is not None else None, _d(loc), m, _d(out)))
+    return out[:m]
