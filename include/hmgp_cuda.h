@@ -229,6 +229,11 @@ int hmgp_sweep_gather(hmgp_ctx* ctx, hmgp_comm* comm, const int32_t* idx, const 
    every rank; m == 0 returns without a collective. */
 int hmgp_predict_gather(hmgp_ctx* ctx, hmgp_comm* comm, const double* local, int m, double* out);
 
+/* Free the device workspaces the library keeps between calls: the calling
+   thread's temporary arena and captured factorization, and those of the
+   persistent θ-batch workers.  The next call allocates them again. */
+void hmgp_release_workspace(void);
+
 /* ------------------------------------------------------- instrumentation */
 /* the context's CUDA stream (cudaStream_t), for event timing by callers */
 int hmgp_ctx_stream(hmgp_ctx* ctx, void** stream);

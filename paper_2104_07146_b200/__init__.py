@@ -153,6 +153,7 @@ _sig("hmgp_loglik_batch", C.c_int, [_vp, _vp, C.c_void_p, C.POINTER(Matern), C.c
                                     C.POINTER(_LogLik)])
 _sig("hmgp_loglik_sweep", C.c_int, [_vp, _vp, _dp, C.POINTER(Matern), C.c_int, C.POINTER(_Config),
                                     C.POINTER(_LogLik)])
+_sig("hmgp_release_workspace", None, [])
 _sig("hmgp_sweep_shard", C.c_int, [C.POINTER(Matern), C.c_int, C.c_int, C.c_int, _ip, C.POINTER(C.c_int)])
 _sig("hmgp_predict_range", C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)])
 _sig("hmgp_comm_unique_id", C.c_int, [C.c_void_p])
@@ -226,6 +227,11 @@ class Context:
 
     def launches(self):
         return int(_lib.hmgp_kernel_launches(self.h))
+
+
+def release_workspace():
+    """hmgp_release_workspace: free the arenas / captured factorizations kept between calls."""
+    _lib.hmgp_release_workspace()
 
 
 _default_ctx = None

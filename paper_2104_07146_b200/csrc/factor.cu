@@ -23,6 +23,7 @@
 #include <array>
 #include <chrono>
 #include <map>
+#include <mutex>
 #include <set>
 #include <string>
 #include <type_traits>
@@ -131,8 +132,64 @@ struct Arena {
   ~Arena() { free_all(); }
 };
 
+// Descriptor storage of a captured factorization (CUDA graph): the item lists are
+// uploaded once, on a stream of their own (outside the capture), into chunks that
+// live as long as the graph; replays read them in place.
+struct DescStore {
+  struct Chunk {
+    char* h = nullptr;
+    char* d = nullptr;
+    size_t cap = 0;
+  };
+  std::vector<Chunk> chunks;
+  size_t off = 0, bytes = 0;
+  cudaStream_t up = nullptr;
+  static constexpr size_t kChunk = (size_t)32 << 20;
+  void* put(const void* src, size_t n) {
+    const size_t a = (n + 255) & ~size_t(255);
+    if (chunks.empty() || off + a > chunks.back().cap) {
+      Chunk c;
+      c.cap = std::max(kChunk, a);
+      HMGP_CUDA(cudaMallocHost(&c.h, c.cap));
+      HMGP_CUDA(dev_malloc_plain((void**)&c.d, c.cap));
+      chunks.push_back(c);
+      off = 0;
+    }
+    if (!up) HMGP_CUDA(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
+    Chunk& c = chunks.back();
+    std::memcpy(c.h + off, src, n);
+    HMGP_CUDA(cudaMemcpyAsync(c.d + off, c.h + off, n, cudaMemcpyHostToDevice, up));
+    void* r = c.d + off;
+    off += a;
+    bytes += a;
+    return r;
+  }
+  void finish_upload() {  // after the capture: wait for the copies, drop the pinned side
+    if (up) HMGP_CUDA(cudaStreamSynchronize(up));
+    for (Chunk& c : chunks)
+      if (c.h) {
+        cudaFreeHost(c.h);
+        c.h = nullptr;
+      }
+  }
+  void clear() {
+    if (up) cudaStreamSynchronize(up);
+    for (Chunk& c : chunks) {
+      if (c.h) cudaFreeHost(c.h);
+      if (c.d) cudaFree(c.d);
+    }
+    chunks.clear();
+    off = bytes = 0;
+  }
+  ~DescStore() {
+    clear();
+    if (up) cudaStreamDestroy(up);
+  }
+};
+
 // Pinned host ring -> device ring for item descriptors (stream ordered).
 struct Stager {
+  DescStore* store = nullptr;  // set while a factorization is being captured
   char* h = nullptr;
   char* d = nullptr;
   size_t cap = 0, off = 0;
@@ -142,6 +199,7 @@ struct Stager {
   std::vector<cudaStream_t> used;     // streams that may still read the ring
   void use(cudaStream_t s) {
     st = s;
+    if (store) return;
     if (std::find(used.begin(), used.end(), s) == used.end()) used.push_back(s);
   }
   void init(size_t bytes, cudaStream_t s) {  // persistent across factorizations
@@ -172,6 +230,7 @@ struct Stager {
   }
   template <class T>
   const T* put(const std::vector<T>& v) {
+    if (store) return static_cast<const T*>(store->put(v.data(), v.size() * sizeof(T)));
     const size_t bytes = (v.size() * sizeof(T) + 255) & ~size_t(255);
     if (bytes > cap) throw Error(6, "item batch exceeds staging ring");
     if (off + bytes > cap) {  // wrap: every stream that read the ring must be done
@@ -253,8 +312,13 @@ thread_local SidePool g_side;
 thread_local size_t t_last_arena_peak = 0, t_last_pool_bytes = 0;
 thread_local bool t_one_stream = false;
 
-// release this host thread's factorization temporaries (θ-batch workers)
-void release_thread_workspace() { g_arena.free_all(); }
+// release this host thread's factorization temporaries (θ-batch workers); the
+// captured factorization (below) lives in the arena, so it goes first
+void drop_thread_graph();
+void release_thread_workspace() {
+  drop_thread_graph();
+  g_arena.free_all();
+}
 
 struct Engine {
   Factor& F;
@@ -1876,7 +1940,7 @@ struct Engine {
     if (kind(a) == DENSE) {
       const LeafDev& l = LF(a);
       A(l.a, 1);
-      run("leaf", [&](cudaStream_t s) { launch_leaf_factor(l.a, l.m, rb(a), ldl ? 1 : 0, F.d_d, F.clamp_tol, F.d_status, s); });
+      run("leaf", [&](cudaStream_t s) { launch_leaf_factor(l.a, l.m, rb(a), ldl ? 1 : 0, F.d_d, -1.0, F.d_status, s); });
       stat(S_LEAF, 1);
       return;
     }
@@ -2412,12 +2476,14 @@ static void solve_sweep(const Factor& F, double* v, bool trans, cudaStream_t st)
 
 // ------------------------------------------------------------ Factor API --
 Factor::~Factor() {
-  dev_free(pool);
-  dev_free(d_leaf);
-  dev_free(d_rank);
-  dev_free(d_compact);
-  dev_free(d_d);
-  dev_free(d_status);
+  if (!borrowed) {  // (a graph-replayed factor borrows these from the thread's graph cache)
+    dev_free(pool);
+    dev_free(d_leaf);
+    dev_free(d_rank);
+    dev_free(d_compact);
+    dev_free(d_d);
+    dev_free(d_status);
+  }
   dev_free(d_fwd);
   dev_free(d_bwd);
   dev_free(d_work);
@@ -2435,7 +2501,292 @@ Factor::~Factor() {
 struct CapMemo {
   int n = -1, dim = 0, leaves = -1, tcap = 256, grow = 1;
 };
-static thread_local CapMemo t_cap_memo;
+// shared by the host threads (θ-batch workers start from what the caller's first
+// θ found); read / written under g_memo_mu
+static CapMemo g_cap_memo;
+static std::mutex g_memo_mu;
+static CapMemo memo_get() {
+  std::lock_guard<std::mutex> lk(g_memo_mu);
+  return g_cap_memo;
+}
+static void memo_set(const CapMemo& m) {
+  std::lock_guard<std::mutex> lk(g_memo_mu);
+  g_cap_memo = m;
+}
+
+// ------------------------------------------------ captured factorization ---
+// The host walk of the factorization depends only on the block structure, the
+// capacities and the configuration — never on θ (ranks stay on the device, the
+// pivot clamp is read from the status block).  For the ephemeral factor of an
+// L(θ) / predict call the walk is therefore captured ONCE per host thread into
+// a CUDA graph over buffers the thread keeps (factor pool at fixed capacities,
+// rank arrays, arena, descriptor store), and every later evaluation on the same
+// structure clones its H-matrix into those buffers and replays the graph: one
+// cudaGraphLaunch instead of ~85 000 launches + ~99 000 descriptor copies at C3.
+// Same kernels, same arguments, same order => bit-identical results.  A θ whose
+// assembled ranks outgrow the captured capacities re-captures with larger ones;
+// a device-detected overflow falls back to the stream path with its redo loop.
+thread_local bool t_graph_ok = false;
+
+struct GraphCache {
+  bool valid = false;
+  uint64_t key = 0;
+  int tcap = 0, grow = 0, L = 0, n = 0;
+  bool ldl = false, one_stream = false;
+  double eps = 0.0;
+  std::vector<int> caps;
+  std::vector<size_t> off;
+  size_t total = 0;
+  double* pool = nullptr;
+  LeafDev* d_leaf = nullptr;
+  int* d_rank = nullptr;
+  int* d_compact = nullptr;
+  double* d_d = nullptr;
+  LeafFactorStatus* d_status = nullptr;
+  CloneItem* d_ci = nullptr;
+  size_t ci_cap = 0;
+  std::vector<CloneItem> ci_host;
+  LeafFactorStatus s0{};
+  int* d_err = nullptr;
+  char* arena_base = nullptr;
+  size_t arena_cap = 0, arena_peak = 0;
+  cudaGraphExec_t exec = nullptr;
+  size_t nodes = 0;
+  long long replays = 0;
+  DescStore desc;
+  void drop_graph() {
+    if (exec) cudaGraphExecDestroy(exec);
+    exec = nullptr;
+    desc.clear();
+    valid = false;
+  }
+  void free_buffers() {
+    drop_graph();
+    cudaFree(pool);
+    cudaFree(d_leaf);
+    cudaFree(d_rank);
+    cudaFree(d_compact);
+    cudaFree(d_d);
+    cudaFree(d_status);
+    cudaFree(d_ci);
+    pool = nullptr;
+    d_leaf = nullptr;
+    d_rank = d_compact = nullptr;
+    d_d = nullptr;
+    d_status = nullptr;
+    d_ci = nullptr;
+    ci_cap = 0;
+    total = 0;
+    L = n = 0;
+    key = 0;
+    caps.clear();
+  }
+  ~GraphCache() { free_buffers(); }
+};
+static thread_local GraphCache t_gc;
+void drop_thread_graph() { t_gc.free_buffers(); }
+
+static uint64_t structure_key(const HMat& H) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](uint64_t v) {
+    h ^= v;
+    h *= 1099511628211ull;
+  };
+  const Geometry& G = *H.g;
+  mix((uint64_t)G.n);
+  mix((uint64_t)G.dim);
+  mix(H.leaf.size());
+  for (const LeafDev& l : H.leaf) mix(((uint64_t)l.m << 34) ^ ((uint64_t)l.n << 4) ^ (uint64_t)l.kind);
+  for (const HNode& nd : H.nodes) mix(((uint64_t)(uint32_t)nd.row << 32) ^ ((uint64_t)(uint32_t)nd.col << 2) ^ (uint64_t)nd.kind);
+  return h;
+}
+
+// Returns 0 when the factorization ran (captured or replayed) without a capacity
+// overflow; 1: could not capture (take the stream path at the same capacities);
+// 2: overflow detected on device (take the stream path at doubled capacities).
+static int factorize_graph(Factor& F, HMat& H, cudaStream_t st, size_t arena_bytes, int tcap, int grow) {
+  GraphCache& gc = t_gc;
+  const Geometry& G = *H.g;
+  const int L = (int)H.leaf.size();
+  const uint64_t key = structure_key(H);
+  std::vector<int> need(L, 0);
+  bool fits = gc.valid && gc.key == key && gc.tcap == tcap && gc.grow == grow && gc.ldl == F.ldl &&
+              gc.eps == F.eps && gc.one_stream == t_one_stream && gc.arena_base == g_arena.base &&
+              gc.arena_cap == g_arena.cap && (int)gc.caps.size() == L;
+  for (int k = 0; k < L; ++k) {
+    const LeafDev& l = H.leaf[k];
+    if (l.kind == DENSE) continue;
+    need[k] = std::min(std::min(l.m, l.n) + 16, l.cap * grow);
+    if (fits && need[k] > gc.caps[k]) fits = false;
+  }
+  if (!fits) {
+    // new layout: this θ's capacities with slack, never below the previous ones
+    const bool same = gc.key == key && (int)gc.caps.size() == L;
+    std::vector<int> caps(L, 0);
+    std::vector<size_t> off(L);
+    size_t total = 0;
+    for (int k = 0; k < L; ++k) {
+      const LeafDev& l = H.leaf[k];
+      off[k] = total;
+      if (l.kind == DENSE) {
+        total += (size_t)l.m * l.n;
+      } else {
+        int c = need[k] + need[k] / 4 + 8;
+        if (same) c = std::max(c, gc.caps[k]);
+        caps[k] = std::min(std::min(l.m, l.n) + 16, c);
+        total += (size_t)(l.m + l.n) * caps[k];
+      }
+    }
+    gc.drop_graph();
+    if (total != gc.total || !gc.pool) {
+      cudaFree(gc.pool);
+      gc.pool = nullptr;
+      gc.total = 0;
+      if (dev_malloc_plain((void**)&gc.pool, std::max<size_t>(1, total) * 8) != cudaSuccess) {
+        cudaGetLastError();
+        gc.pool = nullptr;
+        return 1;
+      }
+      gc.total = total;
+    }
+    if (L != gc.L || G.n != gc.n || !gc.d_leaf) {
+      cudaFree(gc.d_leaf);
+      cudaFree(gc.d_rank);
+      cudaFree(gc.d_compact);
+      cudaFree(gc.d_d);
+      cudaFree(gc.d_status);
+      gc.d_leaf = nullptr;
+      HMGP_CUDA(dev_malloc_plain((void**)&gc.d_leaf, sizeof(LeafDev) * std::max(L, 1)));
+      HMGP_CUDA(dev_malloc_plain((void**)&gc.d_rank, 4 * std::max(L, 1)));
+      HMGP_CUDA(dev_malloc_plain((void**)&gc.d_compact, 4 * std::max(L, 1)));
+      HMGP_CUDA(dev_malloc_plain((void**)&gc.d_d, 8ull * G.n));
+      HMGP_CUDA(dev_malloc_plain((void**)&gc.d_status, sizeof(LeafFactorStatus)));
+      gc.L = L;
+      gc.n = G.n;
+    }
+    gc.key = key;
+    gc.caps = caps;
+    gc.off = off;
+    gc.tcap = tcap;
+    gc.grow = grow;
+    gc.ldl = F.ldl;
+    gc.eps = F.eps;
+    gc.one_stream = t_one_stream;
+  }
+  // the factor borrows the cache's buffers
+  F.leaf = H.leaf;
+  gc.ci_host.clear();
+  for (int k = 0; k < L; ++k) {
+    LeafDev& l = F.leaf[k];
+    if (l.kind != DENSE) l.cap = gc.caps[k];
+    l.a = gc.pool + gc.off[k];
+    l.b = l.kind == DENSE ? nullptr : l.a + (size_t)l.m * l.cap;
+    const LeafDev& sl = H.leaf[k];
+    if (l.kind == DENSE) {
+      gc.ci_host.push_back(CloneItem{sl.a, l.a, (size_t)l.m * l.n});
+    } else if (H.rank_host[k] > 0) {
+      gc.ci_host.push_back(CloneItem{sl.a, l.a, (size_t)l.m * H.rank_host[k]});
+      gc.ci_host.push_back(CloneItem{sl.b, l.b, (size_t)l.n * H.rank_host[k]});
+    }
+  }
+  F.pool = gc.pool;
+  F.d_leaf = gc.d_leaf;
+  F.d_rank = gc.d_rank;
+  F.d_compact = gc.d_compact;
+  F.d_d = gc.d_d;
+  F.d_status = gc.d_status;
+  F.borrowed = true;
+  // per-evaluation state: payload clone (hblock.cpp:17-28, compact_cols = 0), ranks, status
+  if (!fits) HMGP_CUDA(cudaMemcpyAsync(gc.d_leaf, F.leaf.data(), sizeof(LeafDev) * L, cudaMemcpyHostToDevice, st));
+  if (!gc.ci_host.empty()) {
+    if (gc.ci_host.size() > gc.ci_cap) {
+      cudaFree(gc.d_ci);
+      gc.ci_cap = gc.ci_host.size() + gc.ci_host.size() / 2;
+      HMGP_CUDA(dev_malloc_plain((void**)&gc.d_ci, sizeof(CloneItem) * gc.ci_cap));
+    }
+    HMGP_CUDA(cudaMemcpyAsync(gc.d_ci, gc.ci_host.data(), sizeof(CloneItem) * gc.ci_host.size(),
+                              cudaMemcpyHostToDevice, st));
+    k_clone<<<(int)gc.ci_host.size(), 256, 0, st>>>(gc.d_ci);
+    HMGP_LAUNCH_CHECK();
+  }
+  HMGP_CUDA(cudaMemcpyAsync(F.d_rank, H.d_rank, 4ull * L, cudaMemcpyDeviceToDevice, st));
+  HMGP_CUDA(cudaMemsetAsync(F.d_compact, 0, 4ull * L, st));
+  HMGP_CUDA(cudaMemsetAsync(F.d_d, 0, 8ull * G.n, st));
+  gc.s0 = LeafFactorStatus{INT_MAX, 0, 0, 0, 0.0, INFINITY, F.clamp_tol};
+  HMGP_CUDA(cudaMemcpyAsync(F.d_status, &gc.s0, sizeof(gc.s0), cudaMemcpyHostToDevice, st));
+  int err = 0;
+  if (fits) {
+    HMGP_CUDA(cudaMemsetAsync(gc.d_err, 0, 4, st));
+    HMGP_CUDA(cudaGraphLaunch(gc.exec, st));
+    g_launches.fetch_add(gc.nodes);
+    ++gc.replays;
+  } else {
+    std::vector<int> lr;
+    for (int k = 0; k < L; ++k)
+      if (F.leaf[k].kind == LOWRANK) lr.push_back(F.leaf_node[k]);
+    cudaGraph_t graph = nullptr;
+    bool ok = true;
+    try {
+      Engine E(F, st, arena_bytes, tcap, false);  // (re)sizes the arena, zeroes d_err on st
+      gc.d_err = E.d_err;
+      E.sg.store = &gc.desc;
+      HMGP_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+      try {
+        E.factor_diag(0);
+        E.compress(lr);  // compress_all (hfactor.cpp:321-328)
+      } catch (const Error&) {
+        ok = false;  // arena too small for this schedule: the stream path handles it
+      }
+      const cudaError_t ce = cudaStreamEndCapture(st, &graph);
+      E.sg.store = nullptr;
+      if (ce != cudaSuccess) {
+        cudaGetLastError();
+        ok = false;
+      }
+      gc.arena_peak = E.ar.peak;
+    } catch (...) {
+      g_stager.store = nullptr;
+      if (graph) cudaGraphDestroy(graph);
+      gc.drop_graph();
+      throw;
+    }
+    if (ok) {
+      gc.desc.finish_upload();
+      ok = cudaGraphInstantiate(&gc.exec, graph, 0) == cudaSuccess;
+      if (!ok) cudaGetLastError();
+    }
+    if (ok) {
+      size_t nn = 0;
+      cudaGraphGetNodes(graph, nullptr, &nn);
+      gc.nodes = nn;
+    }
+    if (graph) cudaGraphDestroy(graph);
+    if (!ok) {
+      gc.drop_graph();
+      HMGP_CUDA(cudaStreamSynchronize(st));
+      return 1;
+    }
+    gc.arena_base = g_arena.base;
+    gc.arena_cap = g_arena.cap;
+    gc.valid = true;
+    if (getenv("HMGP_TIMING"))
+      fprintf(stderr, "[hmgp] captured factorization: %zu graph nodes, %.1f MB descriptors, arena peak %.2f GB\n",
+              gc.nodes, gc.desc.bytes / 1e6, gc.arena_peak / 1e9);
+    HMGP_CUDA(cudaGraphLaunch(gc.exec, st));
+  }
+  phase_mark(PH_FACTOR);
+  HMGP_CUDA(cudaMemcpyAsync(&err, gc.d_err, 4, cudaMemcpyDeviceToHost, st));
+  HMGP_CUDA(cudaStreamSynchronize(st));
+  F.arena_peak = gc.arena_peak;
+  t_last_arena_peak = gc.arena_peak;
+  g_work.arena_peak = std::max(g_work.arena_peak, (double)gc.arena_peak);
+  g_work.factor_attempts += 1;
+  if (err) {  // capacity overflow detected on device: the stream path redoes it with larger capacities
+    gc.drop_graph();
+    return 2;
+  }
+  return 0;
+}
 
 void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size_t arena_bytes) {
   NvtxRange nvtx_range("hmgp:factorize(K6-K9)");
@@ -2447,12 +2798,6 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
   F.leaf_node = H.leaf_node;
   const int L = (int)H.leaf.size();
   t_last_pool_bytes = H.pool_doubles * 8;
-  // clone payload (hblock.cpp:17-28): same layout, new pool; compact_cols = 0
-  F.d_leaf = static_cast<std::remove_reference_t<decltype(F.d_leaf)>>(dev_alloc(sizeof(LeafDev) * std::max(L, 1)));
-  F.d_rank = static_cast<std::remove_reference_t<decltype(F.d_rank)>>(dev_alloc(4 * std::max(L, 1)));
-  F.d_compact = static_cast<std::remove_reference_t<decltype(F.d_compact)>>(dev_alloc(4 * std::max(L, 1)));
-  F.d_d = static_cast<std::remove_reference_t<decltype(F.d_d)>>(dev_alloc(8ull * G.n));
-  F.d_status = static_cast<std::remove_reference_t<decltype(F.d_status)>>(dev_alloc(sizeof(LeafFactorStatus)));
   F.clamp_tol = 1e-14 * H.max_diag;  // hfactor.cpp:349
 
   // Temporaries are sized with a width capacity TCAP; a product wider than that
@@ -2470,10 +2815,12 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
     tcap0 = 512;
     start_3d = true;
   }
-  if (t_cap_memo.n == G.n && t_cap_memo.dim == G.dim && t_cap_memo.leaves == L) {
+  const CapMemo memo = memo_get();
+  const bool memo_hit = memo.n == G.n && memo.dim == G.dim && memo.leaves == L;
+  if (memo_hit) {
     start_3d = false;
-    grow = std::max(grow, t_cap_memo.grow);
-    tcap0 = std::max(tcap0, t_cap_memo.tcap);
+    grow = std::max(grow, memo.grow);
+    tcap0 = std::max(tcap0, memo.tcap);
   }
   size_t pool_doubles = 0;
   struct OneStreamScope {  // restores t_one_stream when factorize leaves
@@ -2492,7 +2839,38 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
   // off by default.
   bool use_dag = getenv("HMGP_STATS") == nullptr && getenv("HMGP_SERIAL") == nullptr &&
                  ((getenv("HMGP_DAG") && atoi(getenv("HMGP_DAG")) != 0) || getenv("HMGP_DAG_DIAG"));
-  for (int tcap = tcap0;;) {
+  // Ephemeral factors (L(θ), predict) on a structure whose capacities are known:
+  // captured once per host thread, replayed afterwards (factorize_graph above).
+  bool graph_done = false;
+  {
+    const char* ge = getenv("HMGP_GRAPH");
+    if (t_graph_ok && memo_hit && !use_dag && !(ge && atoi(ge) == 0) && !getenv("HMGP_STATS") &&
+        !getenv("HMGP_SERIAL")) {
+      const int rc = factorize_graph(F, H, st, arena_bytes, tcap0, grow);
+      graph_done = rc == 0;
+      if (!graph_done) {  // hand the borrowed buffers back; the stream path owns its own
+        F.pool = nullptr;
+        F.d_leaf = nullptr;
+        F.d_rank = F.d_compact = nullptr;
+        F.d_d = nullptr;
+        F.d_status = nullptr;
+        F.borrowed = false;
+        if (rc == 2) {
+          if (tcap0 >= 1024 && grow >= 16) throw Error(6, "factorize: low-rank capacity exceeded");
+          tcap0 = std::min(1024, tcap0 * 2);
+          grow *= 2;
+        }
+      }
+    }
+  }
+  if (!graph_done) {
+    F.d_leaf = static_cast<std::remove_reference_t<decltype(F.d_leaf)>>(dev_alloc(sizeof(LeafDev) * std::max(L, 1)));
+    F.d_rank = static_cast<std::remove_reference_t<decltype(F.d_rank)>>(dev_alloc(4 * std::max(L, 1)));
+    F.d_compact = static_cast<std::remove_reference_t<decltype(F.d_compact)>>(dev_alloc(4 * std::max(L, 1)));
+    F.d_d = static_cast<std::remove_reference_t<decltype(F.d_d)>>(dev_alloc(8ull * G.n));
+    F.d_status = static_cast<std::remove_reference_t<decltype(F.d_status)>>(dev_alloc(sizeof(LeafFactorStatus)));
+  }
+  for (int tcap = tcap0; !graph_done;) {
     // clone payload (hblock.cpp:17-28) into the factor's own layout; compact_cols = 0
     F.leaf = H.leaf;
     size_t total = 0;
@@ -2556,7 +2934,7 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
     HMGP_CUDA(cudaMemcpyAsync(F.d_rank, H.d_rank, 4ull * L, cudaMemcpyDeviceToDevice, st));
     HMGP_CUDA(cudaMemsetAsync(F.d_compact, 0, 4ull * L, st));
     HMGP_CUDA(cudaMemsetAsync(F.d_d, 0, 8ull * G.n, st));
-    LeafFactorStatus s0{INT_MAX, 0, 0, 0, 0.0, INFINITY};
+    LeafFactorStatus s0{INT_MAX, 0, 0, 0, 0.0, INFINITY, F.clamp_tol};
     HMGP_CUDA(cudaMemcpyAsync(F.d_status, &s0, sizeof(s0), cudaMemcpyHostToDevice, st));
     int err = 0;
     bool redo_serial = false;
@@ -2624,7 +3002,7 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
       continue;
     }
     if (!err) {
-      t_cap_memo = CapMemo{G.n, G.dim, L, tcap, grow};
+      memo_set(CapMemo{G.n, G.dim, L, tcap, grow});
       break;
     }
     if (tcap >= 1024 && grow >= 16)

@@ -43,6 +43,7 @@ struct Factor {
   double* d_part = nullptr;
   int solve_stride = 1;
   size_t arena_peak = 0;
+  bool borrowed = false;  // pool / rank arrays / d_d / d_status belong to the thread's graph cache
   ~Factor();
 };
 
@@ -64,5 +65,9 @@ extern thread_local size_t t_last_arena_peak, t_last_pool_bytes;
 // concurrency comes from the other workers, and fewer streams per worker keep
 // the hardware work queues from being shared)
 extern thread_local bool t_one_stream;
+// the factor of the next factorize() on this thread is ephemeral (destroyed before
+// the thread factorizes again): its launch sequence may be captured / replayed as a
+// CUDA graph over buffers the thread keeps (factor.cu, "captured factorization")
+extern thread_local bool t_graph_ok;
 
 }  // namespace hmgp_gpu

@@ -621,6 +621,7 @@ __device__ __forceinline__ void atomic_min_double(double* addr, double v) {
 // (hfactor.cpp:22-73); the leaf lives in dynamic shared memory when it fits.
 __global__ void k_leaf_factor(double* __restrict__ Dg, int b, int base, int ldl, double* __restrict__ d,
                               double clamp_tol, LeafFactorStatus* st, int use_smem) {
+  if (clamp_tol < 0.0) clamp_tol = st->clamp_tol;  // per-evaluation value (graph replay)
   extern __shared__ double sm[];
   __shared__ double red[32];
   __shared__ double s_piv;
@@ -702,6 +703,7 @@ __global__ void __launch_bounds__(kLeafRegThreads) k_leaf_factor_reg(double* __r
                                                                      double* __restrict__ d,
                                                                      double clamp_tol,
                                                                      LeafFactorStatus* st) {
+  if (clamp_tol < 0.0) clamp_tol = st->clamp_tol;  // per-evaluation value (graph replay)
   constexpr int G = kLeafRegThreads / BMAX;
   constexpr int kLeafRegMaxK = BMAX / G;  // columns per thread
   __shared__ double col[2][BMAX];

@@ -112,6 +112,10 @@ struct LeafFactorStatus {
   int pad;
   double fail_val;
   double min_pivot;
+  // pivot clamp 1e-14 * max_diag (hfactor.cpp:349), set per evaluation: the leaf
+  // kernels read it here when launched with clamp_tol < 0, so that a captured
+  // launch sequence carries no θ-dependent scalar
+  double clamp_tol;
 };
 
 void launch_gemm(const GemmItem* d_items, int count, int max_tiles, cudaStream_t st);

@@ -6,6 +6,8 @@
 #include <chrono>
 #include <exception>
 #include <mutex>
+#include <condition_variable>
+#include <functional>
 #include <thread>
 #include <climits>
 #include <cmath>
@@ -69,6 +71,94 @@ double now() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
+struct GraphOkScope {
+  GraphOkScope() { t_graph_ok = true; }
+  ~GraphOkScope() { t_graph_ok = false; }
+};
+
+// Persistent θ-batch workers: host threads that outlive one hmgp_loglik_batch
+// call, each with its own stream, temporary arena and captured factorization
+// (factor.cu), so that the next batch on the same block structure replays the
+// workers' CUDA graphs instead of walking the recursion again.
+class BatchPool {
+ public:
+  static BatchPool& get() {
+    static BatchPool p;
+    return p;
+  }
+  // run job(ctx) on workers [0, T) and wait for all of them
+  void run(int T, int device, const std::function<void(hmgp_ctx*)>& job) {
+    std::unique_lock<std::mutex> lk(mu_);
+    while ((int)ws_.size() < T) {
+      ws_.emplace_back(new Worker());
+      Worker* w = ws_.back().get();
+      w->th = std::thread([this, w, device] { loop(w, device); });
+    }
+    pending_ = T;
+    for (int i = 0; i < T; ++i) {
+      ws_[i]->job = job;
+      ws_[i]->has_job = true;
+    }
+    cv_.notify_all();
+    done_.wait(lk, [&] { return pending_ == 0; });
+  }
+  // every worker frees its arena, graph and stream-ordered buffers
+  void release() {
+    if (ws_.empty()) return;
+    const int T = (int)ws_.size();
+    run(T, -1, [](hmgp_ctx*) { release_thread_workspace(); });
+    key_ = 0;
+    share_ = 0;
+    per_ = 0;
+    warm_ = 0;
+  }
+  int size() const { return (int)ws_.size(); }
+  uint64_t key_ = 0;   // structure the workers' workspaces were sized for
+  size_t share_ = 0;   // arena bytes per worker
+  size_t per_ = 0;     // device bytes per worker (arena + payloads)
+  int warm_ = 0;       // workers holding a workspace
+  std::mutex batch_mu_;
+
+ private:
+  struct Worker {
+    std::thread th;
+    std::function<void(hmgp_ctx*)> job;
+    bool has_job = false;
+    hmgp_ctx ctx;
+  };
+  void loop(Worker* w, int device) {
+    if (device >= 0) cudaSetDevice(device);
+    w->ctx.device = device;
+    cudaStreamCreateWithFlags(&w->ctx.stream, cudaStreamNonBlocking);
+    for (;;) {
+      std::function<void(hmgp_ctx*)> job;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return w->has_job || stop_; });
+        if (stop_) return;
+        job = w->job;
+        w->has_job = false;
+      }
+      job(&w->ctx);
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (--pending_ == 0) done_.notify_all();
+      }
+    }
+  }
+  ~BatchPool() {
+    // process exit: the workers stay parked (their thread-local CUDA objects must
+    // not be destroyed while the runtime is shutting down)
+    for (auto& w : ws_)
+      if (w->th.joinable()) w->th.detach();
+  }
+  std::mutex mu_;
+  std::condition_variable cv_, done_;
+  std::vector<std::unique_ptr<Worker>> ws_;
+  int pending_ = 0;
+  bool stop_ = false;
+};
+
 // L(θ) on a built geometry with device z (original order)
 void loglik_on_geom(hmgp_ctx* ctx, Geometry& g, const double* d_z, const hmgp_matern* th,
                     const hmgp_config* cfg, hmgp_loglik_result* res) {
@@ -80,7 +170,11 @@ void loglik_on_geom(hmgp_ctx* ctx, Geometry& g, const double* d_z, const hmgp_ma
   assemble(h, g, make_matern(th->sigma2, th->ell, th->nu, th->tau2), cfg->rank.eps,
            cfg->rank.mode == 1, cfg->rank.rank, cfg->rank.max_rank > 0 ? cfg->rank.max_rank : 256,
            ctx->stream, nullptr);
-  auto f = do_factorize(h, factor_eps(cfg), cfg->form == 1, ctx->stream);
+  std::unique_ptr<Factor> f;
+  {
+    GraphOkScope ephemeral;  // f dies before this thread factorizes again
+    f = do_factorize(h, factor_eps(cfg), cfg->form == 1, ctx->stream);
+  }
   const int n = g.n;
   res->n = n;
   res->logdet = factor_log_det(*f, ctx->stream);
@@ -329,56 +423,110 @@ int hmgp_loglik_batch(hmgp_ctx* ctx, hmgp_geom* g, const double* d_z, const hmgp
       res[t].seconds = now() - t0;
     };
     if (ntheta <= 0) return HMGP_OK;
-    one(ctx, 0);
-    int T = 8;
-    if (const char* e = getenv("HMGP_BATCH_THREADS")) T = std::max(1, atoi(e));
-    T = std::min(T, ntheta - 1);
-    if (T <= 1) {
-      for (int t = 1; t < ntheta; ++t) one(ctx, t);
-      return HMGP_OK;
+    BatchPool& pool = BatchPool::get();
+    std::lock_guard<std::mutex> one_batch(pool.batch_mu_);  // batches of different callers take turns
+    // structure of this batch (workers keep workspaces sized for one structure)
+    const uint64_t bkey = ((uint64_t)g->g.n << 32) ^ ((uint64_t)g->g.nbeg.size() << 8) ^ (uint64_t)cfg->leaf_size ^
+                          ((uint64_t)(cfg->form == 1) << 7);
+    if (pool.key_ != 0 && pool.key_ != bkey) {
+      pool.release();
+      dev_pool_trim();
     }
-    // per worker: the first θ's arena peak with headroom, plus the H-matrix and
-    // factor payloads; the caller's own arena is released first
-    // (a first θ that failed before its factorization leaves no peak: assume 8 GiB)
-    const size_t peak = t_last_arena_peak ? t_last_arena_peak : ((size_t)8 << 30);
-    const size_t pool = t_last_pool_bytes;
-    HMGP_CUDA(cudaStreamSynchronize(ctx->stream));
-    release_thread_workspace();
-    dev_pool_trim();
+    int T = 16;
+    if (const char* e = getenv("HMGP_BATCH_THREADS")) T = std::max(1, atoi(e));
+    // workers that already hold a workspace for this structure take the whole
+    // batch; otherwise the first θ runs alone on the caller's stream and sizes it
+    const bool warm_start = pool.key_ == bkey && pool.warm_ > 0 && ntheta > 1 && T > 1;
+    int first = 0;
+    size_t share = pool.share_, per = pool.per_;
+    if (!warm_start) {
+      one(ctx, 0);
+      first = 1;
+      T = std::min(T, ntheta - 1);
+      if (T <= 1) {
+        for (int t = 1; t < ntheta; ++t) one(ctx, t);
+        return HMGP_OK;
+      }
+      // per worker: the first θ's arena peak with headroom, plus the H-matrix and
+      // factor payloads
+      // (a first θ that failed before its factorization leaves no peak: assume 8 GiB)
+      const size_t peak = t_last_arena_peak ? t_last_arena_peak : ((size_t)8 << 30);
+      const size_t pl = t_last_pool_bytes;
+      HMGP_CUDA(cudaStreamSynchronize(ctx->stream));
+      share = peak + peak / 2 + ((size_t)1 << 30);
+      per = share + pl * 3 + ((size_t)256 << 20);
+      if (pool.key_ == bkey && pool.share_ < share) {  // workspaces too small for this batch
+        pool.release();
+        pool.warm_ = 0;
+        dev_pool_trim();
+      }
+    } else {
+      T = std::min(T, ntheta);
+    }
     size_t fr = 0, tot = 0;
     HMGP_CUDA(cudaMemGetInfo(&fr, &tot));
-    const size_t share = peak + peak / 2 + ((size_t)1 << 30);
-    const size_t per = share + pool * 3 + ((size_t)256 << 20);
     const size_t reserve = (size_t)6 << 30;
-    const size_t usable = fr > reserve ? fr - reserve : 0;
-    T = (int)std::max<size_t>(1, std::min<size_t>(T, usable / per));
-    std::atomic<int> next{1};
+    // the caller's own arena is only needed again for the retries: release it if
+    // the workers would otherwise not fit
+    const int warm = pool.key_ == bkey ? pool.warm_ : 0;
+    auto fit_T = [&](size_t free_now) {
+      const size_t usable = free_now > reserve ? free_now - reserve : 0;
+      return (int)std::max<size_t>(1, std::min<size_t>(T, warm + usable / per));
+    };
+    if (fit_T(fr) < T) {
+      release_thread_workspace();
+      dev_pool_trim();
+      HMGP_CUDA(cudaMemGetInfo(&fr, &tot));
+    }
+    T = fit_T(fr);
+    pool.key_ = bkey;
+    pool.share_ = std::max(pool.share_, share);
+    pool.per_ = std::max(pool.per_, per);
+    const size_t wshare = pool.share_;
+    pool.warm_ = std::max(warm, T);
+    std::atomic<int> next{first};
     std::vector<std::exception_ptr> errs(T);
-    std::vector<std::thread> ws;
-    for (int w = 0; w < T; ++w)
-      ws.emplace_back([&, w] {
-        try {
-          HMGP_CUDA(cudaSetDevice(ctx->device));
-          hmgp_ctx c;
-          c.device = ctx->device;
-          HMGP_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
-          t_arena_bytes = share;
-          t_one_stream = getenv("HMGP_BATCH_SECTIONS") == nullptr;
-          for (int t; (t = next.fetch_add(1)) < ntheta;) one(&c, t);
-          HMGP_CUDA(cudaStreamSynchronize(c.stream));
-          cudaStreamDestroy(c.stream);
-          release_thread_workspace();
-        } catch (...) {
-          errs[w] = std::current_exception();
-        }
-      });
-    for (auto& th : ws) th.join();
+    std::atomic<int> widx{0};
+    pool.run(T, ctx->device, [&](hmgp_ctx* c) {
+      const int w = widx.fetch_add(1);
+      try {
+        HMGP_CUDA(cudaSetDevice(ctx->device));
+        t_arena_bytes = wshare;
+        t_one_stream = getenv("HMGP_BATCH_SECTIONS") == nullptr;
+        for (int t; (t = next.fetch_add(1)) < ntheta;) one(c, t);
+        HMGP_CUDA(cudaStreamSynchronize(c->stream));
+      } catch (...) {
+        errs[w] = std::current_exception();
+      }
+    });
+    // keep the workers' workspaces (arena + captured factorization) for the next
+    // batch on this structure while they are small next to the device memory;
+    // large ones (C3: ~30 GB per worker) go back right away
+    {
+      bool keep = (double)pool.warm_ * (double)per <= 0.3 * (double)tot;
+      if (const char* e = getenv("HMGP_BATCH_KEEP")) keep = atoi(e) != 0;
+      if (!keep) {
+        pool.release();
+        pool.warm_ = 0;
+        dev_pool_trim();
+      }
+    }
     for (auto& e : errs)
       if (e) std::rethrow_exception(e);
     std::sort(retry.begin(), retry.end());
     if (!retry.empty()) dev_pool_trim();
     for (int t : retry) one(ctx, t);  // caller thread, full workspace (arena_bytes_for)
   })
+}
+
+void hmgp_release_workspace(void) {
+  try {
+    std::lock_guard<std::mutex> one_batch(BatchPool::get().batch_mu_);
+    BatchPool::get().release();
+    release_thread_workspace();
+    dev_pool_trim();
+  } catch (...) {
+  }
 }
 
 int hmgp_predict(hmgp_ctx* ctx, const double* train, int n, int dim, const double* z1,
@@ -403,7 +551,11 @@ int hmgp_predict(hmgp_ctx* ctx, const double* train, int n, int dim, const doubl
     assemble(h, g->g, make_matern(theta->sigma2, theta->ell, theta->nu, theta->tau2), cfg->rank.eps,
              cfg->rank.mode == 1, cfg->rank.rank, cfg->rank.max_rank > 0 ? cfg->rank.max_rank : 256,
              ctx->stream, nullptr);
-    auto f = do_factorize(h, factor_eps(cfg), cfg->form == 1, ctx->stream);
+    std::unique_ptr<Factor> f;
+    {
+      GraphOkScope ephemeral;
+      f = do_factorize(h, factor_eps(cfg), cfg->form == 1, ctx->stream);
+    }
     DBuf<double> dz(n), dw(n), dtest((size_t)m * dim), dout(m);
     HMGP_CUDA(cudaMemcpyAsync(dz.p, z1, 8ull * n, cudaMemcpyHostToDevice, ctx->stream));
     HMGP_CUDA(cudaMemcpyAsync(dtest.p, test, 8ull * m * dim, cudaMemcpyHostToDevice, ctx->stream));

@@ -141,12 +141,13 @@ def _vertex(t0, f0, t1, f1, t2, f2):
     return u if math.isfinite(u) else None
 
 
-def fan_max_1d(fbatch, lo, hi, xtol, max_evals, fan=8, known: _Slice = None) -> BrentResult:
+def fan_max_1d(fbatch, lo, hi, xtol, max_evals, fan=8, known: _Slice = None,
+               max_rounds: int = None) -> BrentResult:
     """Maximise a 1-D function on (lo, hi) with batched probes.
 
     ``fbatch(list of abscissae) -> list of values``; at most ``max_evals`` new
-    values are requested, ``fan`` per round.  Stops when the bracket around the
-    best point is within 2·(√ε|x| + xtol) on both sides."""
+    values are requested in at most ``max_rounds`` batches of ``fan``.  Stops when
+    the bracket around the best point is within 2·(√ε|x| + xtol) on both sides."""
     if not lo < hi:
         raise ValueError("brent_max_1d: need lo < hi")
     if max_evals < 3:
@@ -154,6 +155,7 @@ def fan_max_1d(fbatch, lo, hi, xtol, max_evals, fan=8, known: _Slice = None) -> 
     sl = known if known is not None else _Slice(fbatch)
     start = sl.evals
     a, b = lo, hi
+    rounds = 0
     while True:
         kb = sl.best(a, b)
         x = sl.t[kb] if kb >= 0 and sl.f[kb] > _NINF else None
@@ -167,8 +169,9 @@ def fan_max_1d(fbatch, lo, hi, xtol, max_evals, fan=8, known: _Slice = None) -> 
         if x is not None and x - a <= 2.0 * tol and b - x <= 2.0 * tol:
             break
         left = max_evals - (sl.evals - start)
-        if left <= 0:
+        if left <= 0 or (max_rounds is not None and rounds >= max_rounds):
             break
+        rounds += 1
         want = []
         if x is None:
             # nothing finite yet: split the widest gaps between what is known
@@ -237,7 +240,7 @@ class OptimizerConfig:  # mle.hpp:40-49
     bracket_halfwidth: float = 8.0
     max_bracket_expansions: int = 3
     brent_xtol: float = 1e-3
-    brent_max_evals: int = 32
+    brent_max_evals: int = 32  # per 1-D search: probe BATCHES in fit (the dependent chain)
     h: HConfig = field(default_factory=HConfig)
     fan: int = 8  # probes per batch (extension: the device evaluates them concurrently)
 
@@ -338,8 +341,10 @@ def fit(locations, z, cfg: OptimizerConfig = None, ctx=None, evaluator=None,
             for _ in range(cfg.max_bracket_expansions + 1):
                 lo, hi = centre - half, centre + half
                 try:
-                    found = fan_max_1d(sl.fbatch, lo, hi, cfg.brent_xtol, cfg.brent_max_evals,
-                                       fan=cfg.fan, known=sl)
+                    # brent_max_evals bounds the DEPENDENT chain (batches), as it bounds the
+                    # reference's one-probe-at-a-time chain; a batch holds up to `fan` probes
+                    found = fan_max_1d(sl.fbatch, lo, hi, cfg.brent_xtol, cfg.brent_max_evals * cfg.fan,
+                                       fan=cfg.fan, known=sl, max_rounds=cfg.brent_max_evals)
                 except BracketInfeasible:
                     break  # nothing feasible on this bracket: leave the coordinate alone
                 if found.x - lo > edge and hi - found.x > edge:
