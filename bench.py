@@ -358,30 +358,42 @@ def extras(hm, _lib, ctx, stream, comm, rank, ws, peaks):
         # (2 MB of vector copies inside the timed region, noted).
         h3 = hm.assemble(gc3, list(C3["theta"]), hm.RankControl.fixed_accuracy(C3["eps"]))
         hb = h3.stats()["bytes"]
-        h3.matvec(zc3h)
-        ms_mv, _ = dev_ms(lambda: h3.matvec(zc3h))
+        dzv = torch.from_numpy(zc3h).to(dev)
+        dyv = torch.empty_like(dzv)
+        mv = lambda: hm._chk(_lib.hmgp_hmat_matvec_device(ctx.h, h3.h, C.c_void_p(dzv.data_ptr()),  # noqa: E731
+                                                          C.c_void_p(dyv.data_ptr())))
+        mv()
+        ms_mv, _ = dev_ms(lambda: [mv() for _ in range(5)])
+        ms_mv /= 5.0
         f3 = hm.factorize(h3, C3["eps"], C3["form"])
         fb = f3.info["storage_bytes"]
         f3.solve_lower(zc3h)
         ms_sl, _ = dev_ms(lambda: f3.solve_lower(zc3h))
         nvec = 8.0 * C3["g"] ** 2
-        out["roofline_matvec"] = {"bound": "hbm", "kernel": "H-matvec (k_leaf_matvec)", "ms": ms_mv,
-                                  "algorithmic_bytes": hb + 2 * nvec, "achieved": (hb + 2 * nvec) / ms_mv / 1e6,
+        out["roofline_matvec"] = {"bound": "hbm", "kernel": "H-matvec (k_mv_leaf + k_mv_chunk_* + k_mv_gather)",
+                                  "ms": ms_mv, "algorithmic_bytes": hb + 2 * nvec,
+                                  "achieved": (hb + 2 * nvec) / ms_mv / 1e6,
                                   "peak": hbm, "unit": "GB/s", "frac": (hb + 2 * nvec) / ms_mv / 1e6 / hbm,
-                                  "traffic": None, "note": "host-buffer call: 2 x 2 MB vector copies inside"}
+                                  "traffic": None, "note": "device vectors (hmgp_hmat_matvec_device), mean of 5 "
+                                  "back-to-back products; payload 4 GB >> L2"}
         out["roofline_solve"] = {"bound": "hbm", "kernel": "forward solve K10 (k_solve_sweep)", "ms": ms_sl,
                                  "algorithmic_bytes": fb + 2 * nvec, "achieved": (fb + 2 * nvec) / ms_sl / 1e6,
                                  "peak": hbm, "unit": "GB/s", "frac": (fb + 2 * nvec) / ms_sl / 1e6 / hbm,
                                  "traffic": None, "note": "host-buffer call: 2 x 2 MB vector copies inside"}
         del f3, h3
-    # C3 θ-throughput: the same n = 262144 problem, 5 θ per rank (ℓ nudged) through
-    # hmgp_loglik_sweep on one geometry
-    th3 = np.array([[C3["theta"][0], C3["theta"][1] * (1.0 + 0.01 * (k + 5 * rank)), C3["theta"][2], C3["theta"][3]]
-                    for k in range(5)])
-    ms3, (_, v3) = dev_ms(lambda: sw.sweep_host(gc3, zc3h, th3, list(range(5)), cfg3, ctx))
-    out["C3_theta_batch"] = {"n": C3["g"] ** 2, "thetas_per_rank": 5, "ms": ms3,
-                             "evals_per_s": 5 * ws / (ms3 / 1e3), "loglik": v3[:, 0].tolist(),
-                             "status": v3[:, 3].tolist(), "note": "5 θ via hmgp_loglik_sweep on one geometry"}
+    # C3 θ-throughput: the same n = 262144 problem through hmgp_loglik_sweep on one
+    # geometry.  A first batch of 5 θ warms the persistent workers (each captures the
+    # θ-independent factorization launch sequence as a CUDA graph); the timed batch
+    # of 8 further θ (ℓ nudged) replays the graphs concurrently.
+    th3 = np.array([[C3["theta"][0], C3["theta"][1] * (1.0 + 0.01 * (k + 13 * rank)), C3["theta"][2], C3["theta"][3]]
+                    for k in range(13)])
+    ms3w, _ = dev_ms(lambda: sw.sweep_host(gc3, zc3h, th3, list(range(5)), cfg3, ctx))
+    ms3, (_, v3) = dev_ms(lambda: sw.sweep_host(gc3, zc3h, th3, list(range(5, 13)), cfg3, ctx))
+    out["C3_theta_batch"] = {"n": C3["g"] ** 2, "thetas_per_rank": 8, "ms": ms3, "warm_batch_ms": ms3w,
+                             "evals_per_s": 8 * ws / (ms3 / 1e3), "loglik": v3[:, 0].tolist(),
+                             "status": v3[:, 3].tolist(),
+                             "note": "8 θ via hmgp_loglik_sweep on warm workers (CUDA-graph replay of the "
+                                     "captured factorization), after an untimed 5-θ batch that captures"}
     del gc3
     # C2: assembly only, n = 65536 jittered 256x256, leaf 64, eta 2, eps 1e-7; with N
     # ranks each assembles its cost-balanced leaf range (no collective); the time is

@@ -147,6 +147,9 @@ int hmgp_hmat_leaves(const hmgp_hmat* h, int32_t* out6, int64_t cap, int64_t* co
 int hmgp_hmat_leaf_data(const hmgp_hmat* h, int64_t k, double* a, double* b);
 /* HMatrix::matvec (hmatrix.cpp:244-272), original order */
 int hmgp_hmat_matvec(hmgp_ctx* ctx, const hmgp_hmat* h, const double* x, double* y);
+/* the same product with DEVICE vectors (original order), enqueued on the context's
+   stream without a synchronisation: the HBM-bound pass alone (bench roofline) */
+int hmgp_hmat_matvec_device(hmgp_ctx* ctx, const hmgp_hmat* h, const double* d_x, double* d_y);
 /* from_dense(m) (hmatrix.cpp:223-242): single Dense leaf, self-contained tree; a is n x n
  * column-major (host).  hmgp_hmat_symmetric: HMatrix::symmetric() (isApprox(m, m^T)) */
 int hmgp_hmat_from_dense(hmgp_ctx* ctx, const double* a, int n, hmgp_hmat** out);

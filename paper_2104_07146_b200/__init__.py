@@ -154,6 +154,7 @@ _sig("hmgp_loglik_batch", C.c_int, [_vp, _vp, C.c_void_p, C.POINTER(Matern), C.c
 _sig("hmgp_loglik_sweep", C.c_int, [_vp, _vp, _dp, C.POINTER(Matern), C.c_int, C.POINTER(_Config),
                                     C.POINTER(_LogLik)])
 _sig("hmgp_release_workspace", None, [])
+_sig("hmgp_hmat_matvec_device", C.c_int, [_vp, _vp, C.c_void_p, C.c_void_p])
 _sig("hmgp_sweep_shard", C.c_int, [C.POINTER(Matern), C.c_int, C.c_int, C.c_int, _ip, C.POINTER(C.c_int)])
 _sig("hmgp_predict_range", C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)])
 _sig("hmgp_comm_unique_id", C.c_int, [C.c_void_p])

@@ -3,8 +3,8 @@
 Every .cu under csrc/ is compiled to an object with
 ``-gencode arch=compute_100a,code=sm_100a -lineinfo`` and linked into
 ``paper_2104_07146_b200/libhmgp_cuda.so`` (git-ignored; it travels to the GPU box
-with the gpurun snapshot).  Objects are rebuilt only when a source or header is
-newer than the object.
+with the gpurun snapshot).  An object is rebuilt only when its source or one of the
+project headers it includes (transitively) is newer than the object.
 """
 from __future__ import annotations
 
@@ -24,14 +24,22 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", 
          "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
 
 
-def _headers():
-    return glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) + [
-        os.path.join(PKG, "..", "include", "hmgp_cuda.h")]
+def _deps(path, seen=None):
+    """The source and the project headers it includes (transitively, quoted includes)."""
+    import re
+    seen = seen if seen is not None else set()
+    path = os.path.normpath(path)
+    if path in seen or not os.path.exists(path):
+        return seen
+    seen.add(path)
+    for inc in re.findall(r'^\s*#\s*include\s+"([^"]+)"', open(path).read(), flags=re.M):
+        _deps(os.path.join(os.path.dirname(path), inc), seen)
+    return seen
 
 
 def _compile(src, verbose=False):
     obj = os.path.join(OBJ, os.path.basename(src) + ".o")
-    newest = max([os.path.getmtime(src)] + [os.path.getmtime(h) for h in _headers()])
+    newest = max(os.path.getmtime(f) for f in _deps(src))
     if os.path.exists(obj) and os.path.getmtime(obj) >= newest:
         return obj
     cmd = [NVCC] + ARCH + FLAGS + ["-c", src, "-o", obj]

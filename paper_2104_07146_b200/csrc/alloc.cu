@@ -37,6 +37,18 @@ void trim_pool() {
 
 void dev_pool_trim() { trim_pool(); }
 
+// Last resort before reporting out-of-memory: whoever keeps device workspaces
+// between calls (the persistent θ-batch workers, pipeline.cu) registers a
+// callback that gives them back.  Declared here (not in common.cuh) on purpose:
+// only pipeline.cu sets it.
+void (*g_low_memory_hook)() = nullptr;
+static bool reclaim() {
+  if (!g_low_memory_hook) return false;
+  g_low_memory_hook();
+  trim_pool();
+  return true;
+}
+
 AllocScope::AllocScope(cudaStream_t s) : prev(t_alloc_stream) {
   pool_setup();
   t_alloc_stream = s;
@@ -49,6 +61,7 @@ cudaError_t dev_malloc_plain(void** p, size_t bytes) {
     trim_pool();
     e = cudaMalloc(p, bytes);
   }
+  if (e == cudaErrorMemoryAllocation && reclaim()) e = cudaMalloc(p, bytes);
   return e;
 }
 
@@ -60,6 +73,7 @@ void* dev_alloc(size_t bytes) {
       trim_pool();
       e = cudaMallocAsync(&p, bytes, t_alloc_stream);
     }
+    if (e == cudaErrorMemoryAllocation && reclaim()) e = cudaMallocAsync(&p, bytes, t_alloc_stream);
     HMGP_CUDA(e);
     std::lock_guard<std::mutex> lk(g_mu);
     g_async.insert(p);

@@ -335,7 +335,9 @@ int build_payload(HMat& h, const Geometry& g, int bn, bool sym) {
 }
 }  // namespace
 
+void hmat_matvec_forget(const HMat* h);  // matvec.cu: drops the plan cached for this H-matrix
 HMat::~HMat() {
+  hmat_matvec_forget(this);
   dev_free(d_leaf);
   dev_free(d_rank);
   dev_free(d_compact);

@@ -403,6 +403,14 @@ int hmgp_hmat_matvec(hmgp_ctx* ctx, const hmgp_hmat* hm, const double* x, double
   })
 }
 
+int hmgp_hmat_matvec_device(hmgp_ctx* ctx, const hmgp_hmat* hm, const double* d_x, double* d_y) {
+  API_GUARD({
+    HMGP_CUDA(cudaSetDevice(ctx->device));
+    if (hm->h.partial()) throw std::invalid_argument("matvec: H-matrix is a leaf-range shard");
+    hmat_matvec_device(ctx->stream, hm->h, d_x, d_y);
+  })
+}
+
 void hmgp_hmat_destroy(hmgp_hmat* h) { delete h; }
 
 // from_dense (hmatrix.cpp:223-242): a single Dense leaf over a one-cluster tree of

@@ -2586,6 +2586,26 @@ struct GraphCache {
 static thread_local GraphCache t_gc;
 void drop_thread_graph() { t_gc.free_buffers(); }
 
+// High-water capacities per block structure, shared by the host threads: a capture
+// on any thread starts from the largest capacities any θ has needed so far, so a
+// sweep over θ with different ranks settles after the first few captures instead
+// of every worker re-capturing each time it meets a new record.
+static std::mutex g_caps_mu;
+static uint64_t g_caps_key = 0;
+static std::vector<int> g_caps_high;
+static void caps_merge(uint64_t key, std::vector<int>& caps) {  // caps <- max(caps, high); high <- caps
+  std::lock_guard<std::mutex> lk(g_caps_mu);
+  if (g_caps_key != key || g_caps_high.size() != caps.size()) {
+    g_caps_key = key;
+    g_caps_high = caps;
+    return;
+  }
+  for (size_t k = 0; k < caps.size(); ++k) {
+    caps[k] = std::max(caps[k], g_caps_high[k]);
+    g_caps_high[k] = caps[k];
+  }
+}
+
 static uint64_t structure_key(const HMat& H) {
   uint64_t h = 1469598103934665603ull;
   auto mix = [&](uint64_t v) {
@@ -2619,23 +2639,33 @@ static int factorize_graph(Factor& F, HMat& H, cudaStream_t st, size_t arena_byt
     need[k] = std::min(std::min(l.m, l.n) + 16, l.cap * grow);
     if (fits && need[k] > gc.caps[k]) fits = false;
   }
+  if (getenv("HMGP_TIMING")) {
+    int over = 0;
+    if ((int)gc.caps.size() == L)
+      for (int k = 0; k < L; ++k) over += need[k] > gc.caps[k];
+    fprintf(stderr, "[hmgp] graph %s (valid %d key %d caps-over %d arena %d one_stream %d/%d replays %lld)\n",
+            fits ? "replay" : "capture", (int)gc.valid, (int)(gc.key == key), over,
+            (int)(gc.arena_base == g_arena.base && gc.arena_cap == g_arena.cap), (int)gc.one_stream,
+            (int)t_one_stream, gc.replays);
+  }
   if (!fits) {
     // new layout: this θ's capacities with slack, never below the previous ones
     const bool same = gc.key == key && (int)gc.caps.size() == L;
     std::vector<int> caps(L, 0);
+    for (int k = 0; k < L; ++k) {
+      const LeafDev& l = H.leaf[k];
+      if (l.kind == DENSE) continue;
+      int c = need[k] + need[k] / 4 + 8;
+      if (same) c = std::max(c, gc.caps[k]);
+      caps[k] = std::min(std::min(l.m, l.n) + 16, c);
+    }
+    caps_merge(key ^ (uint64_t)grow, caps);
     std::vector<size_t> off(L);
     size_t total = 0;
     for (int k = 0; k < L; ++k) {
       const LeafDev& l = H.leaf[k];
       off[k] = total;
-      if (l.kind == DENSE) {
-        total += (size_t)l.m * l.n;
-      } else {
-        int c = need[k] + need[k] / 4 + 8;
-        if (same) c = std::max(c, gc.caps[k]);
-        caps[k] = std::min(std::min(l.m, l.n) + 16, c);
-        total += (size_t)(l.m + l.n) * caps[k];
-      }
+      total += l.kind == DENSE ? (size_t)l.m * l.n : (size_t)(l.m + l.n) * caps[k];
     }
     gc.drop_graph();
     if (total != gc.total || !gc.pool) {

@@ -73,6 +73,9 @@ void matern_batch(cudaStream_t st, const double* h, int64_t count, double sigma2
 void bessel_batch(cudaStream_t st, const double* nu, const double* x, int64_t count, int generic,
                   double* out);
 void hmat_matvec(cudaStream_t st, const HMat& h, const double* x, double* y);
+// the same product with device vectors (original order); plan cached per H-matrix (matvec.cu)
+void hmat_matvec_device(cudaStream_t st, const HMat& h, const double* d_x, double* d_y);
+void hmat_matvec_forget(const HMat* h);
 // dense diagnostics, n <= 4096 (hmatrix.cpp:274-297, hfactor.cpp:421-449), host out
 void hmat_to_dense(cudaStream_t st, const HMat& h, double* out);              // original order
 void factor_lower_dense(cudaStream_t st, const Factor& F, double* out);       // tree order

@@ -211,9 +211,17 @@ __global__ void k_permute_out(const double* __restrict__ yt, const int* __restri
 }
 
 void hmat_matvec(cudaStream_t st, const HMat& h, const double* x, double* y) {
-  NvtxRange nvtx_range("hmgp:matvec");
   const Geometry& G = *h.g;
   const int n = G.n, L = (int)h.leaf.size();
+  if (!getenv("HMGP_MATVEC_LEGACY")) {  // HBM-oriented deterministic pass (matvec.cu)
+    DBuf<double> dx(n), dy(n);
+    HMGP_CUDA(cudaMemcpyAsync(dx.p, x, 8ull * n, cudaMemcpyHostToDevice, st));
+    hmat_matvec_device(st, h, dx.p, dy.p);
+    HMGP_CUDA(cudaMemcpyAsync(y, dy.p, 8ull * n, cudaMemcpyDeviceToHost, st));
+    HMGP_CUDA(cudaStreamSynchronize(st));
+    return;
+  }
+  NvtxRange nvtx_range("hmgp:matvec(legacy)");
   std::vector<int> r0(L), c0(L);
   int maxcap = 1;
   for (int k = 0; k < L; ++k) {

@@ -20,6 +20,9 @@
 #include "factor.h"
 #include "hmgp_api.h"
 
+namespace hmgp_gpu {
+extern void (*g_low_memory_hook)();  // alloc.cu: called before an allocation reports out-of-memory
+}
 using namespace hmgp_gpu;
 
 hmgp_factor::~hmgp_factor() = default;
@@ -80,6 +83,10 @@ struct GraphOkScope {
 // call, each with its own stream, temporary arena and captured factorization
 // (factor.cu), so that the next batch on the same block structure replays the
 // workers' CUDA graphs instead of walking the recursion again.
+static thread_local bool t_pool_worker = false;
+static thread_local bool t_in_batch = false;  // this thread holds BatchPool::batch_mu_
+void pool_low_memory();
+
 class BatchPool {
  public:
   static BatchPool& get() {
@@ -102,6 +109,7 @@ class BatchPool {
     cv_.notify_all();
     done_.wait(lk, [&] { return pending_ == 0; });
   }
+  bool busy() const { return pending_ > 0; }
   // every worker frees its arena, graph and stream-ordered buffers
   void release() {
     if (ws_.empty()) return;
@@ -127,6 +135,7 @@ class BatchPool {
     hmgp_ctx ctx;
   };
   void loop(Worker* w, int device) {
+    t_pool_worker = true;
     if (device >= 0) cudaSetDevice(device);
     w->ctx.device = device;
     cudaStreamCreateWithFlags(&w->ctx.stream, cudaStreamNonBlocking);
@@ -425,6 +434,11 @@ int hmgp_loglik_batch(hmgp_ctx* ctx, hmgp_geom* g, const double* d_z, const hmgp
     if (ntheta <= 0) return HMGP_OK;
     BatchPool& pool = BatchPool::get();
     std::lock_guard<std::mutex> one_batch(pool.batch_mu_);  // batches of different callers take turns
+    struct InBatch {
+      InBatch() { t_in_batch = true; }
+      ~InBatch() { t_in_batch = false; }
+    } in_batch;
+    hmgp_gpu::g_low_memory_hook = pool_low_memory;
     // structure of this batch (workers keep workspaces sized for one structure)
     const uint64_t bkey = ((uint64_t)g->g.n << 32) ^ ((uint64_t)g->g.nbeg.size() << 8) ^ (uint64_t)cfg->leaf_size ^
                           ((uint64_t)(cfg->form == 1) << 7);
@@ -453,7 +467,10 @@ int hmgp_loglik_batch(hmgp_ctx* ctx, hmgp_geom* g, const double* d_z, const hmgp
       const size_t peak = t_last_arena_peak ? t_last_arena_peak : ((size_t)8 << 30);
       const size_t pl = t_last_pool_bytes;
       HMGP_CUDA(cudaStreamSynchronize(ctx->stream));
-      share = peak + peak / 2 + ((size_t)1 << 30);
+      // (the temporaries are sized by the structure and the capacities, not by θ:
+      // a small margin suffices, and a worker that still runs out hands its θ
+      // back to the caller's full workspace)
+      share = peak + peak / 6 + ((size_t)256 << 20);
       per = share + pl * 3 + ((size_t)256 << 20);
       if (pool.key_ == bkey && pool.share_ < share) {  // workspaces too small for this batch
         pool.release();
@@ -503,7 +520,9 @@ int hmgp_loglik_batch(hmgp_ctx* ctx, hmgp_geom* g, const double* d_z, const hmgp
     // batch on this structure while they are small next to the device memory;
     // large ones (C3: ~30 GB per worker) go back right away
     {
-      bool keep = (double)pool.warm_ * (double)per <= 0.3 * (double)tot;
+      // kept by default: an allocation that would otherwise fail takes them back
+      // (g_low_memory_hook), so holding them costs later calls nothing but a retry
+      bool keep = true;
       if (const char* e = getenv("HMGP_BATCH_KEEP")) keep = atoi(e) != 0;
       if (!keep) {
         pool.release();
@@ -519,10 +538,28 @@ int hmgp_loglik_batch(hmgp_ctx* ctx, hmgp_geom* g, const double* d_z, const hmgp
   })
 }
 
+// out-of-memory on some thread: idle workers give their workspaces back (never
+// from a worker itself, and never while a batch is running — then the failing
+// θ is retried on the caller thread instead)
+}  // extern "C"
+namespace {
+void pool_low_memory() {
+  if (t_pool_worker || t_in_batch) return;
+  BatchPool& pool = BatchPool::get();
+  if (!pool.batch_mu_.try_lock()) return;
+  std::lock_guard<std::mutex> lk(pool.batch_mu_, std::adopt_lock);
+  if (pool.busy()) return;
+  pool.release();
+}
+}  // namespace
+extern "C" {
+
 void hmgp_release_workspace(void) {
   try {
     std::lock_guard<std::mutex> one_batch(BatchPool::get().batch_mu_);
+    t_in_batch = true;
     BatchPool::get().release();
+    t_in_batch = false;
     release_thread_workspace();
     dev_pool_trim();
   } catch (...) {
