@@ -142,21 +142,29 @@ struct DescStore {
     size_t cap = 0;
   };
   std::vector<Chunk> chunks;
+  size_t cur = 0;  // chunk being filled (chunks are kept and re-used by the next capture:
+                   // cudaMalloc / cudaFree / cudaMallocHost synchronise the whole device,
+                   // which stalls every other θ-batch worker)
   size_t off = 0, bytes = 0;
   cudaStream_t up = nullptr;
   static constexpr size_t kChunk = (size_t)32 << 20;
   void* put(const void* src, size_t n) {
     const size_t a = (n + 255) & ~size_t(255);
-    if (chunks.empty() || off + a > chunks.back().cap) {
+    while (cur < chunks.size() && off + a > chunks[cur].cap) {
+      ++cur;
+      off = 0;
+    }
+    if (cur >= chunks.size()) {
       Chunk c;
       c.cap = std::max(kChunk, a);
       HMGP_CUDA(cudaMallocHost(&c.h, c.cap));
       HMGP_CUDA(dev_malloc_plain((void**)&c.d, c.cap));
       chunks.push_back(c);
+      cur = chunks.size() - 1;
       off = 0;
     }
     if (!up) HMGP_CUDA(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
-    Chunk& c = chunks.back();
+    Chunk& c = chunks[cur];
     std::memcpy(c.h + off, src, n);
     HMGP_CUDA(cudaMemcpyAsync(c.d + off, c.h + off, n, cudaMemcpyHostToDevice, up));
     void* r = c.d + off;
@@ -164,13 +172,13 @@ struct DescStore {
     bytes += a;
     return r;
   }
-  void finish_upload() {  // after the capture: wait for the copies, drop the pinned side
+  void finish_upload() {  // after the capture: wait for the copies
     if (up) HMGP_CUDA(cudaStreamSynchronize(up));
-    for (Chunk& c : chunks)
-      if (c.h) {
-        cudaFreeHost(c.h);
-        c.h = nullptr;
-      }
+  }
+  void rewind() {  // the next capture overwrites the chunks in place
+    if (up) cudaStreamSynchronize(up);
+    cur = 0;
+    off = bytes = 0;
   }
   void clear() {
     if (up) cudaStreamSynchronize(up);
@@ -179,6 +187,7 @@ struct DescStore {
       if (c.d) cudaFree(c.d);
     }
     chunks.clear();
+    cur = 0;
     off = bytes = 0;
   }
   ~DescStore() {
@@ -2554,14 +2563,17 @@ struct GraphCache {
   size_t nodes = 0;
   long long replays = 0;
   DescStore desc;
+  size_t pool_alloc = 0;  // doubles allocated for pool (>= total: slack absorbs small regrowth)
   void drop_graph() {
     if (exec) cudaGraphExecDestroy(exec);
     exec = nullptr;
-    desc.clear();
+    desc.rewind();
     valid = false;
   }
   void free_buffers() {
     drop_graph();
+    desc.clear();
+    pool_alloc = 0;
     cudaFree(pool);
     cudaFree(d_leaf);
     cudaFree(d_rank);
@@ -2668,17 +2680,22 @@ static int factorize_graph(Factor& F, HMat& H, cudaStream_t st, size_t arena_byt
       total += l.kind == DENSE ? (size_t)l.m * l.n : (size_t)(l.m + l.n) * caps[k];
     }
     gc.drop_graph();
-    if (total != gc.total || !gc.pool) {
+    if (total > gc.pool_alloc || !gc.pool) {
       cudaFree(gc.pool);
       gc.pool = nullptr;
-      gc.total = 0;
-      if (dev_malloc_plain((void**)&gc.pool, std::max<size_t>(1, total) * 8) != cudaSuccess) {
+      gc.total = gc.pool_alloc = 0;
+      const size_t want = total + total / 8;  // slack: the next regrowth usually fits
+      if (dev_malloc_plain((void**)&gc.pool, std::max<size_t>(1, want) * 8) == cudaSuccess) {
+        gc.pool_alloc = want;
+      } else if (dev_malloc_plain((void**)&gc.pool, std::max<size_t>(1, total) * 8) == cudaSuccess) {
+        gc.pool_alloc = total;
+      } else {
         cudaGetLastError();
         gc.pool = nullptr;
         return 1;
       }
-      gc.total = total;
     }
+    gc.total = total;
     if (L != gc.L || G.n != gc.n || !gc.d_leaf) {
       cudaFree(gc.d_leaf);
       cudaFree(gc.d_rank);
@@ -2874,8 +2891,11 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
   bool graph_done = false;
   {
     const char* ge = getenv("HMGP_GRAPH");
-    if (t_graph_ok && memo_hit && !use_dag && !(ge && atoi(ge) == 0) && !getenv("HMGP_STATS") &&
-        !getenv("HMGP_SERIAL")) {
+    // (small problems: a capture costs more than the few thousand launches it saves)
+    int min_n = 32768;
+    if (const char* e = getenv("HMGP_GRAPH_MIN_N")) min_n = atoi(e);
+    if (t_graph_ok && memo_hit && G.n >= min_n && !use_dag && !(ge && atoi(ge) == 0) &&
+        !getenv("HMGP_STATS") && !getenv("HMGP_SERIAL")) {
       const int rc = factorize_graph(F, H, st, arena_bytes, tcap0, grow);
       graph_done = rc == 0;
       if (!graph_done) {  // hand the borrowed buffers back; the stream path owns its own
