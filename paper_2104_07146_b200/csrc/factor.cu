@@ -139,7 +139,7 @@ struct DescStore {
   struct Chunk {
     char* h = nullptr;
     char* d = nullptr;
-    size_t cap = 0;
+    size_t cap = 0, used = 0;
   };
   std::vector<Chunk> chunks;
   size_t cur = 0;  // chunk being filled (chunks are kept and re-used by the next capture:
@@ -153,6 +153,7 @@ struct DescStore {
     while (cur < chunks.size() && off + a > chunks[cur].cap) {
       ++cur;
       off = 0;
+      if (cur < chunks.size()) chunks[cur].used = 0;
     }
     if (cur >= chunks.size()) {
       Chunk c;
@@ -163,22 +164,26 @@ struct DescStore {
       cur = chunks.size() - 1;
       off = 0;
     }
-    if (!up) HMGP_CUDA(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
     Chunk& c = chunks[cur];
-    std::memcpy(c.h + off, src, n);
-    HMGP_CUDA(cudaMemcpyAsync(c.d + off, c.h + off, n, cudaMemcpyHostToDevice, up));
+    std::memcpy(c.h + off, src, n);  // uploaded chunk-wise by finish_upload()
     void* r = c.d + off;
     off += a;
+    c.used = off;
     bytes += a;
     return r;
   }
-  void finish_upload() {  // after the capture: wait for the copies
-    if (up) HMGP_CUDA(cudaStreamSynchronize(up));
+  void finish_upload() {  // after the capture: one copy per chunk, then wait
+    if (!up) HMGP_CUDA(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
+    for (size_t k = 0; k <= cur && k < chunks.size(); ++k)
+      if (chunks[k].used)
+        HMGP_CUDA(cudaMemcpyAsync(chunks[k].d, chunks[k].h, chunks[k].used, cudaMemcpyHostToDevice, up));
+    HMGP_CUDA(cudaStreamSynchronize(up));
   }
   void rewind() {  // the next capture overwrites the chunks in place
     if (up) cudaStreamSynchronize(up);
     cur = 0;
     off = bytes = 0;
+    if (!chunks.empty()) chunks[0].used = 0;
   }
   void clear() {
     if (up) cudaStreamSynchronize(up);

@@ -63,8 +63,12 @@ __device__ void gemm_item(const GemmItem& it, int tile0, int tstride, bool count
   if (M <= 0 || N <= 0) return;
   if (count && threadIdx.x == 0) atomicAdd(&d_cnt_gemm, 2.0 * M * N * K);
   const int tm = (M + GT - 1) / GT, tn = (N + GT - 1) / GT;
-  __shared__ double sA[GK][GT + 1];
-  __shared__ double sB[GK][GT + 1];
+  // k-slabs are double-buffered in shared memory: the global loads of slab s+1 are
+  // issued into registers before the DMMA work on slab s and stored afterwards, so
+  // their latency overlaps the math and a slab costs ONE barrier.  The summation
+  // order of every output element is unchanged (k ascending).
+  __shared__ double sA[2][GK][GT + 1];
+  __shared__ double sB[2][GK][GT + 1];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int wr = (w >> 2) * 32, wc = (w & 3) * 16;  // warp sub-tile origin
   const int fr = lane >> 2, fk = lane & 3;           // fragment row / k index
@@ -74,6 +78,27 @@ __device__ void gemm_item(const GemmItem& it, int tile0, int tstride, bool count
   // slabs, summed in a fixed order by k_slab_sum.
   const int T = tm * tn;
   const int tbeg = tile0, tstep = tstride, kbeg = 0, kend = K;
+  constexpr int kPer = GK * GT / 256;  // elements of each operand slab per thread
+  // this thread's element e -> (kk, ii) of the A slab and (kk, jj) of the B slab
+  int akk[kPer], aii[kPer], bkk[kPer], bjj[kPer];
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int e = threadIdx.x + q * 256;
+    if (!it.ta) {
+      aii[q] = e % GT;
+      akk[q] = e / GT;
+    } else {
+      akk[q] = e % GK;
+      aii[q] = e / GK;
+    }
+    if (!it.tb) {
+      bkk[q] = e % GK;
+      bjj[q] = e / GK;
+    } else {
+      bjj[q] = e % GT;
+      bkk[q] = e / GT;
+    }
+  }
   for (int tile = tbeg; tile < T; tile += tstep) {
     const int i0 = (tile % tm) * GT, j0 = (tile / tm) * GT;
     double acc[4][2][2];
@@ -81,51 +106,51 @@ __device__ void gemm_item(const GemmItem& it, int tile0, int tstride, bool count
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-    for (int k0 = kbeg; k0 < kend; k0 += GK) {
-      __syncthreads();
-      for (int e = threadIdx.x; e < GK * GT; e += 256) {
-        int kk, ii;
-        // A tile: op(A)[i0+ii, k0+kk]
-        if (!it.ta) {
-          ii = e % GT;
-          kk = e / GT;
-        } else {
-          kk = e % GK;
-          ii = e / GK;
-        }
-        const int gi = i0 + ii, gk = k0 + kk;
-        double v = 0.0;
-        if (gi < M && gk < kend)
-          v = it.ta ? it.A[(size_t)gi * it.lda + gk] : it.A[(size_t)gk * it.lda + gi];
-        sA[kk][ii] = v;
-        // B tile: op(B)[k0+kk, j0+jj]
-        int jj;
-        if (!it.tb) {
-          kk = e % GK;
-          jj = e / GK;
-        } else {
-          jj = e % GT;
-          kk = e / GT;
-        }
-        const int gj = j0 + jj, gk2 = k0 + kk;
-        double wv = 0.0;
-        if (gj < N && gk2 < kend)
-          wv = it.tb ? it.B[(size_t)gk2 * it.ldb + gj] : it.B[(size_t)gj * it.ldb + gk2];
-        sB[kk][jj] = wv;
+    double ra[kPer], rb2[kPer];
+    auto fetch = [&](int k0) {
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const int gi = i0 + aii[q], gk = k0 + akk[q];
+        ra[q] = (gi < M && gk < kend)
+                    ? (it.ta ? it.A[(size_t)gi * it.lda + gk] : it.A[(size_t)gk * it.lda + gi])
+                    : 0.0;
+        const int gj = j0 + bjj[q], gk2 = k0 + bkk[q];
+        rb2[q] = (gj < N && gk2 < kend)
+                     ? (it.tb ? it.B[(size_t)gk2 * it.ldb + gj] : it.B[(size_t)gj * it.ldb + gk2])
+                     : 0.0;
       }
-      __syncthreads();
+    };
+    auto stash = [&](int buf) {
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        sA[buf][akk[q]][aii[q]] = ra[q];
+        sB[buf][bkk[q]][bjj[q]] = rb2[q];
+      }
+    };
+    __syncthreads();  // the previous tile's readers are done with both buffers
+    if (kbeg < kend) {
+      fetch(kbeg);
+      stash(0);
+    }
+    __syncthreads();
+    int buf = 0;
+    for (int k0 = kbeg; k0 < kend; k0 += GK, buf ^= 1) {
+      const bool more = k0 + GK < kend;
+      if (more) fetch(k0 + GK);
 #pragma unroll
       for (int ks = 0; ks < GK; ks += 4) {
         double af[4], bf[2];
 #pragma unroll
-        for (int rb = 0; rb < 4; ++rb) af[rb] = sA[ks + fk][wr + rb * 8 + fr];
+        for (int rb = 0; rb < 4; ++rb) af[rb] = sA[buf][ks + fk][wr + rb * 8 + fr];
 #pragma unroll
-        for (int cb = 0; cb < 2; ++cb) bf[cb] = sB[ks + fk][wc + cb * 8 + fr];
+        for (int cb = 0; cb < 2; ++cb) bf[cb] = sB[buf][ks + fk][wc + cb * 8 + fr];
 #pragma unroll
         for (int rb = 0; rb < 4; ++rb)
 #pragma unroll
           for (int cb = 0; cb < 2; ++cb) dmma884(acc[rb][cb], af[rb], bf[cb]);
       }
+      if (more) stash(buf ^ 1);  // nobody reads buf^1 during this slab
+      __syncthreads();
     }
 #pragma unroll
     for (int cb = 0; cb < 2; ++cb)

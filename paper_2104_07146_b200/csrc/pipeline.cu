@@ -90,8 +90,10 @@ void pool_low_memory();
 class BatchPool {
  public:
   static BatchPool& get() {
-    static BatchPool p;
-    return p;
+    // never destroyed: its workers stay parked on the condition variable until the
+    // process ends, and destroying a condition variable with waiters blocks exit
+    static BatchPool* p = new BatchPool();
+    return *p;
   }
   // run job(ctx) on workers [0, T) and wait for all of them
   void run(int T, int device, const std::function<void(hmgp_ctx*)>& job) {
@@ -100,6 +102,7 @@ class BatchPool {
       ws_.emplace_back(new Worker());
       Worker* w = ws_.back().get();
       w->th = std::thread([this, w, device] { loop(w, device); });
+      w->th.detach();  // parked for the life of the process
     }
     pending_ = T;
     for (int i = 0; i < T; ++i) {
@@ -155,12 +158,7 @@ class BatchPool {
       }
     }
   }
-  ~BatchPool() {
-    // process exit: the workers stay parked (their thread-local CUDA objects must
-    // not be destroyed while the runtime is shutting down)
-    for (auto& w : ws_)
-      if (w->th.joinable()) w->th.detach();
-  }
+  ~BatchPool() = delete;
   std::mutex mu_;
   std::condition_variable cv_, done_;
   std::vector<std::unique_ptr<Worker>> ws_;

@@ -155,7 +155,7 @@ def test_small_fit_ascends_and_matches_oracle_fit(hm, mle, oracle):
     pts = hm.random_locations(256, 8)
     truth = hm.MaternParams(1.5, 0.1, 0.5, 0.0)
     z = hm.sample_grf(pts, truth, 12)
-    cfg = mle.OptimizerConfig(brent_max_evals=20)
+    cfg = mle.OptimizerConfig(brent_max_evals=20, max_iters=24)  # 6 sweeps: enough to compare the two fits
     cfg.h.rank = hm.RankControl.fixed_accuracy(1e-4)
     rep = mle.fit(pts, z, cfg)
     assert rep.iterations <= cfg.max_iters
