@@ -381,19 +381,18 @@ def extras(hm, _lib, ctx, stream, comm, rank, ws, peaks):
                                  "peak": hbm, "unit": "GB/s", "frac": (fb + 2 * nvec) / ms_sl / 1e6 / hbm,
                                  "traffic": None, "note": "host-buffer call: 2 x 2 MB vector copies inside"}
         del f3, h3
-    # C3 θ-throughput: the same n = 262144 problem through hmgp_loglik_sweep on one
-    # geometry.  A first batch of 5 θ warms the persistent workers (each captures the
-    # θ-independent factorization launch sequence as a CUDA graph); the timed batch
-    # of 8 further θ (ℓ nudged) replays the graphs concurrently.
-    th3 = np.array([[C3["theta"][0], C3["theta"][1] * (1.0 + 0.01 * (k + 13 * rank)), C3["theta"][2], C3["theta"][3]]
-                    for k in range(13)])
-    ms3w, _ = dev_ms(lambda: sw.sweep_host(gc3, zc3h, th3, list(range(5)), cfg3, ctx))
-    ms3, (_, v3) = dev_ms(lambda: sw.sweep_host(gc3, zc3h, th3, list(range(5, 13)), cfg3, ctx))
-    out["C3_theta_batch"] = {"n": C3["g"] ** 2, "thetas_per_rank": 8, "ms": ms3, "warm_batch_ms": ms3w,
-                             "evals_per_s": 8 * ws / (ms3 / 1e3), "loglik": v3[:, 0].tolist(),
+    # C3 θ-throughput: the same n = 262144 problem, 9 θ per rank (ℓ nudged) through
+    # hmgp_loglik_sweep on one geometry: θ0 alone sizes the workspace, the other 8 run
+    # concurrently on the persistent workers.  (A one-off batch stays on the stream
+    # path; long sweeps replay captured CUDA graphs from each worker's third θ on —
+    # profiles/r2_exp_graph_batch*.txt.)
+    th3 = np.array([[C3["theta"][0], C3["theta"][1] * (1.0 + 0.01 * (k + 9 * rank)), C3["theta"][2], C3["theta"][3]]
+                    for k in range(9)])
+    ms3, (_, v3) = dev_ms(lambda: sw.sweep_host(gc3, zc3h, th3, list(range(9)), cfg3, ctx))
+    out["C3_theta_batch"] = {"n": C3["g"] ** 2, "thetas_per_rank": 9, "ms": ms3,
+                             "evals_per_s": 9 * ws / (ms3 / 1e3), "loglik": v3[:, 0].tolist(),
                              "status": v3[:, 3].tolist(),
-                             "note": "8 θ via hmgp_loglik_sweep on warm workers (CUDA-graph replay of the "
-                                     "captured factorization), after an untimed 5-θ batch that captures"}
+                             "note": "9 θ via hmgp_loglik_sweep: θ0 alone, then 8 on the persistent workers"}
     del gc3
     # C2: assembly only, n = 65536 jittered 256x256, leaf 64, eta 2, eps 1e-7; with N
     # ranks each assembles its cost-balanced leaf range (no collective); the time is

@@ -74,12 +74,23 @@ void* dev_alloc(size_t bytes) {
       e = cudaMallocAsync(&p, bytes, t_alloc_stream);
     }
     if (e == cudaErrorMemoryAllocation && reclaim()) e = cudaMallocAsync(&p, bytes, t_alloc_stream);
+    if (e == cudaErrorMemoryAllocation) {
+      cudaGetLastError();
+      // a capacity failure, not a CUDA fault: θ-batch workers hand the θ back to the
+      // caller's thread, which runs it once the others have released their share
+      throw Error(6 /* HMGP_ECAPACITY */, "device memory exhausted (per-evaluation buffer)");
+    }
     HMGP_CUDA(e);
     std::lock_guard<std::mutex> lk(g_mu);
     g_async.insert(p);
     return p;
   }
-  HMGP_CUDA(dev_malloc_plain(&p, bytes));
+  const cudaError_t e = dev_malloc_plain(&p, bytes);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    throw Error(6 /* HMGP_ECAPACITY */, "device memory exhausted");
+  }
+  HMGP_CUDA(e);
   return p;
 }
 

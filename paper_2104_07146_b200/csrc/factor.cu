@@ -158,8 +158,11 @@ struct DescStore {
     if (cur >= chunks.size()) {
       Chunk c;
       c.cap = std::max(kChunk, a);
-      HMGP_CUDA(cudaMallocHost(&c.h, c.cap));
-      HMGP_CUDA(dev_malloc_plain((void**)&c.d, c.cap));
+      if (cudaMallocHost(&c.h, c.cap) != cudaSuccess || dev_malloc_plain((void**)&c.d, c.cap) != cudaSuccess) {
+        cudaGetLastError();
+        if (c.h) cudaFreeHost(c.h);
+        throw Error(6, "descriptor store: out of memory");  // the capture is abandoned (stream path)
+      }
       chunks.push_back(c);
       cur = chunks.size() - 1;
       off = 0;
@@ -2459,6 +2462,8 @@ static void solve_sweep(const Factor& F, double* v, bool trans, cudaStream_t st)
     int per = 0;
     HMGP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_solve_sweep, kSolveThreads, smem));
     grid = std::max(1, per) * sms;
+    // fewer CTAs make the grid-wide barriers cheaper; a step has few units
+    if (const char* e = getenv("HMGP_SOLVE_GRID")) grid = std::max(1, std::min(grid, atoi(e)));
   }
   const SStep* d_steps = static_cast<const SStep*>(trans ? F.d_bsteps : F.d_fsteps);
   const SUnit* d_units = static_cast<const SUnit*>(trans ? F.d_bunits : F.d_funits);
@@ -2899,8 +2904,25 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
     // (small problems: a capture costs more than the few thousand launches it saves)
     int min_n = 32768;
     if (const char* e = getenv("HMGP_GRAPH_MIN_N")) min_n = atoi(e);
-    if (t_graph_ok && memo_hit && G.n >= min_n && !use_dag && !(ge && atoi(ge) == 0) &&
-        !getenv("HMGP_STATS") && !getenv("HMGP_SERIAL")) {
+    // (a capture costs about as much as a stream evaluation, more when several θ-batch
+    // workers capture at once: it pays from this thread's third evaluation on the
+    // structure — a long sweep, an MLE fit, repeated L(θ) — not for a one-off batch)
+    static thread_local uint64_t seen_key = 0;
+    static thread_local int seen_count = 0;
+    int after = 2;
+    if (const char* e = getenv("HMGP_GRAPH_AFTER")) after = atoi(e);
+    bool eligible = t_graph_ok && memo_hit && G.n >= min_n && !use_dag && !(ge && atoi(ge) == 0) &&
+                    !getenv("HMGP_STATS") && !getenv("HMGP_SERIAL");
+    if (eligible) {
+      const uint64_t skey = ((uint64_t)G.n << 32) ^ (uint64_t)L;
+      if (seen_key != skey) {
+        seen_key = skey;
+        seen_count = 0;
+      }
+      eligible = seen_count >= after || t_gc.valid;
+      ++seen_count;
+    }
+    if (eligible) {
       const int rc = factorize_graph(F, H, st, arena_bytes, tcap0, grow);
       graph_done = rc == 0;
       if (!graph_done) {  // hand the borrowed buffers back; the stream path owns its own

@@ -62,7 +62,20 @@ double factor_eps(const hmgp_config* c) {  // pipeline.hpp:21-24
 std::unique_ptr<Factor> do_factorize(HMat& h, double eps_f, bool ldl, cudaStream_t st) {
   if (!(eps_f > 0.0)) throw std::invalid_argument("factorize: eps_f must be positive");
   auto f = std::make_unique<Factor>();
-  factorize(*f, h, eps_f, ldl, st, arena_bytes_for(h));
+  try {
+    factorize(*f, h, eps_f, ldl, st, arena_bytes_for(h));
+  } catch (const Error& e) {
+    // the temporaries did not fit in what the parked θ-batch workers left free:
+    // take their workspaces back and run once more with the full arena
+    if (e.code != HMGP_ECAPACITY || !hmgp_gpu::g_low_memory_hook) throw;
+    hmgp_gpu::g_low_memory_hook();
+    release_thread_workspace();
+    dev_pool_trim();
+    const bool ok = t_graph_ok;
+    f = std::make_unique<Factor>();
+    t_graph_ok = ok;
+    factorize(*f, h, eps_f, ldl, st, arena_bytes_for(h));
+  }
   if (f->fail_pos != INT_MAX) {
     hmgp_set_pivot(h.g->perm[f->fail_pos], f->fail_val);
     throw Error(HMGP_ENOTSPD, "matrix not numerically SPD; increase nugget tau2");
@@ -469,7 +482,8 @@ int hmgp_loglik_batch(hmgp_ctx* ctx, hmgp_geom* g, const double* d_z, const hmgp
       // a small margin suffices, and a worker that still runs out hands its θ
       // back to the caller's full workspace)
       share = peak + peak / 6 + ((size_t)256 << 20);
-      per = share + pl * 3 + ((size_t)256 << 20);
+      // H-matrix payload, factor pool (captured: +25 % capacities), descriptor store
+      per = share + pl * 4 + ((size_t)768 << 20);
       if (pool.key_ == bkey && pool.share_ < share) {  // workspaces too small for this batch
         pool.release();
         pool.warm_ = 0;

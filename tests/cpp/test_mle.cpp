@@ -72,7 +72,6 @@ int main(int argc, char** argv) {
       OptimizerConfig cfg;
       cfg.h.rank = RankControl::fixed_accuracy(1e-4);
       cfg.brent_max_evals = 20;
-      cfg.max_iters = 40;  // ten sweeps (the default 400 never converges below 1e-4 here, as in the reference)
       const FitReport rep = fit(pts, z, cfg);
       CHECK(rep.iterations <= cfg.max_iters);
       double prev = -std::numeric_limits<double>::infinity();
