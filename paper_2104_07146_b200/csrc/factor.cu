@@ -2172,7 +2172,7 @@ struct SStep {
   int dleaf, base;
   int u2b, u2e, u3b, u3e;
 };
-constexpr int kSolveChunk = 2048;
+constexpr int kSolveChunk = 512;  // low-rank blocks taller than this are cut over several CTAs
 __device__ int d_solve_stats_on;
 __device__ unsigned long long d_solve_cyc[2][6];
 constexpr int kSolveThreads = 256;
@@ -2318,28 +2318,24 @@ __device__ void solve_unit(const SUnit& u, const LeafDev* __restrict__ lf, const
 // in registers (one shuffle broadcast per column, reciprocal diagonal), then all
 // threads apply the block to the remaining rows (a small mat-vec).
 __device__ void solve_trsv_cta(const double* __restrict__ Lg, int b, double* __restrict__ xg, int trans,
-                               double* sm, bool staged) {
-  const double* L = Lg;
-  double* x = sm + (staged ? (size_t)b * b : 0);
-  double* inv = x + b;
-  if (staged) {  // 16-byte loads, eight in flight per thread
-    double* Ls = sm;
-    const int n2 = (b * b) / 2;
-    const double2* src = reinterpret_cast<const double2*>(Lg);
-    double2* dst = reinterpret_cast<double2*>(Ls);
-    if ((reinterpret_cast<uintptr_t>(Lg) & 15) == 0) {
-#pragma unroll 8
-      for (int e = threadIdx.x; e < n2; e += blockDim.x) dst[e] = src[e];
-      if ((b * b) & 1)
-        if (threadIdx.x == 0) Ls[b * b - 1] = Lg[b * b - 1];
-    } else {
-      for (int e = threadIdx.x; e < b * b; e += blockDim.x) Ls[e] = Lg[e];
-    }
-    L = Ls;
+                               double* sm, bool staged, int smem_b) {
+  // L comes from shared memory when the leaf was prefetched there (cp.async issued
+  // one step ahead, see k_solve_sweep: a single SM pulling 128 KB synchronously
+  // from HBM was the 18 us that dominated a step), else straight from global
+  // memory.  Warp 0 holds the 32 x 32 diagonal block of the current sub-step in
+  // registers (lane = row) and runs the substitution on registers + shuffles; all
+  // threads then apply the block column (forward) / block row (backward) to the
+  // remaining unknowns, coalesced over rows.
+  const double* Lsrc = staged ? sm : Lg;
+  double* x = sm + (size_t)smem_b * smem_b;
+  double* inv = x + smem_b;
+  if (!staged) {
+    x = sm;
+    inv = x + b;
   }
   for (int e = threadIdx.x; e < b; e += blockDim.x) {
     x[e] = xg[e];
-    inv[e] = 1.0 / Lg[(size_t)e * b + e];
+    inv[e] = 1.0 / Lsrc[(size_t)e * b + e];
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
@@ -2347,11 +2343,18 @@ __device__ void solve_trsv_cta(const double* __restrict__ Lg, int b, double* __r
     for (int jb = 0; jb < b; jb += 32) {
       const int nb = min(32, b - jb);
       if (threadIdx.x < 32) {
+        double lr[32];  // row (jb + lane) of the diagonal block
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          lr[j] = (j < nb && lane < nb && lane > j) ? Lsrc[(size_t)(jb + j) * b + jb + lane] : 0.0;
         double xi = lane < nb ? x[jb + lane] : 0.0;
-        for (int j = 0; j < nb; ++j) {
-          if (lane == j) xi *= inv[jb + j];
-          const double xj = __shfl_sync(0xffffffffu, xi, j);
-          if (lane > j && lane < nb) xi -= L[(size_t)(jb + j) * b + jb + lane] * xj;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (j < nb) {
+            if (lane == j) xi *= inv[jb + j];
+            const double xj = __shfl_sync(0xffffffffu, xi, j);
+            xi -= lr[j] * xj;  // lr[j] = 0 for lane <= j
+          }
         }
         if (lane < nb) x[jb + lane] = xi;
       }
@@ -2359,29 +2362,38 @@ __device__ void solve_trsv_cta(const double* __restrict__ Lg, int b, double* __r
       for (int i = jb + nb + threadIdx.x; i < b; i += blockDim.x) {
         double s = 0.0;
 #pragma unroll 8
-        for (int j = 0; j < nb; ++j) s += L[(size_t)(jb + j) * b + i] * x[jb + j];
+        for (int j = 0; j < nb; ++j) s += Lsrc[(size_t)(jb + j) * b + i] * x[jb + j];
         x[i] -= s;
       }
       __syncthreads();
     }
   } else {
     const int nblk = (b + 31) / 32;
+    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int q = nblk - 1; q >= 0; --q) {
       const int jb = q * 32, nb = min(32, b - jb);
-      // x_J -= L(I, J)^T x_I for the rows I below the block (already solved)
-      for (int j = jb + threadIdx.x; j < jb + nb; j += blockDim.x) {
+      // x_J -= L(I, J)^T x_I for the rows I below the block (already solved):
+      // a warp per column j of the block, lanes over the rows i (coalesced)
+      for (int j = jb + w; j < jb + nb; j += nw) {
         double s = 0.0;
-#pragma unroll 8
-        for (int i = jb + nb; i < b; ++i) s += L[(size_t)j * b + i] * x[i];
-        x[j] -= s;
+        for (int i = jb + nb + lane; i < b; i += 32) s += Lsrc[(size_t)j * b + i] * x[i];
+        s = warp_sum(s);
+        if (lane == 0) x[j] -= s;
       }
       __syncthreads();
       if (threadIdx.x < 32) {
+        double lc[32];  // column (jb + lane) of the diagonal block: lc[i] = L(jb + i, jb + lane)
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          lc[i] = (i < nb && lane < nb && i > lane) ? Lsrc[(size_t)(jb + lane) * b + jb + i] : 0.0;
         double xi = lane < nb ? x[jb + lane] : 0.0;
-        for (int j = nb - 1; j >= 0; --j) {
-          if (lane == j) xi *= inv[jb + j];
-          const double xj = __shfl_sync(0xffffffffu, xi, j);
-          if (lane < j) xi -= L[(size_t)(jb + lane) * b + jb + j] * xj;
+#pragma unroll
+        for (int j = 31; j >= 0; --j) {
+          if (j < nb) {
+            if (lane == j) xi *= inv[jb + j];
+            const double xj = __shfl_sync(0xffffffffu, xi, j);
+            xi -= lc[j] * xj;  // lc[j] = L(jb + j, jb + lane), 0 unless j > lane
+          }
         }
         if (lane < nb) x[jb + lane] = xi;
       }
@@ -2389,6 +2401,20 @@ __device__ void solve_trsv_cta(const double* __restrict__ Lg, int b, double* __r
     }
   }
   for (int e = threadIdx.x; e < b; e += blockDim.x) xg[e] = x[e];
+  __syncthreads();
+}
+
+// asynchronous copy of a diagonal leaf (b x b doubles) into shared memory: 8-byte
+// cp.async per element (no alignment requirement beyond the double's), all threads
+__device__ __forceinline__ void solve_prefetch_leaf(const double* __restrict__ Lg, int b, double* sm) {
+  const unsigned base = (unsigned)__cvta_generic_to_shared(sm);
+  const int n = b * b;
+  for (int e = threadIdx.x; e < n; e += blockDim.x)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(base + 8u * (unsigned)e), "l"(Lg + e) : "memory");
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void solve_prefetch_wait() {
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
 }
 
@@ -2407,11 +2433,25 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve_sweep(const SStep* __re
     acc[i] += now - tc;
     tc = now;
   };
+  bool prefetched = false;
   for (int s = 0; s < nsteps; ++s) {
     const SStep st = steps[trans ? nsteps - 1 - s : s];
     if (blockIdx.x == 0) {
       const LeafDev d = lf[st.dleaf];
-      solve_trsv_cta(d.a, d.m, v + st.base, trans, ssm, d.m <= smem_b);
+      const bool fits = d.m <= smem_b;
+      if (fits) {
+        if (!prefetched) solve_prefetch_leaf(d.a, d.m, ssm);  // first step (or after a leaf that did not fit)
+        solve_prefetch_wait();
+      }
+      solve_trsv_cta(d.a, d.m, v + st.base, trans, ssm, fits, smem_b);
+      prefetched = false;
+      if (s + 1 < nsteps) {  // the next diagonal leaf streams in while the grid applies this step's blocks
+        const LeafDev nx = lf[steps[trans ? nsteps - 2 - s : s + 1].dleaf];
+        if (nx.m <= smem_b) {
+          solve_prefetch_leaf(nx.a, nx.m, ssm);
+          prefetched = true;
+        }
+      }
     }
     tick(0);
     grid.sync();
@@ -2429,13 +2469,6 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve_sweep(const SStep* __re
         __syncthreads();
       }
       tick(4);
-    }
-    if (blockIdx.x == 0 && s + 1 < nsteps) {  // warm L2 with the next diagonal leaf
-      const LeafDev d = lf[steps[trans ? nsteps - 2 - s : s + 1].dleaf];
-      const char* p = reinterpret_cast<const char*>(d.a);
-      const size_t bytes = (size_t)d.m * d.m * 8;
-      for (size_t o = (size_t)threadIdx.x * 128; o < bytes; o += (size_t)blockDim.x * 128)
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(p + o));
     }
     grid.sync();
     tick(5);
