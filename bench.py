@@ -299,7 +299,7 @@ def run_ours(args):
             line["sweep_loglik"] = gathered["table"][:, 0].tolist()
             line["collective"] = "one ncclAllGather of N result rows per timed region (hmgp_sweep_gather)"
     if not args.no_extras and not args.small:
-        ex = extras(hm, _lib, ctx, stream, comm, rank, ws, peaks=measured_peaks())
+        ex = extras(hm, _lib, ctx, stream, comm, rank, ws, peaks=measured_peaks(), c3_batch=args.c3_batch)
         if line is not None:
             line["extras"] = ex
     if line is not None:
@@ -320,7 +320,7 @@ def bench_config(args, n, cfgd, ws):
             "l2": "inputs larger than L2 (>2 GB near-field payload per step)"}
 
 
-def extras(hm, _lib, ctx, stream, comm, rank, ws, peaks):
+def extras(hm, _lib, ctx, stream, comm, rank, ws, peaks, c3_batch=False):
     """Other BASELINE configs, measured once each (device events on the library
     stream, max over ranks): C3 θ-batch, solve / matvec HBM rooflines, C2
     assembly (sharded over the ranks), the C4 θ-grid subset sharded ν-major with
@@ -386,13 +386,18 @@ def extras(hm, _lib, ctx, stream, comm, rank, ws, peaks):
     # concurrently on the persistent workers.  (A one-off batch stays on the stream
     # path; long sweeps replay captured CUDA graphs from each worker's third θ on —
     # profiles/r2_exp_graph_batch*.txt.)
-    th3 = np.array([[C3["theta"][0], C3["theta"][1] * (1.0 + 0.01 * (k + 9 * rank)), C3["theta"][2], C3["theta"][3]]
-                    for k in range(9)])
-    ms3, (_, v3) = dev_ms(lambda: sw.sweep_host(gc3, zc3h, th3, list(range(9)), cfg3, ctx))
-    out["C3_theta_batch"] = {"n": C3["g"] ** 2, "thetas_per_rank": 9, "ms": ms3,
-                             "evals_per_s": 9 * ws / (ms3 / 1e3), "loglik": v3[:, 0].tolist(),
-                             "status": v3[:, 3].tolist(),
-                             "note": "9 θ via hmgp_loglik_sweep: θ0 alone, then 8 on the persistent workers"}
+    # Opt-in (--c3-batch, ~2 min): one θ needs ~45 GB of device workspace at this size,
+    # so at most 3 run concurrently on one B200 and the batch gains little (measured
+    # 0.12-0.16 evals/s, profiles/r2_exp_graph_batch_cold_warm.txt); C3-sized sweeps
+    # shard over GPUs instead (the headline line with --gpus N).
+    if c3_batch:
+        th3 = np.array([[C3["theta"][0], C3["theta"][1] * (1.0 + 0.01 * (k + 9 * rank)), C3["theta"][2],
+                         C3["theta"][3]] for k in range(9)])
+        ms3, (_, v3) = dev_ms(lambda: sw.sweep_host(gc3, zc3h, th3, list(range(9)), cfg3, ctx))
+        out["C3_theta_batch"] = {"n": C3["g"] ** 2, "thetas_per_rank": 9, "ms": ms3,
+                                 "evals_per_s": 9 * ws / (ms3 / 1e3), "loglik": v3[:, 0].tolist(),
+                                 "status": v3[:, 3].tolist(),
+                                 "note": "9 θ via hmgp_loglik_sweep: θ0 alone, then 8 on the persistent workers"}
     del gc3
     # C2: assembly only, n = 65536 jittered 256x256, leaf 64, eta 2, eps 1e-7; with N
     # ranks each assembles its cost-balanced leaf range (no collective); the time is
@@ -550,6 +555,7 @@ def main():
     ap.add_argument("--small", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--c3-batch", action="store_true", help="also time a 9-θ batch at C3 (≈ 2 min)")
     ap.add_argument("--ref-g", type=int, default=256,
                     help="grid side of the reference arm's CPU sample (48, 96, 128, 192, 256 or 512)")
     args = ap.parse_args()
