@@ -2905,6 +2905,15 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
     tcap0 = 512;
     start_3d = true;
   }
+  // (experiments: HMGP_TCAP / HMGP_GROW force the starting capacities)
+  if (const char* e = getenv("HMGP_TCAP")) {
+    tcap0 = std::max(64, atoi(e));
+    start_3d = false;
+  }
+  if (const char* e = getenv("HMGP_GROW")) {
+    grow = std::max(1, atoi(e));
+    start_3d = false;
+  }
   const CapMemo memo = memo_get();
   const bool memo_hit = memo.n == G.n && memo.dim == G.dim && memo.leaves == L;
   if (memo_hit) {
@@ -3017,6 +3026,7 @@ void factorize(Factor& F, HMat& H, double eps_f, bool ldl, cudaStream_t st, size
         if (!F.pool) F.pool = dev_alloc_n<double>(std::max<size_t>(1, total));
       }
       pool_doubles = total;
+      start_3d = false;  // the fallback applies to the initial start only (not to a regrown pool)
     }
     std::vector<CloneItem> ci;
     for (int k = 0; k < L; ++k) {
