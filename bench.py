@@ -374,7 +374,12 @@ def extras(hm, _lib, ctx, stream, comm, rank, ws, peaks, c3_batch=False):
                                   "ms": ms_mv, "algorithmic_bytes": hb + 2 * nvec,
                                   "achieved": (hb + 2 * nvec) / ms_mv / 1e6,
                                   "peak": hbm, "unit": "GB/s", "frac": (hb + 2 * nvec) / ms_mv / 1e6 / hbm,
-                                  "traffic": None, "note": "device vectors (hmgp_hmat_matvec_device), mean of 5 "
+                                  "traffic": 5712027480.0,
+                                  "traffic_source": "ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum over "
+                                  "the product's seven kernels (profiles/r2_hbm_kernels_raw.csv): 1.45x the "
+                                  "algorithmic bytes - tall low-rank leaves are read twice (dots, then apply), "
+                                  "plus the private output segments; the kernels run at 4.2-5.2 TB/s of DRAM",
+                                  "note": "device vectors (hmgp_hmat_matvec_device), mean of 5 "
                                   "back-to-back products; payload 4 GB >> L2"}
         out["roofline_solve"] = {"bound": "hbm", "kernel": "forward solve K10 (k_solve_sweep)", "ms": ms_sl,
                                  "algorithmic_bytes": fb + 2 * nvec, "achieved": (fb + 2 * nvec) / ms_sl / 1e6,
