@@ -606,14 +606,45 @@ int hmgp_predict(hmgp_ctx* ctx, const double* train, int n, int dim, const doubl
       f = do_factorize(h, factor_eps(cfg), cfg->form == 1, ctx->stream);
     }
     DBuf<double> dz(n), dw(n), dtest((size_t)m * dim), dout(m);
+    // The new locations are visited in Morton order: the 32 lanes of a warp then hold
+    // neighbouring points, whose distances to one training point — hence the Bessel
+    // branch (Temme / Steed) and iteration counts of the general-ν path — are close,
+    // instead of diverging lane by lane.  Each prediction's own sum is unchanged
+    // (same training order), so the values are bit-identical to the unsorted pass.
+    std::vector<int> order(m);
+    std::vector<double> tsorted((size_t)m * dim), osorted(m);
+    {
+      double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+      for (int k = 0; k < m; ++k)
+        for (int d = 0; d < dim; ++d) {
+          lo[d] = std::min(lo[d], test[(size_t)k * dim + d]);
+          hi[d] = std::max(hi[d], test[(size_t)k * dim + d]);
+        }
+      std::vector<uint64_t> key(m);
+      for (int k = 0; k < m; ++k) {
+        uint64_t code = 0;
+        for (int d = 0; d < dim; ++d) {
+          const double span = hi[d] > lo[d] ? hi[d] - lo[d] : 1.0;
+          uint64_t q = (uint64_t)std::min(65535.0, std::max(0.0, (test[(size_t)k * dim + d] - lo[d]) / span * 65535.0));
+          for (int b = 0; b < 16; ++b) code |= ((q >> b) & 1ull) << (b * dim + d);
+        }
+        key[k] = code;
+        order[k] = k;
+      }
+      std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return key[a] < key[b]; });
+      for (int k = 0; k < m; ++k)
+        for (int d = 0; d < dim; ++d) tsorted[(size_t)k * dim + d] = test[(size_t)order[k] * dim + d];
+    }
     HMGP_CUDA(cudaMemcpyAsync(dz.p, z1, 8ull * n, cudaMemcpyHostToDevice, ctx->stream));
-    HMGP_CUDA(cudaMemcpyAsync(dtest.p, test, 8ull * m * dim, cudaMemcpyHostToDevice, ctx->stream));
+    HMGP_CUDA(cudaMemcpyAsync(dtest.p, tsorted.data(), 8ull * m * dim, cudaMemcpyHostToDevice, ctx->stream));
     factor_solve_dev(*f, dz.p, dw.p, true, ctx->stream);
     phase_mark(PH_BWD);
     cross_apply(ctx->stream, g->g.d_x, n, dim, dw.p, dtest.p, m,
                 make_matern(theta->sigma2, theta->ell, theta->nu, theta->tau2), dout.p);
     phase_mark(PH_CROSS);
-    HMGP_CUDA(cudaMemcpyAsync(out, dout.p, 8ull * m, cudaMemcpyDeviceToHost, ctx->stream));
+    HMGP_CUDA(cudaMemcpyAsync(osorted.data(), dout.p, 8ull * m, cudaMemcpyDeviceToHost, ctx->stream));
+    HMGP_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int k = 0; k < m; ++k) out[order[k]] = osorted[k];
     ps.finish();
     if (seconds) *seconds = now() - t0;
   })
