@@ -2175,6 +2175,7 @@ struct SStep {
 constexpr int kSolveChunk = 512;  // low-rank blocks taller than this are cut over several CTAs
 __device__ int d_solve_stats_on;
 __device__ unsigned long long d_solve_cyc[2][6];
+__device__ unsigned long long d_solve_sub[4];  // (stats) CTA 0: descriptor loads, prefetch wait, substitution, prefetch issue
 constexpr int kSolveThreads = 256;
 
 struct SolvePlan {
@@ -2437,13 +2438,23 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve_sweep(const SStep* __re
   for (int s = 0; s < nsteps; ++s) {
     const SStep st = steps[trans ? nsteps - 1 - s : s];
     if (blockIdx.x == 0) {
+      long long ts = clock64();
+      auto sub = [&](int i) {
+        if (!d_solve_stats_on || threadIdx.x != 0) return;
+        const long long now = clock64();
+        atomicAdd(&d_solve_sub[i], (unsigned long long)(now - ts));
+        ts = now;
+      };
       const LeafDev d = lf[st.dleaf];
       const bool fits = d.m <= smem_b;
+      sub(0);
       if (fits) {
         if (!prefetched) solve_prefetch_leaf(d.a, d.m, ssm);  // first step (or after a leaf that did not fit)
         solve_prefetch_wait();
       }
+      sub(1);
       solve_trsv_cta(d.a, d.m, v + st.base, trans, ssm, fits, smem_b);
+      sub(2);
       prefetched = false;
       if (s + 1 < nsteps) {  // the next diagonal leaf streams in while the grid applies this step's blocks
         const LeafDev nx = lf[steps[trans ? nsteps - 2 - s : s + 1].dleaf];
@@ -2452,6 +2463,7 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve_sweep(const SStep* __re
           prefetched = true;
         }
       }
+      sub(3);
     }
     tick(0);
     grid.sync();
@@ -2517,6 +2529,13 @@ static void solve_sweep(const Factor& F, double* v, bool trans, cudaStream_t st)
     unsigned long long c[2][6];
     HMGP_CUDA(cudaStreamSynchronize(st));
     HMGP_CUDA(cudaMemcpyFromSymbol(c, d_solve_cyc, sizeof(c)));
+    {
+      unsigned long long sb[4], zz[4] = {0, 0, 0, 0};
+      HMGP_CUDA(cudaMemcpyFromSymbol(sb, d_solve_sub, sizeof(sb)));
+      HMGP_CUDA(cudaMemcpyToSymbol(d_solve_sub, zz, sizeof(zz)));
+      fprintf(stderr, "[hmgp] solve sweep CTA 0 (ms): descriptor loads %.2f prefetch wait %.2f substitution %.2f prefetch issue %.2f\n",
+              sb[0] / 1.965e6, sb[1] / 1.965e6, sb[2] / 1.965e6, sb[3] / 1.965e6);
+    }
     for (int b = 0; b < 2; ++b)
       fprintf(stderr,
               "[hmgp] solve sweep (%s, CTA %d of %d, ms @1.965GHz): trsv %.2f sync %.2f units %.2f sync %.2f "
