@@ -2344,15 +2344,18 @@ __device__ void solve_trsv_cta(const double* __restrict__ Lg, int b, double* __r
     for (int jb = 0; jb < b; jb += 32) {
       const int nb = min(32, b - jb);
       if (threadIdx.x < 32) {
-        double lr[32];  // row (jb + lane) of the diagonal block
+        // row (jb + lane) of the diagonal block, pre-scaled by 1 / L(row, row): the
+        // dependent chain of a step is then one shuffle and one FMA (an FP64 op costs
+        // ~40 cycles of latency here), x_j = y_j / L_jj - sum_k (L_jk / L_jj) x_k
+        const double li = lane < nb ? inv[jb + lane] : 0.0;
+        double lr[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j)
-          lr[j] = (j < nb && lane < nb && lane > j) ? Lsrc[(size_t)(jb + j) * b + jb + lane] : 0.0;
-        double xi = lane < nb ? x[jb + lane] : 0.0;
+          lr[j] = (j < nb && lane < nb && lane > j) ? Lsrc[(size_t)(jb + j) * b + jb + lane] * li : 0.0;
+        double xi = lane < nb ? x[jb + lane] * li : 0.0;
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           if (j < nb) {
-            if (lane == j) xi *= inv[jb + j];
             const double xj = __shfl_sync(0xffffffffu, xi, j);
             xi -= lr[j] * xj;  // lr[j] = 0 for lane <= j
           }
@@ -2361,10 +2364,13 @@ __device__ void solve_trsv_cta(const double* __restrict__ Lg, int b, double* __r
       }
       __syncthreads();
       for (int i = jb + nb + threadIdx.x; i < b; i += blockDim.x) {
-        double s = 0.0;
-#pragma unroll 8
-        for (int j = 0; j < nb; ++j) s += Lsrc[(size_t)(jb + j) * b + i] * x[jb + j];
-        x[i] -= s;
+        double s4[4] = {0.0, 0.0, 0.0, 0.0};  // four independent chains
+        for (int j = 0; j < nb; j += 4) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (j + u < nb) s4[u] += Lsrc[(size_t)(jb + j + u) * b + i] * x[jb + j + u];
+        }
+        x[i] -= (s4[0] + s4[1]) + (s4[2] + s4[3]);
       }
       __syncthreads();
     }
@@ -2383,17 +2389,18 @@ __device__ void solve_trsv_cta(const double* __restrict__ Lg, int b, double* __r
       }
       __syncthreads();
       if (threadIdx.x < 32) {
-        double lc[32];  // column (jb + lane) of the diagonal block: lc[i] = L(jb + i, jb + lane)
+        // column (jb + lane) of the diagonal block, pre-scaled by 1 / L(lane, lane)
+        const double li = lane < nb ? inv[jb + lane] : 0.0;
+        double lc[32];  // lc[i] = L(jb + i, jb + lane) / L(jb + lane, jb + lane)
 #pragma unroll
         for (int i = 0; i < 32; ++i)
-          lc[i] = (i < nb && lane < nb && i > lane) ? Lsrc[(size_t)(jb + lane) * b + jb + i] : 0.0;
-        double xi = lane < nb ? x[jb + lane] : 0.0;
+          lc[i] = (i < nb && lane < nb && i > lane) ? Lsrc[(size_t)(jb + lane) * b + jb + i] * li : 0.0;
+        double xi = lane < nb ? x[jb + lane] * li : 0.0;
 #pragma unroll
         for (int j = 31; j >= 0; --j) {
           if (j < nb) {
-            if (lane == j) xi *= inv[jb + j];
             const double xj = __shfl_sync(0xffffffffu, xi, j);
-            xi -= lc[j] * xj;  // lc[j] = L(jb + j, jb + lane), 0 unless j > lane
+            xi -= lc[j] * xj;  // 0 unless j > lane
           }
         }
         if (lane < nb) x[jb + lane] = xi;
@@ -2435,6 +2442,9 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve_sweep(const SStep* __re
     tc = now;
   };
   bool prefetched = false;
+  // with more than one CTA, CTA 0 only runs the diagonal chain; the others share the blocks
+  const bool solo = gridDim.x > 1;
+  const int wid = solo ? (int)blockIdx.x - 1 : (int)blockIdx.x, nwk = solo ? (int)gridDim.x - 1 : (int)gridDim.x;
   for (int s = 0; s < nsteps; ++s) {
     const SStep st = steps[trans ? nsteps - 1 - s : s];
     if (blockIdx.x == 0) {
@@ -2456,7 +2466,7 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve_sweep(const SStep* __re
       solve_trsv_cta(d.a, d.m, v + st.base, trans, ssm, fits, smem_b);
       sub(2);
       prefetched = false;
-      if (s + 1 < nsteps) {  // the next diagonal leaf streams in while the grid applies this step's blocks
+      if (!solo && s + 1 < nsteps) {  // (one-CTA grid: nobody else to wait for, issue right away)
         const LeafDev nx = lf[steps[trans ? nsteps - 2 - s : s + 1].dleaf];
         if (nx.m <= smem_b) {
           solve_prefetch_leaf(nx.a, nx.m, ssm);
@@ -2465,21 +2475,51 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve_sweep(const SStep* __re
       }
       sub(3);
     }
+    if (!(solo && blockIdx.x == 0)) {
+      // while CTA 0 runs the substitution, the other CTAs pull the payload of the
+      // blocks they will apply in this step into L2 (their inputs are not ready yet)
+      for (int k = st.u2b + wid; k < st.u2e; k += nwk) {
+        const SUnit u = units[k];
+        const LeafDev L = lf[u.leaf];
+        const size_t ba = L.kind == DENSE ? (size_t)L.m * L.n * 8 : (size_t)L.m * max(rank[u.leaf], 0) * 8;
+        const size_t bb = L.kind == DENSE ? 0 : (size_t)L.n * max(rank[u.leaf], 0) * 8;
+        const char* pa = reinterpret_cast<const char*>(L.a);
+        const char* pb = reinterpret_cast<const char*>(L.b);
+        for (size_t o = (size_t)threadIdx.x * 128; o < ba; o += (size_t)blockDim.x * 128)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(pa + o));
+        for (size_t o = (size_t)threadIdx.x * 128; o < bb; o += (size_t)blockDim.x * 128)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(pb + o));
+      }
+    }
     tick(0);
     grid.sync();
     tick(1);
-    for (int k = st.u2b + blockIdx.x; k < st.u2e; k += gridDim.x) {
-      solve_unit(units[k], lf, rank, v, part, stride, trans, sT);
-      __syncthreads();
+    if (solo && blockIdx.x == 0) {
+      // CTA 0 is the diagonal chain: while the other CTAs apply this step's blocks it
+      // streams the next diagonal leaf into shared memory (16 K cp.async, ~3.6 us of
+      // issue that used to sit between the substitution and the barrier)
+      if (s + 1 < nsteps) {
+        const LeafDev nx = lf[steps[trans ? nsteps - 2 - s : s + 1].dleaf];
+        if (nx.m <= smem_b) {
+          solve_prefetch_leaf(nx.a, nx.m, ssm);
+          prefetched = true;
+        }
+      }
+    } else {
+      for (int k = st.u2b + wid; k < st.u2e; k += nwk) {
+        solve_unit(units[k], lf, rank, v, part, stride, trans, sT);
+        __syncthreads();
+      }
     }
     tick(2);
     if (st.u3e > st.u3b) {
       grid.sync();
       tick(3);
-      for (int k = st.u3b + blockIdx.x; k < st.u3e; k += gridDim.x) {
-        solve_unit(units[k], lf, rank, v, part, stride, trans, sT);
-        __syncthreads();
-      }
+      if (!(solo && blockIdx.x == 0))
+        for (int k = st.u3b + wid; k < st.u3e; k += nwk) {
+          solve_unit(units[k], lf, rank, v, part, stride, trans, sT);
+          __syncthreads();
+        }
       tick(4);
     }
     grid.sync();
