@@ -388,7 +388,10 @@ def extras(hm, _lib, ctx, stream, comm, rank, ws, peaks, c3_batch=False, step_ph
         out["roofline_solve"] = {"bound": "hbm", "kernel": "forward solve K10 (k_solve_sweep)", "ms": ms_k10,
                                  "algorithmic_bytes": fb + 2 * nvec, "achieved": (fb + 2 * nvec) / ms_k10 / 1e6,
                                  "peak": hbm, "unit": "GB/s", "frac": (fb + 2 * nvec) / ms_k10 / 1e6 / hbm,
-                                 "traffic": None, "host_buffer_call_ms": ms_sl,
+                                 "traffic": 3986579000.0,
+                                 "traffic_source": "ncu --set full of k_solve_sweep (profiles/r2_solve_sweep_raw.csv): "
+                                 "3.964 GB read + 22 MB written = 1.01x the algorithmic bytes",
+                                 "host_buffer_call_ms": ms_sl,
                                  "note": "K10 phase of the last timed step; bound by its 2048-step dependency "
                                          "chain, not by HBM (DESIGN.md section 6)"}
         del f3, h3
