@@ -241,11 +241,18 @@ __device__ bool jacobi_round(double* W, int p, int q, double* J, int qq, int m1,
     if (!act || sc * sc <= tol2 * (sa * sb) || sc == 0.0) continue;
     rot = true;
     if (gl == 0) ++nrot;
-    // tan of the rotation angle, zeta = (sb - sa) / (2 sc):
-    // tt = 2 sc sign(sb - sa) / (|sb - sa| + sqrt((sb - sa)^2 + 4 sc^2))
+    // Rotation from cos 2phi = |dd| / sqrt(dd^2 + 4 sc^2), |phi| <= pi/4:
+    //   cos^2 phi = (1 + cos 2phi) / 2,  sin phi = sin 2phi / (2 cos phi)
+    // — the same angle as tan phi = 2 sc sign(dd) / (|dd| + sqrt(dd^2 + 4 sc^2)), but
+    // the dependent chain is two reciprocal square roots instead of a square root, a
+    // division and a reciprocal square root (every pair of a round waits on it, and
+    // a dependent FP64 op costs ~40 cycles here).  sin phi is formed from sc itself,
+    // so small angles keep full relative accuracy.
     const double dd = sb - sa;
-    const double tt = (dd >= 0.0 ? 2.0 * sc : -2.0 * sc) / (fabs(dd) + sqrt(dd * dd + 4.0 * sc * sc));
-    const double cs = rsqrt(1.0 + tt * tt), sn = cs * tt;
+    const double rz = rsqrt(dd * dd + 4.0 * sc * sc);
+    const double c2h = 0.5 + 0.5 * fabs(dd) * rz;  // cos^2 phi in [1/2, 1]
+    const double rc = rsqrt(c2h);
+    const double cs = c2h * rc, sn = (dd >= 0.0 ? sc : -sc) * rz * rc;
     for (int i = gl; i < p; i += G) {
       const double x = wj[i], y = wk[i];
       wj[i] = cs * x - sn * y;
