@@ -781,10 +781,17 @@ __global__ void __launch_bounds__(kLeafRegThreads) k_leaf_factor_reg(double* __r
       }
       if (ldl) d[base + j] = s;
     }
+    // One reciprocal (LDL) or reciprocal square root (Cholesky) of the pivot per
+    // step, shared by the trailing update and the column scaling: a division, a
+    // square root and a second division used to sit on every step's dependent chain
+    // (the owner warps of column j hold the barrier of step j + 1).  x * rsqrt(s)
+    // differs from x / sqrt(s) by at most an ulp or two.
+    const double rp = ldl ? 1.0 / s : rsqrt(s);  // 1/s  or  1/sqrt(s)
+    const double rs = ldl ? rp : rp * rp;         // 1/s
     // trailing update of the columns k > j this thread owns (rows i > j only are
     // ever read again, so the strict upper part may hold stale values)
     if (active && i > j) {
-      const double ci = cj[i] / s;
+      const double ci = cj[i] * rs;
       const int qmin = j >= g ? (j - g) / G + 1 : 0;  // first q with g + q*G > j
 #pragma unroll
       for (int q = 0; q < kLeafRegMaxK; ++q)
@@ -792,8 +799,7 @@ __global__ void __launch_bounds__(kLeafRegThreads) k_leaf_factor_reg(double* __r
     }
     // finalize column j in its owners' registers
     if (own) {
-      const double piv = ldl ? s : sqrt(s);
-      const double v = (i == j) ? (ldl ? 1.0 : piv) : (i > j ? aj / piv : 0.0);
+      const double v = (i == j) ? (ldl ? 1.0 : s * rp) : (i > j ? aj * rp : 0.0);  // s * rsqrt(s) = sqrt(s)
 #pragma unroll
       for (int q = 0; q < kLeafRegMaxK; ++q)
         if (q == qj) a[q] = v;
